@@ -1,0 +1,416 @@
+// extern "C" boundary (include/hecnn_b200.h). Each entry converts C++
+// exceptions into status codes + a thread-local message, mirroring the
+// reference's exception types: std::invalid_argument -> HECNN_EINVAL,
+// std::runtime_error (and anything else) -> HECNN_ERUNTIME.
+#include <cstring>
+#include <string>
+
+#include "engine.hpp"
+#include "hecnn_b200.h"
+
+using namespace hecnn_b200;
+
+struct hecnn_context {
+    std::unique_ptr<Context> ctx;
+};
+struct hecnn_tensor {
+    TensorPtr t;
+};
+struct hecnn_model {
+    Model m;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return HECNN_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return HECNN_EINVAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return HECNN_ERUNTIME;
+    } catch (...) {
+        g_err = "unknown error";
+        return HECNN_ERUNTIME;
+    }
+}
+
+Context& C(hecnn_context* c) {
+    if (!c || !c->ctx) throw std::invalid_argument("null context");
+    cudaSetDevice(c->ctx->device);
+    return *c->ctx;
+}
+const Context& C(const hecnn_context* c) {
+    if (!c || !c->ctx) throw std::invalid_argument("null context");
+    return *c->ctx;
+}
+const Tensor& T(const hecnn_tensor* t) {
+    if (!t || !t->t) throw std::invalid_argument("null tensor");
+    return *t->t;
+}
+hecnn_tensor* wrap(TensorPtr t) {
+    auto* h = new hecnn_tensor;
+    h->t = std::move(t);
+    return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hecnn_last_error(void) { return g_err.c_str(); }
+int hecnn_abi_version(void) { return 1; }
+
+int hecnn_find_chain(size_t n, const int* prime_bits, size_t count, uint64_t* primes_out) {
+    return guard([&] {
+        std::vector<u64> c = make_chain(n, std::vector<int>(prime_bits, prime_bits + count));
+        std::memcpy(primes_out, c.data(), c.size() * 8);
+    });
+}
+
+int hecnn_context_create(size_t n, const uint64_t* primes, size_t nprimes, double scale, double sigma,
+                         int degenerate_noise, int device, hecnn_context** out) {
+    return guard([&] {
+        auto h = std::make_unique<hecnn_context>();
+        h->ctx = std::make_unique<Context>(n, std::vector<u64>(primes, primes + nprimes), scale, sigma,
+                                           degenerate_noise != 0, device);
+        *out = h.release();
+    });
+}
+
+int hecnn_context_destroy(hecnn_context* ctx) {
+    return guard([&] { delete ctx; });
+}
+
+int hecnn_context_set_stream(hecnn_context* ctx, void* stream) {
+    return guard([&] {
+        Context& c = C(ctx);
+        c.sync();
+        if (c.own_stream) cudaStreamDestroy(c.stream);
+        c.own_stream = false;
+        c.stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int hecnn_context_synchronize(hecnn_context* ctx) {
+    return guard([&] { C(ctx).sync(); });
+}
+
+int hecnn_context_info(const hecnn_context* ctx, size_t* n, size_t* top_level, double* scale) {
+    return guard([&] {
+        const Context& c = C(ctx);
+        if (n) *n = c.n();
+        if (top_level) *top_level = c.top();
+        if (scale) *scale = c.scale;
+    });
+}
+
+int hecnn_relin_digits(const hecnn_context* ctx, size_t level, size_t* digits) {
+    return guard([&] {
+        const Context& c = C(ctx);
+        if (level > c.top()) throw std::invalid_argument("relin_digits: level out of range");
+        *digits = c.ring.relin_digits(level);
+    });
+}
+
+int hecnn_launch_count(const hecnn_context* ctx, uint64_t* launches) {
+    return guard([&] { *launches = C(ctx).launches; });
+}
+
+int hecnn_keygen(hecnn_context* ctx, uint64_t seed) {
+    return guard([&] { keygen(C(ctx), seed); });
+}
+
+int hecnn_import_keys(hecnn_context* ctx, const uint64_t* secret, const uint64_t* pk_b, const uint64_t* pk_a,
+                      const uint64_t* evk, size_t evk_digits) {
+    return guard([&] { import_keys(C(ctx), secret, pk_b, pk_a, evk, evk_digits); });
+}
+
+int hecnn_export_secret_key(const hecnn_context* ctx, uint64_t* secret) {
+    return guard([&] {
+        const Context& c = C(ctx);
+        if (!c.has_secret) throw std::invalid_argument("no secret key");
+        std::memcpy(secret, c.secret_host.data(), c.secret_host.size() * 8);
+    });
+}
+
+int hecnn_export_public_key(const hecnn_context* ctx, uint64_t* pk_b, uint64_t* pk_a) {
+    return guard([&] {
+        Context& c = *const_cast<hecnn_context*>(ctx)->ctx;
+        if (!c.has_pk) throw std::invalid_argument("no public key");
+        const std::size_t poly = (c.top() + 1) * c.n() * 8;
+        c.download(pk_b, c.pk.get(), poly);
+        c.download(pk_a, c.pk.as<u64>() + poly / 8, poly);
+    });
+}
+
+int hecnn_eval_key_digits(const hecnn_context* ctx, size_t* digits) {
+    return guard([&] { *digits = C(ctx).evk_digits; });
+}
+
+int hecnn_export_eval_key(const hecnn_context* ctx, uint64_t* evk) {
+    return guard([&] {
+        Context& c = *const_cast<hecnn_context*>(ctx)->ctx;
+        if (!c.evk_digits) throw std::invalid_argument("no evaluation key");
+        c.download(evk, c.evk.get(), c.evk.bytes());
+    });
+}
+
+int hecnn_device_alloc(hecnn_context* ctx, size_t bytes, void** dptr) {
+    return guard([&] {
+        Context& c = C(ctx);
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
+        (void)c;
+        *dptr = p;
+    });
+}
+
+int hecnn_device_free(hecnn_context* ctx, void* dptr) {
+    return guard([&] {
+        C(ctx).sync();
+        cudaFree(dptr);
+    });
+}
+
+int hecnn_memcpy_h2d(hecnn_context* ctx, void* dst, const void* src, size_t bytes) {
+    return guard([&] { C(ctx).upload(dst, src, bytes); });
+}
+
+int hecnn_memcpy_d2h(hecnn_context* ctx, void* dst, const void* src, size_t bytes) {
+    return guard([&] { C(ctx).download(dst, src, bytes); });
+}
+
+int hecnn_ntt_forward(hecnn_context* ctx, uint64_t* polys, size_t level, size_t count) {
+    return guard([&] {
+        Context& c = C(ctx);
+        if (level > c.top()) throw std::invalid_argument("ntt_transform: level out of range");
+        ntt_forward(c.dev, polys, static_cast<int>(level), count, c.L());
+    });
+}
+
+int hecnn_ntt_inverse(hecnn_context* ctx, uint64_t* polys, size_t level, size_t count) {
+    return guard([&] {
+        Context& c = C(ctx);
+        if (level > c.top()) throw std::invalid_argument("ntt_transform: level out of range");
+        ntt_inverse(c.dev, polys, static_cast<int>(level), count, c.L());
+    });
+}
+
+static int ew(hecnn_context* ctx, EwOp op, const uint64_t* a, const uint64_t* b, uint64_t* out, size_t level,
+              size_t count) {
+    return guard([&] {
+        Context& c = C(ctx);
+        if (level > c.top()) throw std::invalid_argument("ring op: level out of range");
+        poly_elementwise(c.dev, op, a, b, out, static_cast<int>(level), count, c.L());
+    });
+}
+
+int hecnn_poly_add(hecnn_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, size_t level, size_t count) {
+    return ew(ctx, EwOp::Add, a, b, out, level, count);
+}
+int hecnn_poly_sub(hecnn_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, size_t level, size_t count) {
+    return ew(ctx, EwOp::Sub, a, b, out, level, count);
+}
+int hecnn_poly_neg(hecnn_context* ctx, const uint64_t* a, uint64_t* out, size_t level, size_t count) {
+    return ew(ctx, EwOp::Neg, a, nullptr, out, level, count);
+}
+int hecnn_poly_pointwise_mul(hecnn_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, size_t level,
+                             size_t count) {
+    return ew(ctx, EwOp::Mul, a, b, out, level, count);
+}
+int hecnn_poly_pointwise_mac(hecnn_context* ctx, uint64_t* acc, const uint64_t* a, const uint64_t* b, size_t level,
+                             size_t count) {
+    return ew(ctx, EwOp::Mac, a, b, acc, level, count);
+}
+
+int hecnn_rescale_poly(hecnn_context* ctx, const uint64_t* in, uint64_t* out, size_t level, size_t count) {
+    return guard([&] {
+        Context& c = C(ctx);
+        if (level == 0) throw std::invalid_argument("rescale_poly: already at last level");
+        if (level > c.top()) throw std::invalid_argument("rescale_poly: level out of range");
+        rescale(c.dev, in, out, static_cast<int>(level), count, c.L());
+    });
+}
+
+int hecnn_key_switch(hecnn_context* ctx, const uint64_t* d2, uint64_t* out, size_t level, size_t count) {
+    return guard([&] {
+        Context& c = C(ctx);
+        if (level > c.top()) throw std::invalid_argument("key_switch: level out of range");
+        key_switch_raw(c, d2, out, level, count);
+    });
+}
+
+int hecnn_tensor_create(hecnn_context* ctx, size_t cells, uint32_t level, double scale, hecnn_tensor** out) {
+    return guard([&] {
+        Context& c = C(ctx);
+        if (level > c.top()) throw std::invalid_argument("tensor: level out of range");
+        *out = wrap(make_tensor(c, cells, level, scale));
+    });
+}
+
+int hecnn_tensor_destroy(hecnn_tensor* t) {
+    return guard([&] {
+        if (t && t->t) cudaSetDevice(t->t->ctx->device);
+        delete t;
+    });
+}
+
+int hecnn_tensor_info(const hecnn_tensor* t, size_t* cells, uint32_t* level, double* scale) {
+    return guard([&] {
+        const Tensor& x = T(t);
+        if (cells) *cells = x.cells;
+        if (level) *level = x.level;
+        if (scale) *scale = x.scale;
+    });
+}
+
+int hecnn_tensor_set_shape(hecnn_tensor* t, int flat, size_t h, size_t w, size_t c, size_t batch) {
+    return guard([&] {
+        Tensor& x = *t->t;
+        Shape s = flat ? Shape::flattened(h) : Shape::spatial(h, w, c);
+        if (s.positions() != x.cells) throw std::invalid_argument("tensor: shape does not match the cell count");
+        x.shape = s;
+        x.batch = batch;
+    });
+}
+
+int hecnn_tensor_shape(const hecnn_tensor* t, int* flat, size_t* h, size_t* w, size_t* c, size_t* batch) {
+    return guard([&] {
+        const Tensor& x = T(t);
+        *flat = x.shape.flat ? 1 : 0;
+        *h = x.shape.flat ? x.shape.feat : x.shape.h;
+        *w = x.shape.w;
+        *c = x.shape.c;
+        *batch = x.batch;
+    });
+}
+
+int hecnn_tensor_data(const hecnn_tensor* t, uint64_t** dptr) {
+    return guard([&] { *dptr = T(t).data(); });
+}
+
+int hecnn_tensor_upload(hecnn_context* ctx, hecnn_tensor* t, const uint64_t* host) {
+    return guard([&] { C(ctx).upload(t->t->data(), host, t->t->cells * t->t->cell_words() * 8); });
+}
+
+int hecnn_tensor_download(hecnn_context* ctx, const hecnn_tensor* t, uint64_t* host) {
+    return guard([&] { C(ctx).download(host, T(t).data(), T(t).cells * T(t).cell_words() * 8); });
+}
+
+int hecnn_encrypt_tensor(hecnn_context* ctx, const double* data, size_t batch, size_t positions, uint64_t seed,
+                         hecnn_tensor** out) {
+    return guard([&] { *out = wrap(encrypt_tensor(C(ctx), data, batch, positions, seed)); });
+}
+
+int hecnn_encrypt_raw(hecnn_context* ctx, const uint64_t* m, const int64_t* r, const int64_t* e0, const int64_t* e1,
+                      size_t count, double scale, hecnn_tensor** out) {
+    return guard([&] {
+        *out = wrap(encrypt_raw(C(ctx), m, reinterpret_cast<const long long*>(r),
+                                reinterpret_cast<const long long*>(e0), reinterpret_cast<const long long*>(e1), count,
+                                scale));
+    });
+}
+
+int hecnn_decrypt_raw(hecnn_context* ctx, const hecnn_tensor* t, uint64_t* out_host) {
+    return guard([&] { decrypt_raw(C(ctx), T(t), out_host); });
+}
+
+int hecnn_decrypt_tensor(hecnn_context* ctx, const hecnn_tensor* t, size_t batch, double* out) {
+    return guard([&] { decrypt_tensor(C(ctx), T(t), batch, out); });
+}
+
+int hecnn_ct_add(hecnn_context* ctx, const hecnn_tensor* x, const hecnn_tensor* y, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ct_add(C(ctx), T(x), T(y), false)); });
+}
+int hecnn_ct_sub(hecnn_context* ctx, const hecnn_tensor* x, const hecnn_tensor* y, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ct_add(C(ctx), T(x), T(y), true)); });
+}
+int hecnn_ct_mul(hecnn_context* ctx, const hecnn_tensor* x, const hecnn_tensor* y, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ct_mul(C(ctx), T(x), T(y))); });
+}
+int hecnn_ct_square(hecnn_context* ctx, const hecnn_tensor* x, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ct_square(C(ctx), T(x))); });
+}
+int hecnn_ct_rescale(hecnn_context* ctx, const hecnn_tensor* x, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ct_rescale(C(ctx), T(x))); });
+}
+int hecnn_ct_mod_switch(hecnn_context* ctx, const hecnn_tensor* x, uint32_t to_level, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ct_mod_switch(C(ctx), T(x), to_level)); });
+}
+int hecnn_ct_mul_const(hecnn_context* ctx, const hecnn_tensor* x, double c, double scale, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ct_mul_const(C(ctx), T(x), c, scale)); });
+}
+int hecnn_ct_add_const(hecnn_context* ctx, const hecnn_tensor* x, double c, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ct_add_const(C(ctx), T(x), c)); });
+}
+
+int hecnn_eval_activation(hecnn_context* ctx, const double* coefficients, size_t n_coefficients, double interval_bound,
+                          const hecnn_tensor* x, hecnn_tensor** out) {
+    return guard([&] {
+        Activation a{std::vector<double>(coefficients, coefficients + n_coefficients), interval_bound};
+        *out = wrap(eval_activation(C(ctx), a, T(x)));
+    });
+}
+
+int hecnn_model_create(hecnn_context* ctx, const hecnn_model_desc* d, hecnn_model** out) {
+    return guard([&] {
+        (void)C(ctx);
+        auto h = std::make_unique<hecnn_model>();
+        Model& m = h->m;
+        m.input = d->input_flat ? Shape::flattened(d->input_features)
+                                : Shape::spatial(d->input_h, d->input_w, d->input_c);
+        for (size_t a = 0; a < d->n_activations; ++a) {
+            Activation act;
+            act.coefficients.assign(d->activations[a].coefficients,
+                                    d->activations[a].coefficients + d->activations[a].n_coefficients);
+            act.interval_bound = d->activations[a].interval_bound;
+            m.acts.push_back(act);
+        }
+        for (size_t i = 0; i < d->n_layers; ++i) {
+            const hecnn_layer_desc& L = d->layers[i];
+            Layer l;
+            l.kind = L.kind;
+            if (l.kind < 0 || l.kind > 5) throw std::invalid_argument("model: unknown layer kind");
+            l.filters = static_cast<size_t>(L.filters);
+            l.kh = static_cast<size_t>(L.kernel_h);
+            l.kw = static_cast<size_t>(L.kernel_w);
+            l.stride = static_cast<size_t>(L.stride);
+            l.valid = L.padding_valid != 0;
+            l.pool = static_cast<size_t>(L.pool);
+            l.pad = static_cast<size_t>(L.pad);
+            l.units = static_cast<size_t>(L.units);
+            l.act = L.activation;
+            if (L.weights) l.w.assign(L.weights, L.weights + L.n_weights);
+            if (L.biases) l.b.assign(L.biases, L.biases + L.n_biases);
+            m.layers.push_back(std::move(l));
+        }
+        *out = h.release();
+    });
+}
+
+int hecnn_model_destroy(hecnn_model* m) {
+    return guard([&] { delete m; });
+}
+
+int hecnn_model_depth_cost(const hecnn_model* m, size_t* cost) {
+    return guard([&] {
+        const_cast<hecnn_model*>(m)->m.infer_shapes();
+        *cost = m->m.depth_cost();
+    });
+}
+
+int hecnn_forward_encrypted(hecnn_context* ctx, const hecnn_model* m, const hecnn_tensor* x, uint64_t seed,
+                            hecnn_tensor** out, double* layer_seconds) {
+    return guard([&] {
+        *out = wrap(forward_encrypted(C(ctx), const_cast<hecnn_model*>(m)->m, T(x), seed, layer_seconds));
+    });
+}
+
+}  // extern "C"

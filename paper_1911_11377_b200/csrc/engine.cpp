@@ -1,0 +1,932 @@
+// Device-resident CKKS engine (see engine.hpp).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <sstream>
+#include <stdexcept>
+#include <thread>
+#include <tuple>
+
+namespace hecnn_b200 {
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+// Scratch budget per batched scheme op; chunks of ciphertexts are sized to it.
+constexpr std::size_t kScratchBytes = std::size_t(3) << 30;
+
+unsigned host_threads() {
+    unsigned t = std::thread::hardware_concurrency();
+    return t ? std::min(t, 64u) : 4u;
+}
+
+// Disjoint-output parallel loop for host-side sampling (results do not
+// depend on the chunking: every item owns its seed and output slot).
+void parallel_items(std::size_t count, const std::function<void(std::size_t)>& fn) {
+    unsigned workers = static_cast<unsigned>(std::min<std::size_t>(host_threads(), count));
+    if (workers <= 1) {
+        for (std::size_t i = 0; i < count; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    std::size_t chunk = (count + workers - 1) / workers;
+    for (unsigned w = 0; w < workers; ++w) {
+        std::size_t b = w * chunk, e = std::min(count, b + chunk);
+        if (b >= e) break;
+        pool.emplace_back([&fn, b, e] {
+            for (std::size_t i = b; i < e; ++i) fn(i);
+        });
+    }
+    for (auto& t : pool) t.join();
+}
+
+std::vector<ulonglong2> with_shoup(const RingTables& R, const std::vector<u64>& res) {
+    std::vector<ulonglong2> out(res.size());
+    for (std::size_t i = 0; i < res.size(); ++i) out[i] = make_ulonglong2(res[i], shoup_of(res[i], R.primes[i]));
+    return out;
+}
+
+void require_scale_match(double sx, double sy, const char* op) {
+    double m = std::max(std::abs(sx), std::abs(sy));
+    if (std::abs(sx - sy) > 0x1p-30 * m)
+        throw std::invalid_argument(std::string(op) + ": scale mismatch (no silent alignment)");
+}
+
+void check_scale_headroom(const Context& C, double sx, double sy, std::size_t level) {
+    if (std::log2(sx) + std::log2(sy) >= C.ring.log2_mod[level] - 1.0)
+        throw std::invalid_argument("mul: scale overflow for the active modulus");
+}
+
+std::vector<long long> sample_error(const Context& C, u64 seed) {
+    if (C.degenerate || C.sigma == 0.0) return std::vector<long long>(C.n(), 0);
+    return sample_gaussian(C.n(), C.sigma, seed);
+}
+
+std::vector<long long> sample_secretish(const Context& C, double density, u64 seed) {
+    if (C.degenerate) return std::vector<long long>(C.n(), 0);
+    return sample_ternary(C.n(), density, seed);
+}
+
+void to_int8(const std::vector<long long>& v, signed char* out) {
+    for (std::size_t i = 0; i < v.size(); ++i) {
+        if (v[i] < -127 || v[i] > 127)
+            throw std::invalid_argument("encrypt: noise coefficient outside the device sampler's int8 range");
+        out[i] = static_cast<signed char>(v[i]);
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- memory
+
+DevBuf::DevBuf(Context* ctx, std::size_t bytes) : ctx_(ctx), bytes_(bytes) {
+    if (bytes) cuda_check(cudaMallocAsync(&ptr_, bytes, ctx->stream), "cudaMallocAsync");
+}
+
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+        reset();
+        ctx_ = o.ctx_;
+        ptr_ = o.ptr_;
+        bytes_ = o.bytes_;
+        o.ptr_ = nullptr;
+        o.bytes_ = 0;
+    }
+    return *this;
+}
+
+void DevBuf::reset() {
+    if (ptr_) cudaFreeAsync(ptr_, ctx_->stream);
+    ptr_ = nullptr;
+    bytes_ = 0;
+}
+
+std::string Shape::str() const {
+    std::ostringstream os;
+    if (flat) os << "(" << feat << ")";
+    else os << "(" << h << "x" << w << "x" << c << ")";
+    return os.str();
+}
+
+// ---------------------------------------------------------------- context
+
+Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, double sg, bool degen, int dev_id)
+    : device(dev_id), scale(sc), sigma(sg), degenerate(degen) {
+    validate_chain(n, primes);  // RingContext ctor (ring.hpp:173-175)
+    if (!(scale > 1.0)) throw std::invalid_argument("CkksParams: scale must be > 1");
+    if (sigma < 0.0) throw std::invalid_argument("CkksParams: sigma must be >= 0");
+    ring.build(n, primes);
+    enc = std::make_unique<Encoder>(ring, scale);
+
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    own_stream = true;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        std::uint64_t keep = ~std::uint64_t(0);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+
+    std::vector<ModConst> mods;
+    for (const auto& m : ring.mods) mods.push_back(ModConst{m.q, 2 * m.q, m.ratio_lo, m.ratio_hi});
+    std::vector<double> inv_q;
+    for (u64 q : ring.primes) inv_q.push_back(1.0 / static_cast<double>(q));
+
+    tables.push_back(upload_vec(mods));
+    dev.mod = tables.back().as<ModConst>();
+    tables.push_back(upload_vec(ring.fwd));
+    dev.fwd = tables.back().as<ulonglong2>();
+    tables.push_back(upload_vec(ring.inv));
+    dev.inv = tables.back().as<ulonglong2>();
+    tables.push_back(upload_vec(ring.n_inv));
+    dev.n_inv = tables.back().as<ulonglong2>();
+    tables.push_back(upload_vec(ring.inv_dropped));
+    dev.inv_dropped = tables.back().as<ulonglong2>();
+    tables.push_back(upload_vec(ring.p_mod));
+    dev.p_mod = tables.back().as<u64>();
+    tables.push_back(upload_vec(ring.punct_inv));
+    dev.punct_inv = tables.back().as<ulonglong2>();
+    tables.push_back(upload_vec(ring.punct));
+    dev.punct = tables.back().as<u64>();
+    tables.push_back(upload_vec(ring.modulus));
+    dev.modulus = tables.back().as<u64>();
+    tables.push_back(upload_vec(inv_q));
+    dev.inv_q = tables.back().as<double>();
+    dev.n = static_cast<int>(ring.n);
+    dev.logn = static_cast<int>(ring.logn);
+    dev.limbs = static_cast<int>(ring.limbs);
+    dev.crt_words = static_cast<int>(ring.crt_words);
+    sync();
+}
+
+Context::~Context() {
+    cudaSetDevice(device);
+    s_ntt.reset();
+    pk.reset();
+    evk.reset();
+    evk_sh.reset();
+    tables.clear();
+    cudaStreamSynchronize(stream);
+    if (own_stream) cudaStreamDestroy(stream);
+}
+
+void Context::upload(void* dst, const void* src, std::size_t bytes) {
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream), "cudaMemcpyAsync H2D");
+    // pageable source: the copy has been staged when the call returns, but keep the
+    // host buffer's lifetime rule simple for callers by synchronizing here
+    cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+}
+
+void Context::download(void* dst, const void* src, std::size_t bytes) {
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream), "cudaMemcpyAsync D2H");
+    cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+}
+
+void Context::sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+
+TensorPtr make_tensor(Context& C, std::size_t cells, std::uint32_t level, double scale) {
+    auto t = std::make_unique<Tensor>();
+    t->ctx = &C;
+    t->cells = cells;
+    t->level = level;
+    t->scale = scale;
+    t->shape = Shape::flattened(cells);
+    t->buf = DevBuf(&C, cells * 2 * (level + 1) * C.n() * sizeof(u64));
+    return t;
+}
+
+// ---------------------------------------------------------------- keys
+
+// CkksEngine::keygen (ckks.hpp:200-236): host randomness, device arithmetic.
+void keygen(Context& C, u64 seed) {
+    const std::size_t n = C.n(), top = C.top(), limbs = top + 1, poly = limbs * n;
+    Launch L = C.L();
+    auto residues_of = [&](const std::vector<long long>& c) {
+        std::vector<u64> r(poly);
+        for (std::size_t i = 0; i < limbs; ++i)
+            for (std::size_t j = 0; j < n; ++j) r[i * n + j] = C.ring.mods[i].from_signed(c[j]);
+        return r;
+    };
+    std::vector<long long> s = sample_secretish(C, 2.0 / 3.0, derive_seed(seed, 0x5ec0));
+    C.secret_host = residues_of(s);
+    C.s_ntt = C.upload_vec(C.secret_host);
+    ntt_forward(C.dev, C.s_ntt.as<u64>(), static_cast<int>(top), 1, L);
+
+    // public key
+    DevBuf a = C.upload_vec(sample_uniform(C.ring, top, derive_seed(seed, 0xa0a0)));
+    ntt_forward(C.dev, a.as<u64>(), static_cast<int>(top), 1, L);
+    DevBuf e = C.upload_vec(residues_of(sample_error(C, derive_seed(seed, 0xe000))));
+    ntt_forward(C.dev, e.as<u64>(), static_cast<int>(top), 1, L);
+    C.pk = DevBuf(&C, 2 * poly * sizeof(u64));
+    u64* pkb = C.pk.as<u64>();
+    u64* pka = pkb + poly;
+    poly_elementwise(C.dev, EwOp::Mul, a.as<u64>(), C.s_ntt.as<u64>(), pkb, static_cast<int>(top), 1, L);
+    poly_elementwise(C.dev, EwOp::Neg, pkb, nullptr, pkb, static_cast<int>(top), 1, L);
+    poly_elementwise(C.dev, EwOp::Add, pkb, e.as<u64>(), pkb, static_cast<int>(top), 1, L);
+    cuda_check(cudaMemcpyAsync(pka, a.get(), poly * sizeof(u64), cudaMemcpyDeviceToDevice, C.stream), "copy pk.a");
+
+    // evaluation key: b_t = -a_t s + e_t + 2^{20 t} s^2 (NTT domain, top level)
+    const std::size_t D = C.ring.relin_digits(top);
+    DevBuf s2(&C, poly * sizeof(u64));
+    poly_elementwise(C.dev, EwOp::Mul, C.s_ntt.as<u64>(), C.s_ntt.as<u64>(), s2.as<u64>(), static_cast<int>(top), 1, L);
+    std::vector<std::vector<u64>> at(D), et(D);
+    parallel_items(D, [&](std::size_t t) {
+        at[t] = sample_uniform(C.ring, top, derive_seed(seed, 0xeb00 + 2 * t));
+        et[t] = residues_of(sample_error(C, derive_seed(seed, 0xeb01 + 2 * t)));
+    });
+    C.evk = DevBuf(&C, D * 2 * poly * sizeof(u64));
+    C.evk_sh = DevBuf(&C, D * 2 * poly * sizeof(u64));
+    DevBuf et_dev(&C, poly * sizeof(u64));
+    DevBuf consts(&C, limbs * sizeof(ulonglong2));
+    for (std::size_t t = 0; t < D; ++t) {
+        u64* bt = C.evk.as<u64>() + (2 * t) * poly;
+        u64* a_t = bt + poly;
+        C.upload(a_t, at[t].data(), poly * sizeof(u64));
+        ntt_forward(C.dev, a_t, static_cast<int>(top), 1, L);
+        C.upload(et_dev.get(), et[t].data(), poly * sizeof(u64));
+        ntt_forward(C.dev, et_dev.as<u64>(), static_cast<int>(top), 1, L);
+        poly_elementwise(C.dev, EwOp::Mul, a_t, C.s_ntt.as<u64>(), bt, static_cast<int>(top), 1, L);
+        poly_elementwise(C.dev, EwOp::Neg, bt, nullptr, bt, static_cast<int>(top), 1, L);
+        poly_elementwise(C.dev, EwOp::Add, bt, et_dev.as<u64>(), bt, static_cast<int>(top), 1, L);
+        std::vector<u64> f(limbs);
+        for (std::size_t i = 0; i < limbs; ++i) f[i] = C.ring.mods[i].pow(2, 20 * t);
+        std::vector<ulonglong2> fc = with_shoup(C.ring, f);
+        C.upload(consts.get(), fc.data(), limbs * sizeof(ulonglong2));
+        scalar_mul(C.dev, s2.as<u64>(), consts.as<ulonglong2>(), et_dev.as<u64>(), static_cast<int>(top), 1, L);
+        poly_elementwise(C.dev, EwOp::Add, bt, et_dev.as<u64>(), bt, static_cast<int>(top), 1, L);
+    }
+    shoup_table(C.dev, C.evk.as<u64>(), C.evk_sh.as<u64>(), static_cast<int>(limbs), 2 * D, L);
+    C.evk_digits = D;
+    C.has_secret = C.has_pk = true;
+    C.sync();
+}
+
+void import_keys(Context& C, const u64* secret, const u64* pk_b, const u64* pk_a, const u64* evk, std::size_t digits) {
+    const std::size_t poly = (C.top() + 1) * C.n();
+    Launch L = C.L();
+    if (secret) {
+        C.secret_host.assign(secret, secret + poly);
+        C.s_ntt = C.upload_vec(C.secret_host);
+        ntt_forward(C.dev, C.s_ntt.as<u64>(), static_cast<int>(C.top()), 1, L);
+        C.has_secret = true;
+    }
+    if (pk_b && pk_a) {
+        C.pk = DevBuf(&C, 2 * poly * sizeof(u64));
+        C.upload(C.pk.get(), pk_b, poly * sizeof(u64));
+        C.upload(C.pk.as<u64>() + poly, pk_a, poly * sizeof(u64));
+        C.has_pk = true;
+    }
+    if (evk && digits) {
+        C.evk = DevBuf(&C, digits * 2 * poly * sizeof(u64));
+        C.evk_sh = DevBuf(&C, digits * 2 * poly * sizeof(u64));
+        C.upload(C.evk.get(), evk, digits * 2 * poly * sizeof(u64));
+        shoup_table(C.dev, C.evk.as<u64>(), C.evk_sh.as<u64>(), static_cast<int>(C.top() + 1), 2 * digits, L);
+        C.evk_digits = digits;
+    }
+    C.sync();
+}
+
+// ---------------------------------------------------------------- scheme ops
+
+TensorPtr ct_add(Context& C, const Tensor& x, const Tensor& y, bool subtract) {
+    const char* op = subtract ? "sub" : "add";
+    if (x.level != y.level)
+        throw std::invalid_argument(std::string(op) + ": level mismatch (use rescale/mod_switch first)");
+    require_scale_match(x.scale, y.scale, op);
+    if (x.cells != y.cells) throw std::invalid_argument(std::string(op) + ": cell count mismatch");
+    TensorPtr out = make_tensor(C, x.cells, x.level, x.scale);
+    out->shape = x.shape;
+    out->batch = x.batch;
+    poly_elementwise(C.dev, subtract ? EwOp::Sub : EwOp::Add, x.data(), y.data(), out->data(),
+                     static_cast<int>(x.level), 2 * x.cells, C.L());
+    return out;
+}
+
+void key_switch_raw(Context& C, const u64* d2, u64* out, std::size_t level, std::size_t count) {
+    if (!C.evk_digits) throw std::invalid_argument("mul: empty evaluation key");
+    const std::size_t D = C.ring.relin_digits(level);
+    if (D > C.evk_digits) throw std::invalid_argument("mul: evaluation key too short for level");
+    const std::size_t n = C.n(), limbs = level + 1;
+    Launch L = C.L();
+    DevBuf tmp(&C, count * limbs * n * sizeof(u64));
+    DevBuf dig(&C, count * D * n * sizeof(u32));
+    cuda_check(cudaMemcpyAsync(tmp.get(), d2, count * limbs * n * sizeof(u64), cudaMemcpyDeviceToDevice, C.stream), "copy");
+    crt_digits(C.dev, tmp.as<u64>(), dig.as<u32>(), static_cast<int>(level), static_cast<int>(D), count, L);
+    cuda_check(cudaMemsetAsync(out, 0, count * 2 * limbs * n * sizeof(u64), C.stream), "memset");
+    keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), out, static_cast<int>(level),
+                  static_cast<int>(D), count, L);
+}
+
+// mul / square (ckks.hpp:315-369): tensor -> INTT(d2) -> key switch -> INTT -> rescale.
+static TensorPtr relin_product(Context& C, const Tensor& x, const Tensor* y) {
+    const bool sq = y == nullptr;
+    if (!sq) {
+        if (x.level != y->level) throw std::invalid_argument("mul: level mismatch (use rescale/mod_switch first)");
+        if (x.cells != y->cells) throw std::invalid_argument("mul: cell count mismatch");
+    }
+    if (x.level == 0) throw std::invalid_argument("mul: at last level, no room to rescale");
+    const double sy = sq ? x.scale : y->scale;
+    check_scale_headroom(C, x.scale, sy, x.level);
+    if (!C.evk_digits) throw std::invalid_argument("mul: empty evaluation key");
+    const std::size_t l = x.level, n = C.n(), limbs = l + 1;
+    const std::size_t D = C.ring.relin_digits(l);
+    if (D > C.evk_digits) throw std::invalid_argument("mul: evaluation key too short for level");
+
+    TensorPtr out = make_tensor(C, x.cells, static_cast<std::uint32_t>(l - 1),
+                                x.scale * sy / static_cast<double>(C.ring.primes[l]));
+    out->shape = x.shape;
+    out->batch = x.batch;
+    const std::size_t cw = 2 * limbs * n;
+    const std::size_t per_ct = (sq ? 1 : 2) * cw * 8 + limbs * n * 8 + D * n * 4;
+    const std::size_t chunk = std::max<std::size_t>(1, std::min(x.cells, kScratchBytes / per_ct));
+    DevBuf d01(&C, chunk * cw * 8), fy(&C, sq ? 0 : chunk * cw * 8), d2(&C, chunk * limbs * n * 8),
+        dig(&C, chunk * D * n * 4);
+    Launch L = C.L();
+    const int lv = static_cast<int>(l);
+    for (std::size_t c0 = 0; c0 < x.cells; c0 += chunk) {
+        const std::size_t m = std::min(chunk, x.cells - c0);
+        cuda_check(cudaMemcpyAsync(d01.get(), x.cell(c0), m * cw * 8, cudaMemcpyDeviceToDevice, C.stream), "copy x");
+        ntt_forward(C.dev, d01.as<u64>(), lv, 2 * m, L);
+        if (sq) {
+            tensor_square(C.dev, d01.as<u64>(), d01.as<u64>(), d2.as<u64>(), lv, m, L);
+        } else {
+            cuda_check(cudaMemcpyAsync(fy.get(), y->cell(c0), m * cw * 8, cudaMemcpyDeviceToDevice, C.stream), "copy y");
+            ntt_forward(C.dev, fy.as<u64>(), lv, 2 * m, L);
+            tensor_mul(C.dev, d01.as<u64>(), fy.as<u64>(), d01.as<u64>(), d2.as<u64>(), lv, m, L);
+        }
+        ntt_inverse(C.dev, d2.as<u64>(), lv, m, L);
+        crt_digits(C.dev, d2.as<u64>(), dig.as<u32>(), lv, static_cast<int>(D), m, L);
+        keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), d01.as<u64>(), lv,
+                      static_cast<int>(D), m, L);
+        ntt_inverse(C.dev, d01.as<u64>(), lv, 2 * m, L);
+        rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L);
+    }
+    return out;
+}
+
+TensorPtr ct_mul(Context& C, const Tensor& x, const Tensor& y) { return relin_product(C, x, &y); }
+TensorPtr ct_square(Context& C, const Tensor& x) { return relin_product(C, x, nullptr); }
+
+TensorPtr ct_rescale(Context& C, const Tensor& x) {
+    if (x.level == 0) throw std::invalid_argument("rescale: no level headroom");
+    TensorPtr out = make_tensor(C, x.cells, x.level - 1, x.scale / static_cast<double>(C.ring.primes[x.level]));
+    out->shape = x.shape;
+    out->batch = x.batch;
+    rescale(C.dev, x.data(), out->data(), static_cast<int>(x.level), 2 * x.cells, C.L());
+    return out;
+}
+
+TensorPtr ct_mod_switch(Context& C, const Tensor& x, std::uint32_t to_level) {
+    if (to_level > x.level) throw std::invalid_argument("mod_switch: cannot raise level");
+    TensorPtr out = make_tensor(C, x.cells, to_level, x.scale);
+    out->shape = x.shape;
+    out->batch = x.batch;
+    if (to_level == x.level)
+        cuda_check(cudaMemcpyAsync(out->data(), x.data(), x.cells * x.cell_words() * 8, cudaMemcpyDeviceToDevice, C.stream),
+                   "copy");
+    else
+        drop_limbs(C.dev, x.data(), out->data(), static_cast<int>(x.level), static_cast<int>(to_level), 2 * x.cells, C.L());
+    return out;
+}
+
+// mul_plain(x, encode_const(c, scale, x.level)) (ckks.hpp:395-398, 372-382, 588-597)
+TensorPtr ct_mul_const(Context& C, const Tensor& x, double c, double scale) {
+    C.enc->check_encode(1, std::abs(c), scale, x.level);
+    std::vector<u64> res =
+        C.enc->residues_of_rounded(roundl(static_cast<long double>(c) * static_cast<long double>(scale)), x.level);
+    if (x.level == 0) throw std::invalid_argument("mul_plain: at last level, no room to rescale");
+    check_scale_headroom(C, x.scale, scale, x.level);
+    std::vector<ulonglong2> consts = with_shoup(C.ring, res);
+    DevBuf dc = C.upload_vec(consts);
+    DevBuf tmp(&C, x.cells * x.cell_words() * 8);
+    Launch L = C.L();
+    scalar_mul(C.dev, x.data(), dc.as<ulonglong2>(), tmp.as<u64>(), static_cast<int>(x.level), 2 * x.cells, L);
+    const double raw_scale = x.scale * scale;
+    TensorPtr out = make_tensor(C, x.cells, x.level - 1, raw_scale / static_cast<double>(C.ring.primes[x.level]));
+    out->shape = x.shape;
+    out->batch = x.batch;
+    rescale(C.dev, tmp.as<u64>(), out->data(), static_cast<int>(x.level), 2 * x.cells, L);
+    return out;
+}
+
+// add_plain(x, encode_const(c, x.scale, x.level)) (ckks.hpp:305-311)
+TensorPtr ct_add_const(Context& C, const Tensor& x, double c) {
+    C.enc->check_encode(1, std::abs(c), x.scale, x.level);
+    std::vector<u64> res =
+        C.enc->residues_of_rounded(roundl(static_cast<long double>(c) * static_cast<long double>(x.scale)), x.level);
+    DevBuf dc = C.upload_vec(res);
+    TensorPtr out = make_tensor(C, x.cells, x.level, x.scale);
+    out->shape = x.shape;
+    out->batch = x.batch;
+    cuda_check(cudaMemcpyAsync(out->data(), x.data(), x.cells * x.cell_words() * 8, cudaMemcpyDeviceToDevice, C.stream),
+               "copy");
+    add_coeff0(C.dev, out->data(), dc.as<u64>(), static_cast<int>(x.level), x.cells, C.L());
+    return out;
+}
+
+// ---------------------------------------------------------------- activation
+
+std::size_t Activation::encrypted_depth() const {
+    std::size_t d = degree(), lg = 0;
+    while ((std::size_t(1) << lg) < d) ++lg;
+    return lg + 1;
+}
+
+void Activation::validate() const {
+    if (degree() < 1) throw std::invalid_argument("PolyActivation: degree must be >= 1");
+    for (double c : coefficients)
+        if (!std::isfinite(c)) throw std::invalid_argument("PolyActivation: non-finite coefficient");
+    if (!(interval_bound > 0)) throw std::invalid_argument("PolyActivation: interval bound must be > 0");
+}
+
+// eval_encrypted (activation.hpp:228-265): power-basis plan over whole tensors.
+TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x) {
+    act.validate();
+    const std::size_t d = act.degree(), depth = act.encrypted_depth();
+    if (x.level < depth) throw std::invalid_argument("eval_encrypted: insufficient depth budget");
+    std::map<std::size_t, TensorPtr> powers;
+    std::function<const Tensor&(std::size_t)> power = [&](std::size_t k) -> const Tensor& {
+        if (k == 1) return x;
+        auto it = powers.find(k);
+        if (it != powers.end()) return *it->second;
+        if (k % 2 == 0) {
+            TensorPtr sq = ct_square(C, power(k / 2));
+            return *powers.emplace(k, std::move(sq)).first->second;
+        }
+        const Tensor& hi = power((k + 1) / 2);
+        const Tensor& lo = power(k / 2);
+        std::uint32_t lvl = std::min(hi.level, lo.level);
+        TensorPtr h = ct_mod_switch(C, hi, lvl), l = ct_mod_switch(C, lo, lvl);
+        TensorPtr prod = ct_mul(C, *h, *l);
+        return *powers.emplace(k, std::move(prod)).first->second;
+    };
+    const double target = C.scale;
+    std::vector<TensorPtr> terms;
+    for (std::size_t k = 1; k <= d; ++k) {
+        const Tensor& p = power(k);
+        double u = target * static_cast<double>(C.ring.primes[p.level]) / p.scale;
+        terms.push_back(ct_mul_const(C, p, act.coefficients[k], u));
+    }
+    std::uint32_t out_level = terms.back()->level;
+    for (auto& t : terms) out_level = std::min(out_level, t->level);
+    TensorPtr acc = ct_mod_switch(C, *terms[0], out_level);
+    for (std::size_t i = 1; i < terms.size(); ++i) {
+        TensorPtr t = ct_mod_switch(C, *terms[i], out_level);
+        acc = ct_add(C, *acc, *t, false);
+    }
+    if (act.coefficients[0] != 0.0) acc = ct_add_const(C, *acc, act.coefficients[0]);
+    acc->shape = x.shape;
+    acc->batch = x.batch;
+    return acc;
+}
+
+// ---------------------------------------------------------------- encryption
+
+namespace {
+
+// Public-key encryptions of `count` messages (or zeros) at limbs 0..level,
+// randomness from make_encryption_randomness(seeds[i]) (ckks.hpp:238-266).
+// out: [count][2][level+1][n] device.
+void encrypt_into(Context& C, std::size_t count, const u64* seeds, const std::vector<EncodedCoeffs>* msgs,
+                  std::uint32_t level, u64* out) {
+    if (!C.has_pk) throw std::invalid_argument("encrypt: no public key loaded");
+    const std::size_t n = C.n(), limbs = level + 1, cw = 2 * limbs * n;
+    const std::size_t chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, 1024));
+    Launch L = C.L();
+    std::vector<signed char> hr(chunk * n), he0(chunk * n), he1(chunk * n);
+    std::vector<long long> hm;
+    std::vector<u64> hres;
+    DevBuf dr(&C, chunk * n), de0(&C, chunk * n), de1(&C, chunk * n), rr(&C, chunk * limbs * n * 8);
+    DevBuf dm(&C, msgs ? chunk * limbs * n * 8 : 0), dmi(&C, msgs ? chunk * n * 8 : 0);
+    for (std::size_t c0 = 0; c0 < count; c0 += chunk) {
+        const std::size_t m = std::min(chunk, count - c0);
+        parallel_items(m, [&](std::size_t k) {
+            const u64 s = seeds[c0 + k];
+            to_int8(sample_secretish(C, 0.5, derive_seed(s, 0x0a01)), &hr[k * n]);
+            to_int8(sample_error(C, derive_seed(s, 0x0a02)), &he0[k * n]);
+            to_int8(sample_error(C, derive_seed(s, 0x0a03)), &he1[k * n]);
+        });
+        C.upload(dr.get(), hr.data(), m * n);
+        C.upload(de0.get(), he0.data(), m * n);
+        C.upload(de1.get(), he1.data(), m * n);
+        const u64* mres = nullptr;
+        if (msgs) {
+            bool all_small = true;
+            for (std::size_t k = 0; k < m; ++k) all_small = all_small && (*msgs)[c0 + k].small;
+            if (all_small) {
+                hm.resize(m * n);
+                for (std::size_t k = 0; k < m; ++k) std::memcpy(&hm[k * n], (*msgs)[c0 + k].coeffs.data(), n * 8);
+                C.upload(dmi.get(), hm.data(), m * n * 8);
+                i64_to_rns(C.dev, dmi.as<long long>(), dm.as<u64>(), static_cast<int>(level), m, L);
+            } else {
+                hres.assign(m * limbs * n, 0);
+                for (std::size_t k = 0; k < m; ++k) {
+                    const EncodedCoeffs& e = (*msgs)[c0 + k];
+                    for (std::size_t i = 0; i < limbs; ++i)
+                        for (std::size_t j = 0; j < n; ++j)
+                            hres[(k * limbs + i) * n + j] =
+                                e.small ? C.ring.mods[i].from_signed(e.coeffs[j]) : e.residues[i * n + j];
+                }
+                C.upload(dm.get(), hres.data(), hres.size() * 8);
+            }
+            mres = dm.as<u64>();
+        }
+        small_to_rns(C.dev, dr.as<signed char>(), rr.as<u64>(), static_cast<int>(level), m, L);
+        ntt_forward(C.dev, rr.as<u64>(), static_cast<int>(level), m, L);
+        u64* o = out + c0 * cw;
+        mul_by_key(C.dev, rr.as<u64>(), C.pk.as<u64>(), C.top() + 1, o, static_cast<int>(level), m, L);
+        ntt_inverse(C.dev, o, static_cast<int>(level), 2 * m, L);
+        add_noise_msg(C.dev, o, de0.as<signed char>(), de1.as<signed char>(), mres, static_cast<int>(level), m, L);
+    }
+}
+
+}  // namespace
+
+// encrypt_tensor (tensor.hpp:77-94)
+TensorPtr encrypt_tensor(Context& C, const double* data, std::size_t batch, std::size_t positions, u64 seed) {
+    if (batch > C.n() / 2) throw std::invalid_argument("encrypt_tensor: batch exceeds slot count");
+    const std::size_t top = C.top();
+    std::vector<EncodedCoeffs> msgs(positions);
+    std::vector<u64> seeds(positions);
+    parallel_items(positions, [&](std::size_t pos) {
+        std::vector<double> slots(batch);
+        for (std::size_t i = 0; i < batch; ++i) slots[i] = data[i * positions + pos];
+        C.enc->encode_real(slots.data(), batch, C.scale, top, msgs[pos]);
+        seeds[pos] = derive_seed(seed, 0xce11 + pos);
+    });
+    TensorPtr out = make_tensor(C, positions, static_cast<std::uint32_t>(top), C.scale);
+    out->batch = batch;
+    encrypt_into(C, positions, seeds.data(), &msgs, static_cast<std::uint32_t>(top), out->data());
+    return out;
+}
+
+// CkksEngine::encrypt with explicit randomness (ckks.hpp:249-266)
+TensorPtr encrypt_raw(Context& C, const u64* m, const long long* r, const long long* e0, const long long* e1,
+                      std::size_t count, double scale) {
+    if (!C.has_pk) throw std::invalid_argument("encrypt: no public key loaded");
+    const std::size_t n = C.n(), top = C.top(), limbs = top + 1;
+    TensorPtr out = make_tensor(C, count, static_cast<std::uint32_t>(top), scale);
+    std::vector<signed char> hr(count * n), h0(count * n), h1(count * n);
+    to_int8(std::vector<long long>(r, r + count * n), hr.data());
+    to_int8(std::vector<long long>(e0, e0 + count * n), h0.data());
+    to_int8(std::vector<long long>(e1, e1 + count * n), h1.data());
+    DevBuf dr = C.upload_vec(hr), d0 = C.upload_vec(h0), d1 = C.upload_vec(h1);
+    DevBuf dm(&C, count * limbs * n * 8), rr(&C, count * limbs * n * 8);
+    C.upload(dm.get(), m, count * limbs * n * 8);
+    Launch L = C.L();
+    small_to_rns(C.dev, dr.as<signed char>(), rr.as<u64>(), static_cast<int>(top), count, L);
+    ntt_forward(C.dev, rr.as<u64>(), static_cast<int>(top), count, L);
+    mul_by_key(C.dev, rr.as<u64>(), C.pk.as<u64>(), limbs, out->data(), static_cast<int>(top), count, L);
+    ntt_inverse(C.dev, out->data(), static_cast<int>(top), 2 * count, L);
+    add_noise_msg(C.dev, out->data(), d0.as<signed char>(), d1.as<signed char>(), dm.as<u64>(), static_cast<int>(top),
+                  count, L);
+    return out;
+}
+
+// decrypt (ckks.hpp:273-279): c0 + c1 * s at the ciphertext level
+void decrypt_raw(Context& C, const Tensor& t, u64* out_host) {
+    if (!C.has_secret) throw std::invalid_argument("decrypt: no secret key loaded");
+    const std::size_t n = C.n(), limbs = t.level + 1, pw = limbs * n;
+    DevBuf tmp(&C, t.cells * pw * 8);
+    Launch L = C.L();
+    cuda_check(cudaMemcpy2DAsync(tmp.get(), pw * 8, t.data() + pw, 2 * pw * 8, pw * 8, t.cells,
+                                 cudaMemcpyDeviceToDevice, C.stream),
+               "copy c1");
+    ntt_forward(C.dev, tmp.as<u64>(), static_cast<int>(t.level), t.cells, L);
+    mul_secret(C.dev, tmp.as<u64>(), C.s_ntt.as<u64>(), static_cast<int>(t.level), t.cells, L);
+    ntt_inverse(C.dev, tmp.as<u64>(), static_cast<int>(t.level), t.cells, L);
+    add_c0(C.dev, t.data(), tmp.as<u64>(), static_cast<int>(t.level), t.cells, L);
+    C.download(out_host, tmp.get(), t.cells * pw * 8);
+}
+
+// decrypt_tensor (tensor.hpp:96-106): out [batch][positions]
+void decrypt_tensor(Context& C, const Tensor& t, std::size_t batch, double* out) {
+    if (batch > C.n() / 2) throw std::invalid_argument("decrypt_tensor: batch exceeds slot count");
+    const std::size_t pw = (t.level + 1) * C.n();
+    std::vector<u64> plain(t.cells * pw);
+    decrypt_raw(C, t, plain.data());
+    parallel_items(t.cells, [&](std::size_t pos) {
+        std::vector<double> v(batch);
+        C.enc->decode_real(&plain[pos * pw], t.level, t.scale, v.data(), batch);
+        for (std::size_t i = 0; i < batch; ++i) out[i * t.cells + pos] = v[i];
+    });
+}
+
+// ---------------------------------------------------------------- network
+
+const char* Layer::kind_name() const {
+    switch (kind) {
+        case 0: return "conv2d";
+        case 1: return "avg_pool2d";
+        case 2: return "zero_pad2d";
+        case 3: return "dense";
+        case 4: return "activation";
+        case 5: return "sigmoid";
+    }
+    return "?";
+}
+
+// shape_infer / infer_layer_shape (model.hpp:116-157)
+void Model::infer_shapes() {
+    shapes.clear();
+    Shape cur = input;
+    for (std::size_t i = 0; i < layers.size(); ++i) {
+        const Layer& l = layers[i];
+        if (l.kind == 5 && i + 1 != layers.size())
+            throw std::invalid_argument("shape_infer: sigmoid allowed only as final layer");
+        if (l.kind == 3 && !cur.flat) cur = cur.as_flat();
+        switch (l.kind) {
+            case 0: {
+                if (cur.flat) throw std::invalid_argument("shape_infer: conv2d on flattened input");
+                if (l.filters == 0 || l.kh == 0 || l.kw == 0 || l.stride == 0)
+                    throw std::invalid_argument("shape_infer: conv2d parameters must be positive");
+                auto dim = [&](std::size_t in, std::size_t k) -> std::size_t {
+                    if (!l.valid) return (in + l.stride - 1) / l.stride;
+                    if (in < k) throw std::invalid_argument("shape_infer: conv kernel larger than input (valid padding)");
+                    return (in - k) / l.stride + 1;
+                };
+                std::size_t oh = dim(cur.h, l.kh);
+                std::size_t ow = dim(cur.w, l.kw);
+                cur = Shape::spatial(oh, ow, l.filters);
+                break;
+            }
+            case 1:
+                if (cur.flat) throw std::invalid_argument("shape_infer: avg_pool2d on flattened input");
+                if (l.pool == 0) throw std::invalid_argument("shape_infer: pool size must be positive");
+                if (cur.h < l.pool || cur.w < l.pool)
+                    throw std::invalid_argument("shape_infer: spatial dims smaller than pool size");
+                cur = Shape::spatial(cur.h / l.pool, cur.w / l.pool, cur.c);
+                break;
+            case 2:
+                if (cur.flat) throw std::invalid_argument("shape_infer: zero_pad2d on flattened input");
+                cur = Shape::spatial(cur.h + 2 * l.pad, cur.w + 2 * l.pad, cur.c);
+                break;
+            case 3:
+                if (l.units == 0) throw std::invalid_argument("shape_infer: dense units must be positive");
+                cur = Shape::flattened(l.units);
+                break;
+            case 4:
+                if (l.act < 0 || static_cast<std::size_t>(l.act) >= acts.size())
+                    throw std::invalid_argument("model: activation layer references unregistered surrogate 'act" +
+                                                std::to_string(l.act) + "'");
+                break;
+            case 5: break;
+            default: throw std::invalid_argument("shape_infer: unknown layer kind");
+        }
+        shapes.push_back(cur);
+    }
+}
+
+std::size_t Model::depth_cost() const {
+    std::size_t cost = 0;
+    for (const auto& l : layers) {
+        if (l.kind == 0 || l.kind == 1 || l.kind == 3) cost += 1;
+        else if (l.kind == 4) cost += acts.at(static_cast<std::size_t>(l.act)).encrypted_depth();
+    }
+    return cost;
+}
+
+namespace {
+
+// conv2d / dense as a gather-MAC (layers.hpp:174-211, 269-293)
+TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, const Shape& out_shape) {
+    const Layer& l = M.layers[li];
+    const bool conv = l.kind == 0;
+    const Shape& in = x.shape;
+    const std::size_t rows = conv ? l.kh * l.kw * in.c : in.positions();
+    const std::size_t oc = conv ? l.filters : l.units;
+    if (l.w.size() != rows * oc || l.b.size() != oc)
+        throw std::invalid_argument(conv ? "conv2d: weight/bias shape mismatch" : "dense: weight/bias shape mismatch");
+    if (x.level == 0) throw std::invalid_argument(conv ? "conv2d: no level headroom" : "dense: no level headroom");
+    const std::uint32_t level = x.level;
+    const std::size_t limbs = level + 1;
+    const double wscale = C.scale;
+
+    auto key = std::make_pair(li, level);
+    auto it = M.linear.find(key);
+    if (it == M.linear.end()) {
+        Model::LinearCache lc;
+        lc.oc = static_cast<int>(oc);
+        lc.oc_pad = static_cast<int>((oc + 7) / 8 * 8);
+        std::vector<ulonglong2> w(rows * lc.oc_pad * limbs, make_ulonglong2(0, 0));
+        for (std::size_t r = 0; r < rows; ++r)
+            for (std::size_t o = 0; o < oc; ++o) {
+                std::vector<u64> res = C.enc->scalar_residues(l.w[r * oc + o], wscale, level);
+                for (std::size_t i = 0; i < limbs; ++i)
+                    w[(r * lc.oc_pad + o) * limbs + i] = make_ulonglong2(res[i], shoup_of(res[i], C.ring.primes[i]));
+            }
+        std::vector<int> src, wrow;
+        if (conv) {
+            const std::size_t need_h = (out_shape.h - 1) * l.stride + l.kh, need_w = (out_shape.w - 1) * l.stride + l.kw;
+            long long pad_top = 0, pad_left = 0;
+            if (!l.valid) {
+                pad_top = need_h > in.h ? static_cast<long long>((need_h - in.h) / 2) : 0;
+                pad_left = need_w > in.w ? static_cast<long long>((need_w - in.w) / 2) : 0;
+            }
+            lc.pixels = static_cast<int>(out_shape.h * out_shape.w);
+            lc.K = static_cast<int>(rows);
+            for (std::size_t oy = 0; oy < out_shape.h; ++oy)
+                for (std::size_t ox = 0; ox < out_shape.w; ++ox)
+                    for (std::size_t ky = 0; ky < l.kh; ++ky)
+                        for (std::size_t kx = 0; kx < l.kw; ++kx)
+                            for (std::size_t ic = 0; ic < in.c; ++ic) {
+                                long long y = static_cast<long long>(oy * l.stride + ky) - pad_top;
+                                long long xx = static_cast<long long>(ox * l.stride + kx) - pad_left;
+                                bool ok = y >= 0 && xx >= 0 && y < static_cast<long long>(in.h) &&
+                                          xx < static_cast<long long>(in.w);
+                                src.push_back(ok ? static_cast<int>((y * in.w + xx) * in.c + ic) : -1);
+                                wrow.push_back(static_cast<int>((ky * l.kw + kx) * in.c + ic));
+                            }
+        } else {
+            lc.pixels = 1;
+            lc.K = static_cast<int>(rows);
+            for (std::size_t k = 0; k < rows; ++k) {
+                src.push_back(static_cast<int>(k));
+                wrow.push_back(static_cast<int>(k));
+            }
+        }
+        lc.weights = C.upload_vec(w);
+        lc.src = C.upload_vec(src);
+        lc.wrow = C.upload_vec(wrow);
+        it = M.linear.emplace(key, std::move(lc)).first;
+    }
+    Model::LinearCache& lc = it->second;
+
+    const double acc_scale = x.scale * wscale;
+    auto bkey = std::make_tuple(li, level, acc_scale);
+    auto bit = M.bias.find(bkey);
+    if (bit == M.bias.end()) {
+        std::vector<u64> b(oc * limbs);
+        for (std::size_t o = 0; o < oc; ++o) {
+            std::vector<u64> res = C.enc->scalar_residues(l.b[o], acc_scale, level);
+            std::copy(res.begin(), res.end(), b.begin() + o * limbs);
+        }
+        bit = M.bias.emplace(bkey, C.upload_vec(b)).first;
+    }
+
+    TensorPtr out = make_tensor(C, out_shape.positions(), level - 1, acc_scale / static_cast<double>(C.ring.primes[level]));
+    out->shape = out_shape;
+    out->batch = x.batch;
+    const std::size_t cw = x.cell_words();
+    const std::size_t per_pixel = oc * cw * 8;
+    const std::size_t pix_chunk = std::max<std::size_t>(1, std::min<std::size_t>(lc.pixels, kScratchBytes / per_pixel));
+    DevBuf pre(&C, pix_chunk * per_pixel);
+    Launch L = C.L();
+    for (std::size_t p0 = 0; p0 < static_cast<std::size_t>(lc.pixels); p0 += pix_chunk) {
+        const std::size_t m = std::min(pix_chunk, lc.pixels - p0);
+        GatherMac g{lc.src.as<int>() + p0 * lc.K, lc.wrow.as<int>() + p0 * lc.K, lc.weights.as<ulonglong2>(),
+                    bit->second.as<u64>(), static_cast<int>(m), lc.K, lc.oc, lc.oc_pad, lc.oc};
+        gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), L);
+        rescale(C.dev, pre.as<u64>(), out->cell(p0 * oc), static_cast<int>(level), 2 * m * oc, L);
+    }
+    return out;
+}
+
+// avg_pool2d_encrypted (layers.hpp:213-239)
+TensorPtr pool_layer(Context& C, Model& M, std::size_t li, const Tensor& x, const Shape& out_shape) {
+    const Layer& l = M.layers[li];
+    if (x.level == 0) throw std::invalid_argument("avg_pool2d: no level headroom");
+    const std::uint32_t level = x.level;
+    const double inv_area = 1.0 / static_cast<double>(l.pool * l.pool);
+    std::vector<u64> res = C.enc->scalar_residues(inv_area, C.scale, level);
+    DevBuf wres = C.upload_vec(with_shoup(C.ring, res));
+    auto key = std::make_pair(li, level);
+    auto it = M.pool_srcs.find(key);
+    const std::size_t taps = l.pool * l.pool;
+    if (it == M.pool_srcs.end()) {
+        std::vector<int> srcs;
+        const Shape& in = x.shape;
+        for (std::size_t p = 0; p < out_shape.positions(); ++p) {
+            std::size_t ch = p % out_shape.c, oxy = p / out_shape.c;
+            std::size_t oy = oxy / out_shape.w, ox = oxy % out_shape.w;
+            for (std::size_t dy = 0; dy < l.pool; ++dy)
+                for (std::size_t dx = 0; dx < l.pool; ++dx)
+                    srcs.push_back(static_cast<int>(((oy * l.pool + dy) * in.w + (ox * l.pool + dx)) * in.c + ch));
+        }
+        it = M.pool_srcs.emplace(key, C.upload_vec(srcs)).first;
+    }
+    const std::size_t cells = out_shape.positions();
+    DevBuf pre(&C, cells * x.cell_words() * 8);
+    Launch L = C.L();
+    pool_sum_scale(C.dev, x.data(), it->second.as<int>(), static_cast<int>(taps), wres.as<ulonglong2>(), pre.as<u64>(),
+                   static_cast<int>(level), cells, L);
+    TensorPtr out = make_tensor(C, cells, level - 1, x.scale * C.scale / static_cast<double>(C.ring.primes[level]));
+    out->shape = out_shape;
+    out->batch = x.batch;
+    rescale(C.dev, pre.as<u64>(), out->data(), static_cast<int>(level), 2 * cells, L);
+    return out;
+}
+
+// zero_pad2d_encrypted (layers.hpp:241-267): inner cells copied, border cells
+// are fresh encryptions of zero (host randomness, device arithmetic).
+TensorPtr pad_layer(Context& C, Model& M, std::size_t li, const Tensor& x, const Shape& out_shape, u64 layer_seed) {
+    const Layer& l = M.layers[li];
+    const std::size_t cells = out_shape.positions();
+    std::vector<int> idx_in(cells, -1), idx_border(cells, -1);
+    std::vector<u64> seeds;
+    for (std::size_t p = 0; p < cells; ++p) {
+        std::size_t ch = p % out_shape.c, xy = p / out_shape.c;
+        std::size_t y = xy / out_shape.w, xx = xy % out_shape.w;
+        bool inside = y >= l.pad && y < l.pad + x.shape.h && xx >= l.pad && xx < l.pad + x.shape.w;
+        if (inside) {
+            idx_in[p] = static_cast<int>(((y - l.pad) * x.shape.w + (xx - l.pad)) * x.shape.c + ch);
+        } else {
+            idx_border[p] = static_cast<int>(seeds.size());
+            seeds.push_back(derive_seed(layer_seed, 0xbad0 + p));
+        }
+    }
+    if (!seeds.empty()) C.enc->check_encode(1, 0.0, x.scale, C.top());  // encode_const(0, scale, top)
+    TensorPtr out = make_tensor(C, cells, x.level, x.scale);
+    out->shape = out_shape;
+    out->batch = x.batch;
+    Launch L = C.L();
+    DevBuf din = C.upload_vec(idx_in);
+    gather_cells(x.data(), din.as<int>(), out->data(), x.cell_words(), cells, L);
+    if (!seeds.empty()) {
+        DevBuf fresh(&C, seeds.size() * x.cell_words() * 8);
+        encrypt_into(C, seeds.size(), seeds.data(), nullptr, x.level, fresh.as<u64>());
+        DevBuf db = C.upload_vec(idx_border);
+        gather_cells(fresh.as<u64>(), db.as<int>(), out->data(), x.cell_words(), cells, L);
+    }
+    return out;
+}
+
+}  // namespace
+
+// forward_encrypted (layers.hpp:299-368)
+TensorPtr forward_encrypted(Context& C, Model& M, const Tensor& x, u64 seed, double* layer_seconds) {
+    if (!(x.shape == M.input))
+        throw std::invalid_argument("forward_encrypted: input shape " + x.shape.str() + " != model input " +
+                                    M.input.str());
+    M.infer_shapes();
+    long long level = static_cast<long long>(x.level);
+    for (std::size_t i = 0; i < M.layers.size(); ++i) {
+        const Layer& l = M.layers[i];
+        std::size_t cost = 0;
+        if (l.kind == 0 || l.kind == 1 || l.kind == 3) cost = 1;
+        else if (l.kind == 4) cost = M.acts[static_cast<std::size_t>(l.act)].encrypted_depth();
+        level -= static_cast<long long>(cost);
+        if (level < 0)
+            throw std::invalid_argument("forward_encrypted: depth budget exhausted at layer " + std::to_string(i) + " (" +
+                                        l.kind_name() + ")");
+    }
+    std::vector<cudaEvent_t> ev(M.layers.size() + 1);
+    if (layer_seconds)
+        for (auto& e : ev) cudaEventCreate(&e);
+    if (layer_seconds) cudaEventRecord(ev[0], C.stream);
+
+    TensorPtr cur;
+    auto current = [&]() -> const Tensor& { return cur ? *cur : x; };
+    for (std::size_t i = 0; i < M.layers.size(); ++i) {
+        const Layer& l = M.layers[i];
+        const u64 layer_seed = derive_seed(seed, 0x1a7e + i);
+        Shape in_shape = current().shape;
+        if (l.kind == 3 && !in_shape.flat) {
+            if (!cur) {  // flatten the caller's tensor: metadata only, take a view-copy
+                cur = make_tensor(C, x.cells, x.level, x.scale);
+                cuda_check(cudaMemcpyAsync(cur->data(), x.data(), x.cells * x.cell_words() * 8,
+                                           cudaMemcpyDeviceToDevice, C.stream), "copy");
+                cur->batch = x.batch;
+            }
+            cur->shape = in_shape.as_flat();
+        }
+        TensorPtr next;
+        switch (l.kind) {
+            case 0:
+            case 3: next = linear_layer(C, M, i, current(), M.shapes[i]); break;
+            case 1: next = pool_layer(C, M, i, current(), M.shapes[i]); break;
+            case 2: next = pad_layer(C, M, i, current(), M.shapes[i], layer_seed); break;
+            case 4:
+                next = eval_activation(C, M.acts[static_cast<std::size_t>(l.act)], current());
+                break;
+            case 5: break;  // the client thresholds the decrypted logit (layers.hpp:360-362)
+        }
+        if (next) cur = std::move(next);
+        if (layer_seconds) cudaEventRecord(ev[i + 1], C.stream);
+    }
+    if (!cur) {
+        cur = make_tensor(C, x.cells, x.level, x.scale);
+        cuda_check(cudaMemcpyAsync(cur->data(), x.data(), x.cells * x.cell_words() * 8, cudaMemcpyDeviceToDevice,
+                                   C.stream), "copy");
+        cur->shape = x.shape;
+        cur->batch = x.batch;
+    }
+    if (layer_seconds) {
+        C.sync();
+        for (std::size_t i = 0; i < M.layers.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            layer_seconds[i] = ms / 1000.0;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    return cur;
+}
+
+}  // namespace hecnn_b200

@@ -1,0 +1,170 @@
+// Device-resident CKKS engine: context (tables, keys, stream, memory),
+// ciphertext tensors and the scheme / network operations built from the
+// kernels in kernels.hpp. Host code here only orders kernels, keeps the
+// scale/level ledger with the reference's exact double arithmetic and turns
+// model weights into integer residues; no ciphertext word is computed on the
+// CPU.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host_ckks.hpp"
+#include "kernels.hpp"
+#include "ring_host.hpp"
+
+namespace hecnn_b200 {
+
+struct Context;
+
+// Stream-ordered device allocation (cudaMallocAsync on the context stream).
+class DevBuf {
+public:
+    DevBuf() = default;
+    DevBuf(Context* ctx, std::size_t bytes);
+    ~DevBuf() { reset(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+    DevBuf& operator=(DevBuf&& o) noexcept;
+    void reset();
+    template <class T>
+    T* as() const { return static_cast<T*>(ptr_); }
+    void* get() const { return ptr_; }
+    std::size_t bytes() const { return bytes_; }
+
+private:
+    Context* ctx_ = nullptr;
+    void* ptr_ = nullptr;
+    std::size_t bytes_ = 0;
+};
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    RingTables ring;
+    std::unique_ptr<Encoder> enc;
+    double scale = 0.0, sigma = 3.2;
+    bool degenerate = false;
+    DevRing dev;
+    std::vector<DevBuf> tables;
+    // keys (device resident; the secret also kept on the host for export)
+    std::vector<u64> secret_host;  // [(L+1)][n] coefficient domain
+    DevBuf s_ntt, pk, evk, evk_sh;
+    std::size_t evk_digits = 0;
+    bool has_secret = false, has_pk = false;
+    unsigned long long launches = 0;
+
+    Context(std::size_t n, const std::vector<u64>& primes, double scale, double sigma, bool degenerate, int device);
+    ~Context();
+    Launch L() { return Launch{stream, &launches}; }
+    std::size_t n() const { return ring.n; }
+    std::size_t top() const { return ring.limbs - 1; }
+    void upload(void* dst, const void* src, std::size_t bytes);
+    void download(void* dst, const void* src, std::size_t bytes);
+    void sync();
+    template <class T>
+    DevBuf upload_vec(const std::vector<T>& v) {
+        DevBuf b(this, v.size() * sizeof(T));
+        if (!v.empty()) upload(b.get(), v.data(), v.size() * sizeof(T));
+        return b;
+    }
+};
+
+struct Shape {
+    bool flat = true;
+    std::size_t h = 0, w = 0, c = 0, feat = 0;
+    static Shape spatial(std::size_t h, std::size_t w, std::size_t c) { return {false, h, w, c, 0}; }
+    static Shape flattened(std::size_t f) { return {true, 0, 0, 0, f}; }
+    std::size_t positions() const { return flat ? feat : h * w * c; }
+    Shape as_flat() const { return flattened(positions()); }
+    bool operator==(const Shape& o) const {
+        return flat == o.flat && (flat ? feat == o.feat : (h == o.h && w == o.w && c == o.c));
+    }
+    std::string str() const;
+};
+
+// A device batch of ciphertexts with one shared (scale, level):
+// [cells][2][level+1][n] u64.
+struct Tensor {
+    Context* ctx = nullptr;
+    DevBuf buf;
+    std::size_t cells = 0;
+    std::uint32_t level = 0;
+    double scale = 0.0;
+    Shape shape;
+    std::size_t batch = 0;
+    std::size_t cell_words() const { return 2 * (level + 1) * ctx->n(); }
+    u64* data() const { return buf.as<u64>(); }
+    u64* cell(std::size_t i) const { return data() + i * cell_words(); }
+};
+using TensorPtr = std::unique_ptr<Tensor>;
+
+TensorPtr make_tensor(Context& C, std::size_t cells, std::uint32_t level, double scale);
+
+// ---- keys
+void keygen(Context& C, u64 seed);
+void import_keys(Context& C, const u64* secret, const u64* pk_b, const u64* pk_a, const u64* evk, std::size_t digits);
+
+// ---- scheme ops (ckks.hpp)
+TensorPtr ct_add(Context& C, const Tensor& x, const Tensor& y, bool subtract);
+TensorPtr ct_mul(Context& C, const Tensor& x, const Tensor& y);
+TensorPtr ct_square(Context& C, const Tensor& x);
+TensorPtr ct_rescale(Context& C, const Tensor& x);
+TensorPtr ct_mod_switch(Context& C, const Tensor& x, std::uint32_t to_level);
+TensorPtr ct_mul_const(Context& C, const Tensor& x, double c, double scale);
+TensorPtr ct_add_const(Context& C, const Tensor& x, double c);
+// key_switch on raw d2 polys: out [count][2][level+1][n] NTT domain
+void key_switch_raw(Context& C, const u64* d2, u64* out, std::size_t level, std::size_t count);
+
+struct Activation {
+    std::vector<double> coefficients;
+    double interval_bound = 0.0;
+    std::size_t degree() const { return coefficients.empty() ? 0 : coefficients.size() - 1; }
+    std::size_t encrypted_depth() const;
+    void validate() const;
+};
+TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x);
+
+// ---- client side
+TensorPtr encrypt_tensor(Context& C, const double* data, std::size_t batch, std::size_t positions, u64 seed);
+TensorPtr encrypt_raw(Context& C, const u64* m, const long long* r, const long long* e0, const long long* e1,
+                      std::size_t count, double scale);
+void decrypt_raw(Context& C, const Tensor& t, u64* out_host);
+void decrypt_tensor(Context& C, const Tensor& t, std::size_t batch, double* out);
+
+// ---- network
+struct Layer {
+    int kind = 0;
+    std::size_t filters = 0, kh = 0, kw = 0, stride = 1, pool = 0, pad = 0, units = 0;
+    bool valid = false;
+    int act = -1;
+    std::vector<double> w, b;
+    const char* kind_name() const;
+};
+
+struct Model {
+    Shape input;
+    std::vector<Layer> layers;
+    std::vector<Activation> acts;
+    std::vector<Shape> shapes;  // per-layer output shapes (shape_infer)
+    // integer-weight caches, keyed by (layer, level) and (layer, level, scale)
+    struct LinearCache {
+        DevBuf src, wrow, weights;
+        int pixels = 0, K = 0, oc = 0, oc_pad = 0;
+    };
+    std::map<std::pair<std::size_t, std::uint32_t>, LinearCache> linear;
+    std::map<std::tuple<std::size_t, std::uint32_t, double>, DevBuf> bias;
+    std::map<std::pair<std::size_t, std::uint32_t>, DevBuf> pool_srcs;
+
+    void infer_shapes();
+    std::size_t depth_cost() const;
+};
+
+TensorPtr forward_encrypted(Context& C, Model& M, const Tensor& x, u64 seed, double* layer_seconds);
+
+}  // namespace hecnn_b200

@@ -1,0 +1,109 @@
+// Device tables and kernel launchers shared by the CUDA translation units and
+// the host engine. Launchers take plain device pointers and a stream; every
+// launcher bumps the context's launch counter through `Launch`.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "arith.cuh"
+
+namespace hecnn_b200 {
+
+// Read-only ring tables resident on the device (built by RingTables, ring_host.hpp).
+struct DevRing {
+    int n = 0, logn = 0, limbs = 0, crt_words = 0;
+    const ModConst* mod = nullptr;           // [limbs]
+    const ulonglong2* fwd = nullptr;         // [limbs][n] (psi^bitrev(i), shoup)
+    const ulonglong2* inv = nullptr;         // [limbs][n] (psi^-bitrev(i), shoup)
+    const ulonglong2* n_inv = nullptr;       // [limbs]
+    const ulonglong2* inv_dropped = nullptr; // [limbs][limbs] (p_l^-1 mod q_i, shoup) at [l][i]
+    const u64* p_mod = nullptr;              // [limbs][limbs] p_l mod q_i at [l][i]
+    const ulonglong2* punct_inv = nullptr;   // [limbs][limbs] ((Q_l/q_i)^-1 mod q_i, shoup)
+    const u64* punct = nullptr;              // [limbs][limbs][crt_words] Q_l/q_i
+    const u64* modulus = nullptr;            // [limbs][crt_words] Q_l
+    const double* inv_q = nullptr;           // [limbs] 1/q_i
+};
+
+struct Launch {
+    cudaStream_t stream = nullptr;
+    unsigned long long* counter = nullptr;
+    void count(unsigned long long k = 1) const {
+        if (counter) *counter += k;
+    }
+};
+
+void check_launch(const char* what);
+
+// ---- NTT (ntt.cu). polys: [count][level+1][n], limb index = poly % (level+1)
+void ntt_forward(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L);
+void ntt_inverse(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L);
+
+// ---- elementwise ring ops (ring_ops.cu), [count][level+1][n]
+enum class EwOp { Add, Sub, Neg, Mul, Mac };
+void poly_elementwise(const DevRing& R, EwOp op, const u64* a, const u64* b, u64* out, int level,
+                      std::size_t count, const Launch& L);
+// rescale_poly on [count][level+1][n] -> [count][level][n] (ring.hpp:419-442)
+void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L);
+// copy limbs 0..to_level of [count][level+1][n] into [count][to_level+1][n]
+void drop_limbs(const DevRing& R, const u64* in, u64* out, int level, int to_level, std::size_t count,
+                const Launch& L);
+// NTT-domain tensor products, F* = [count][2][level+1][n]:
+//   d01 = [count][2][level+1][n] (d0, d1), d2 = [count][level+1][n]
+void tensor_mul(const DevRing& R, const u64* fx, const u64* fy, u64* d01, u64* d2, int level, std::size_t count,
+                const Launch& L);
+void tensor_square(const DevRing& R, const u64* fx, u64* d01, u64* d2, int level, std::size_t count,
+                   const Launch& L);
+// out = in * c_i (Shoup) per limb; consts = [level+1] (value, shoup) pairs (ckks.hpp:588-597)
+void scalar_mul(const DevRing& R, const u64* in, const ulonglong2* consts, u64* out, int level, std::size_t count,
+                const Launch& L);
+// c0[ct][i][0] += consts[i] for every ciphertext of a [count][2][level+1][n] batch
+// (add_scalar_inplace / add_plain of a constant, ckks.hpp:305-311, 468-472)
+void add_coeff0(const DevRing& R, u64* cts, const u64* consts, int level, std::size_t count, const Launch& L);
+
+// Shoup companions floor(w * 2^64 / q_i) of a [count][limbs][n] table (evk)
+void shoup_table(const DevRing& R, const u64* in, u64* out, int limbs, std::size_t count, const Launch& L);
+
+// ---- key switching (keyswitch.cu)
+// CRT reconstruction + base-2^20 digits of d2 (coefficient domain): digits [count][D][n] u32
+void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, std::size_t count,
+                const Launch& L);
+// acc01[ct] (NTT domain, [count][2][level+1][n]) += sum_t NTT(digit_t) * evk_t
+//   evk: [Dtop][2][limbs][n] values, evk_sh: Shoup companions
+void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, u64* acc01, int level,
+                   int D, std::size_t count, const Launch& L);
+
+// ---- linear layers (linear.cu)
+// Gather-MAC for conv/dense: see linear.cu for the table formats.
+struct GatherMac {
+    const int* src;            // [pixels][K] input cell index per tap (-1: invalid tap)
+    const int* wrow;           // [pixels][K] weight row per tap
+    const ulonglong2* weights; // [rows][oc_pad][limbs] (residue, shoup) at level, oc_pad % 8 == 0
+    const u64* bias;           // [oc][level+1] residues (added to c0 coeff 0), or null
+    int pixels, K, oc, oc_pad, out_stride_pixel;  // output cell = pixel * out_stride_pixel + oc
+};
+void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, const Launch& L);
+// 2x2-style average pool: out cell p sums srcs[p][0..taps) then multiplies by w (shoup), level kept
+void pool_sum_scale(const DevRing& R, const u64* x, const int* srcs, int taps, const ulonglong2* w, u64* y,
+                    int level, std::size_t out_cells, const Launch& L);
+// gather whole cells: y[i] = x[idx[i]] for idx >= 0 (ciphertext-sized copies)
+void gather_cells(const u64* x, const int* idx, u64* y, std::size_t cell_words, std::size_t cells, const Launch& L);
+
+// ---- encryption pieces (ring_ops.cu)
+// signed small coefficients [count][n] (int8) -> residues [count][level+1][n]
+void small_to_rns(const DevRing& R, const signed char* s, u64* out, int level, std::size_t count, const Launch& L);
+// i64 coefficients [count][n] -> residues [count][level+1][n]
+void i64_to_rns(const DevRing& R, const long long* s, u64* out, int level, std::size_t count, const Launch& L);
+// out[ct][comp][i][j] = rt[ct][i][j] * pk[comp][i][j]   (NTT domain, pk at its own limb stride)
+void mul_by_key(const DevRing& R, const u64* rt, const u64* pk, std::size_t pk_limbs, u64* out, int level,
+                std::size_t count, const Launch& L);
+// out[ct][0] += e0 + m, out[ct][1] += e1 (coefficient domain); m may be null
+void add_noise_msg(const DevRing& R, u64* ct, const signed char* e0, const signed char* e1, const u64* m,
+                   int level, std::size_t count, const Launch& L);
+// decrypt pieces: t[ct] (NTT domain, [count][level+1][n]) *= s_ntt (limb stride n), then
+// t[ct] += c0 of ct batch [count][2][level+1][n]
+void mul_secret(const DevRing& R, u64* t, const u64* s_ntt, int level, std::size_t count, const Launch& L);
+void add_c0(const DevRing& R, const u64* ct, u64* t, int level, std::size_t count, const Launch& L);
+
+}  // namespace hecnn_b200

@@ -1,0 +1,306 @@
+// Key switching (K5 + K6 in SURVEY.md §2.3): CkksEngine::key_switch,
+// ckks.hpp:601-630.
+//
+// Step 1 (k_crt_digits): per coefficient of d2, exact CRT reconstruction
+//   x = sum_i [a_i (Q/q_i)^-1]_{q_i} (Q/q_i) mod Q (reconstruct_mod_q,
+//   ring.hpp:529-538) in multiword registers, the quotient by Q estimated
+//   from sum_i w_i/q_i in double and corrected exactly, then the base-2^20
+//   digits (BigUInt::bits, bigint.hpp:110-114) are written as u32 [D][n].
+// Step 2 (k_keyswitch): one CTA per (ciphertext, limb i, block). For each
+//   digit t it lifts digit_t into limb i (v < q_i, else v mod q_i:
+//   ckks.hpp:622), runs the forward NTT in shared memory (same rounds and
+//   swizzle as ntt.cu) and multiply-accumulates against evk_t (b_t, a_t)
+//   with Shoup constants; accumulators stay in registers across all D
+//   digits, so neither the D lifted digit polynomials nor partial sums ever
+//   touch HBM. The epilogue adds (d0, d1) in place. For N > 2^13 a CTA owns
+//   a 2^13 block and recomputes the C = log2(N) - 13 column stages for its
+//   block directly from the (L2-resident) u32 digits.
+
+#include <stdexcept>
+
+#include "kernels.hpp"
+
+namespace hecnn_b200 {
+
+namespace {
+
+__device__ __forceinline__ int swz(int i) {
+    return i ^ static_cast<int>((0x1eb4d278963c5af0ull >> (4 * ((i >> 4) & 15))) & 15);
+}
+
+template <int W>
+__global__ void __launch_bounds__(128) k_crt_digits(DevRing R, const u64* __restrict__ d2, u32* __restrict__ digits,
+                                                  int level, int D, long long count) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= count * R.n) return;
+    const long long ct = t / R.n;
+    const int j = static_cast<int>(t % R.n);
+    const int limbs = level + 1;
+    const u64* a = d2 + ct * limbs * R.n + j;
+    u64 acc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) acc[w] = 0;
+    double frac = 0.0;
+    for (int i = 0; i < limbs; ++i) {
+        const u64 q = R.mod[i].q;
+        const ulonglong2 pinv = R.punct_inv[level * R.limbs + i];
+        const u64 wi = mul_shoup(a[static_cast<long long>(i) * R.n], pinv.x, pinv.y, q);
+        frac += static_cast<double>(wi) * R.inv_q[i];
+        const u64* P = R.punct + (static_cast<long long>(level) * R.limbs + i) * R.crt_words;
+        u64 carry = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const u64 p = P[w];
+            u64 lo = wi * p, hi = mulhi(wi, p);
+            lo += carry;
+            hi += lo < carry;
+            acc[w] += lo;
+            hi += acc[w] < lo;
+            carry = hi;
+        }
+    }
+    // subtract k*Q with k = floor(sum w_i/q_i) (exact up to one unit), then fix up
+    const u64 k = static_cast<u64>(frac);
+    const u64* Q = R.modulus + static_cast<long long>(level) * R.crt_words;
+    {
+        u64 carry = 0, borrow = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const u64 p = Q[w];
+            u64 lo = k * p, hi = mulhi(k, p);
+            lo += carry;
+            hi += lo < carry;
+            carry = hi;
+            const u64 before = acc[w];
+            const u64 d = before - lo - borrow;
+            borrow = (before < lo) || (before - lo < borrow) ? 1 : 0;
+            acc[w] = d;
+        }
+        if (borrow) {  // went negative: add Q back
+            u64 c = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const u64 s = acc[w] + Q[w];
+                const u64 c1 = s < acc[w];
+                acc[w] = s + c;
+                c = c1 | (acc[w] < s);
+            }
+        } else {  // at most one Q too many
+            bool ge = true;
+#pragma unroll
+            for (int w = W - 1; w >= 0; --w) {
+                // lexicographic compare from the top word, first difference decides
+                if (acc[w] != Q[w]) { ge = acc[w] > Q[w]; break; }
+            }
+            if (ge) {
+                u64 b = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    const u64 before = acc[w];
+                    acc[w] = before - Q[w] - b;
+                    b = (before < Q[w]) || (before - Q[w] < b) ? 1 : 0;
+                }
+            }
+        }
+    }
+    u32* out = digits + ct * D * R.n + j;
+    for (int d = 0; d < D; ++d) {
+        const int off = 20 * d;
+        const int wi = off >> 6, sh = off & 63;
+        u64 v = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            if (w == wi) v = acc[w] >> sh;
+            if (w == wi + 1 && sh > 44) v |= acc[w] << (64 - sh);
+        }
+        out[static_cast<long long>(d) * R.n] = static_cast<u32>(v & 0xFFFFFu);
+    }
+}
+
+__device__ __forceinline__ void ct_butterfly(u64& a, u64& b, ulonglong2 w, u64 q, u64 two_q) {
+    u64 u = a;
+    if (u >= two_q) u -= two_q;
+    u64 v = mul_shoup_lazy(b, w.x, w.y, q);
+    a = u + v;
+    b = u + two_q - v;
+}
+
+__host__ __device__ constexpr int ceil_div(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ constexpr int round_size(int LOGB, int LOGE, int s) { return ceil_div(LOGB - s, ceil_div(LOGB - s, LOGE)); }
+
+__device__ __forceinline__ u64 lift_digit(u32 v, u64 q) { return v < q ? v : v % q; }
+
+// Value at block-local position r after the C column stages (block b).
+template <int LOGN, int C>
+__device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const ulonglong2* __restrict__ tw, u64 q, int r,
+                                            int b) {
+    if constexpr (C == 0) {
+        return lift_digit(dig[r], q);
+    } else {
+        constexpr int E = 1 << C, B = 1 << (LOGN - C);
+        const u64 two_q = q << 1;
+        u64 x[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) x[k] = lift_digit(dig[r + k * B], q);
+#pragma unroll
+        for (int rho = 0; rho < C; ++rho) {
+            const int half = E >> (rho + 1);
+#pragma unroll
+            for (int blk = 0; blk < (1 << rho); ++blk) {
+                const ulonglong2 w = tw[(1 << rho) + blk];
+#pragma unroll
+                for (int kk = 0; kk < half; ++kk) ct_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
+            }
+        }
+        u64 v = x[0];
+#pragma unroll
+        for (int k = 1; k < E; ++k)
+            if (k == b) v = x[k];
+        return v;
+    }
+}
+
+template <int LOGN, int LOGB, int R, int S0, bool FIRST>
+__device__ __forceinline__ void ks_round(u64* s, const u32* __restrict__ dig, const ulonglong2* __restrict__ tw, u64 q,
+                                         int b) {
+    constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R, C = LOGN - LOGB;
+    const u64 two_q = q << 1;
+    for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
+        const int grp = u / STRIDE, col = u % STRIDE;
+        const int base = grp * G + col;
+        u64 x[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+            x[k] = FIRST ? column_value<LOGN, C>(dig, tw, q, base + k * STRIDE, b) : s[swz(base + k * STRIDE)];
+#pragma unroll
+        for (int rho = 0; rho < R; ++rho) {
+            const int st = C + S0 + rho;
+            const int half = E >> (rho + 1);
+            const int tbase = (1 << st) + (b << (S0 + rho)) + (grp << rho);
+#pragma unroll
+            for (int blk = 0; blk < (1 << rho); ++blk) {
+                const ulonglong2 w = tw[tbase + blk];
+#pragma unroll
+                for (int kk = 0; kk < half; ++kk) ct_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < E; ++k) s[swz(base + k * STRIDE)] = x[k];
+    }
+}
+
+template <int LOGN, int LOGB, int LOGE, int S0, bool FIRST>
+__device__ __forceinline__ void ks_rounds(u64* s, const u32* dig, const ulonglong2* tw, u64 q, int b) {
+    if constexpr (S0 < LOGB) {
+        constexpr int R = round_size(LOGB, LOGE, S0);
+        ks_round<LOGN, LOGB, R, S0, FIRST>(s, dig, tw, q, b);
+        __syncthreads();
+        ks_rounds<LOGN, LOGB, LOGE, S0 + R, false>(s, dig, tw, q, b);
+    }
+}
+
+// blockIdx.x = (ct * limbs + i) * nblocks + b
+template <int LOGN, int LOGB, int LOGE, int T>
+__global__ void __launch_bounds__(T) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
+                                                 const u64* __restrict__ evk_sh, u64* __restrict__ acc01, int level, int D) {
+    extern __shared__ u64 smem[];
+    constexpr int B = 1 << LOGB, C = LOGN - LOGB, P = B / T;
+    const int limbs = level + 1;
+    const long long cta = blockIdx.x;
+    const int b = static_cast<int>(cta & ((1 << C) - 1));
+    const long long row = cta >> C;  // ct * limbs + i
+    const long long ct = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    const u64 q = R.mod[i].q, two_q = q << 1;
+    const ulonglong2* tw = R.fwd + (static_cast<long long>(i) << LOGN);
+    const long long n = 1LL << LOGN;
+    const long long key_stride = static_cast<long long>(R.limbs) * n;  // one evk polynomial
+
+    u64 a0[P], a1[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) a0[k] = a1[k] = 0;
+
+    for (int t = 0; t < D; ++t) {
+        const u32* dig = digits + (ct * D + t) * n;
+        ks_rounds<LOGN, LOGB, LOGE, 0, true>(smem, dig, tw, q, b);
+        const long long kb = (2LL * t) * key_stride + static_cast<long long>(i) * n + (static_cast<long long>(b) << LOGB);
+        const long long ka = kb + key_stride;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const int j = threadIdx.x + k * T;
+            const u64 v = smem[swz(j)];
+            u64 s0 = a0[k] + mul_shoup_lazy(v, evk[kb + j], evk_sh[kb + j], q);
+            u64 s1 = a1[k] + mul_shoup_lazy(v, evk[ka + j], evk_sh[ka + j], q);
+            a0[k] = s0 >= two_q ? s0 - two_q : s0;
+            a1[k] = s1 >= two_q ? s1 - two_q : s1;
+        }
+        __syncthreads();
+    }
+    u64* o0 = acc01 + ((ct * 2) * limbs + i) * n + (static_cast<long long>(b) << LOGB);
+    u64* o1 = o0 + static_cast<long long>(limbs) * n;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        const int j = threadIdx.x + k * T;
+        o0[j] = add_mod(o0[j], reduce_2q(a0[k], q), q);
+        o1[j] = add_mod(o1[j], reduce_2q(a1[k], q), q);
+    }
+}
+
+template <int LOGN>
+struct KsPlan {
+    static constexpr int LOGB = LOGN <= 13 ? LOGN : 13;
+    static constexpr int LOGE = LOGB >= 8 ? 4 : 3;
+    static constexpr int B = 1 << LOGB;
+    static constexpr int T = B >= 8192 ? 512 : (B >= 64 ? B / 16 : B < 32 ? B : 32);
+};
+
+template <int LOGN>
+void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, u64* acc01, int level,
+                   int D, std::size_t count, const Launch& L) {
+    using P = KsPlan<LOGN>;
+    auto kern = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T>;
+    const int smem = P::B * 8;
+    static bool init = (smem > 48 * 1024 ? (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true) : true);
+    (void)init;
+    const std::size_t ctas = count * static_cast<std::size_t>(level + 1) << (LOGN - P::LOGB);
+    kern<<<static_cast<unsigned>(ctas), P::T, smem, L.stream>>>(R, digits, evk, evk_sh, acc01, level, D);
+    L.count();
+}
+
+}  // namespace
+
+void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, std::size_t count, const Launch& L) {
+    if (!count) return;
+    const long long total = static_cast<long long>(count) * R.n;
+    const unsigned grid = static_cast<unsigned>((total + 127) / 128);
+    const int W = R.crt_words;
+#define HECNN_CRT_CASE(WW) \
+    case WW: k_crt_digits<WW><<<grid, 128, 0, L.stream>>>(R, d2, digits, level, D, static_cast<long long>(count)); break;
+    switch (W) {
+        HECNN_CRT_CASE(2) HECNN_CRT_CASE(3) HECNN_CRT_CASE(4) HECNN_CRT_CASE(5) HECNN_CRT_CASE(6) HECNN_CRT_CASE(7)
+        HECNN_CRT_CASE(8) HECNN_CRT_CASE(9) HECNN_CRT_CASE(10) HECNN_CRT_CASE(11) HECNN_CRT_CASE(12)
+        HECNN_CRT_CASE(13) HECNN_CRT_CASE(14) HECNN_CRT_CASE(15) HECNN_CRT_CASE(16) HECNN_CRT_CASE(17)
+        HECNN_CRT_CASE(18) HECNN_CRT_CASE(19) HECNN_CRT_CASE(20)
+        default: throw std::invalid_argument("key_switch: modulus chain too long for the device CRT kernel");
+    }
+#undef HECNN_CRT_CASE
+    L.count();
+    check_launch("crt_digits");
+}
+
+void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, u64* acc01, int level,
+                   int D, std::size_t count, const Launch& L) {
+    if (!count) return;
+#define HECNN_KS_CASE(LG) \
+    case LG: run_keyswitch<LG>(R, digits, evk, evk_sh, acc01, level, D, count, L); break;
+    switch (R.logn) {
+        HECNN_KS_CASE(3) HECNN_KS_CASE(4) HECNN_KS_CASE(5) HECNN_KS_CASE(6) HECNN_KS_CASE(7) HECNN_KS_CASE(8)
+        HECNN_KS_CASE(9) HECNN_KS_CASE(10) HECNN_KS_CASE(11) HECNN_KS_CASE(12) HECNN_KS_CASE(13)
+        HECNN_KS_CASE(14) HECNN_KS_CASE(15) HECNN_KS_CASE(16)
+        default: throw std::invalid_argument("key_switch: ring degree outside 2^3..2^16 is not supported on the device");
+    }
+#undef HECNN_KS_CASE
+    check_launch("keyswitch_mac");
+}
+
+}  // namespace hecnn_b200

@@ -1,0 +1,133 @@
+// Plaintext-weight x ciphertext layers (K8 in SURVEY.md §2.3).
+//
+// conv2d_encrypted (layers.hpp:174-211) and dense_encrypted (:269-293) are,
+// per (component, limb, coefficient) column, an exact integer GEMM with a
+// gather: y[pixel*OC + oc] = sum_k w[wrow(pixel,k)][oc] * x[src(pixel,k)]
+// (mod q_i), followed by the bias on coefficient 0 of c0 and a rescale.
+// mul_scalar_mac (ckks.hpp:448-465) does one Shoup multiply + add per tap;
+// here a thread owns one column and a tile of OCT output channels, so each
+// ciphertext word it loads feeds OCT multiply-accumulates (register reuse of
+// the input across output channels), and the partial sums stay lazily
+// reduced in [0, 2q). Modular sums are order independent, so the result is
+// word-identical to the reference's sequential accumulation.
+
+#include <algorithm>
+
+#include "kernels.hpp"
+
+namespace hecnn_b200 {
+
+namespace {
+
+constexpr int TPB = 256;
+constexpr int OCT = 8;
+
+__global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, const u64* __restrict__ x,
+                                                    u64* __restrict__ y, int level) {
+    const int limbs = level + 1;
+    const long long poly_words = static_cast<long long>(limbs) * R.n;
+    const long long cell_words = 2 * poly_words;
+    const long long col = static_cast<long long>(blockIdx.x) * TPB + threadIdx.x;
+    if (col >= cell_words) return;
+    const int comp = static_cast<int>(col / poly_words);
+    const int i = static_cast<int>((col / R.n) % limbs);
+    const int j = static_cast<int>(col % R.n);
+    const int pixel = blockIdx.y;
+    const int oc0 = blockIdx.z * OCT;
+    const u64 q = R.mod[i].q, two_q = q << 1;
+
+    u64 acc[OCT];
+#pragma unroll
+    for (int o = 0; o < OCT; ++o) acc[o] = 0;
+
+    const int* src = g.src + static_cast<long long>(pixel) * g.K;
+    const int* wrow = g.wrow + static_cast<long long>(pixel) * g.K;
+    for (int k = 0; k < g.K; ++k) {
+        const int s = src[k];
+        if (s < 0) continue;
+        const u64 v = x[s * cell_words + col];
+        const ulonglong2* w = g.weights + (static_cast<long long>(wrow[k]) * g.oc_pad + oc0) * limbs + i;
+#pragma unroll
+        for (int o = 0; o < OCT; ++o) {
+            const ulonglong2 c = w[o * limbs];
+            const u64 t = acc[o] + mul_shoup_lazy(v, c.x, c.y, q);
+            acc[o] = t >= two_q ? t - two_q : t;
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < OCT; ++o) {
+        const int oc = oc0 + o;
+        if (oc >= g.oc) break;
+        u64 v = reduce_2q(acc[o], q);
+        if (g.bias && comp == 0 && j == 0) v = add_mod(v, g.bias[static_cast<long long>(oc) * limbs + i], q);
+        y[(static_cast<long long>(pixel) * g.out_stride_pixel + oc) * cell_words + col] = v;
+    }
+}
+
+// avg_pool2d_encrypted (layers.hpp:213-239): sum of the window, times
+// round(Delta / area) (one Shoup multiply), rescale done by the caller.
+__global__ void k_pool(DevRing R, const u64* __restrict__ x, const int* __restrict__ srcs, int taps,
+                       const ulonglong2* __restrict__ w, u64* __restrict__ y, int level) {
+    const int limbs = level + 1;
+    const long long poly_words = static_cast<long long>(limbs) * R.n;
+    const long long cell_words = 2 * poly_words;
+    const long long col = static_cast<long long>(blockIdx.x) * TPB + threadIdx.x;
+    if (col >= cell_words) return;
+    const int i = static_cast<int>((col / R.n) % limbs);
+    const long long cell = blockIdx.y;
+    const u64 q = R.mod[i].q;
+    u64 s = 0;
+    for (int k = 0; k < taps; ++k) s = add_mod(s, x[srcs[cell * taps + k] * cell_words + col], q);
+    const ulonglong2 c = w[i];
+    y[cell * cell_words + col] = mul_shoup(s, c.x, c.y, q);
+}
+
+__global__ void k_gather_cells(const u64* __restrict__ x, const int* __restrict__ idx, u64* __restrict__ y,
+                               long long cell_words) {
+    const long long cell = blockIdx.y;
+    const int s = idx[cell];
+    if (s < 0) return;
+    for (long long w = static_cast<long long>(blockIdx.x) * TPB + threadIdx.x; w < cell_words;
+         w += static_cast<long long>(gridDim.x) * TPB)
+        y[cell * cell_words + w] = x[s * cell_words + w];
+}
+
+}  // namespace
+
+void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, const Launch& L) {
+    const long long cell_words = 2LL * (level + 1) * R.n;
+    dim3 grid(static_cast<unsigned>((cell_words + TPB - 1) / TPB), static_cast<unsigned>(g.pixels),
+              static_cast<unsigned>((g.oc + OCT - 1) / OCT));
+    if (!g.pixels || !g.oc) return;
+    k_gather_mac<<<grid, TPB, 0, L.stream>>>(R, g, x, y, level);
+    L.count();
+    check_launch("gather_mac");
+}
+
+void pool_sum_scale(const DevRing& R, const u64* x, const int* srcs, int taps, const ulonglong2* w, u64* y, int level,
+                    std::size_t out_cells, const Launch& L) {
+    if (!out_cells) return;
+    const long long cell_words = 2LL * (level + 1) * R.n;
+    for (std::size_t off = 0; off < out_cells; off += 65535) {
+        const std::size_t m = std::min<std::size_t>(65535, out_cells - off);
+        dim3 grid(static_cast<unsigned>((cell_words + TPB - 1) / TPB), static_cast<unsigned>(m));
+        k_pool<<<grid, TPB, 0, L.stream>>>(R, x, srcs + off * taps, taps, w, y + off * cell_words, level);
+        L.count();
+    }
+    check_launch("pool_sum_scale");
+}
+
+void gather_cells(const u64* x, const int* idx, u64* y, std::size_t cell_words, std::size_t cells, const Launch& L) {
+    if (!cells) return;
+    const long long cw = static_cast<long long>(cell_words);
+    unsigned gx = static_cast<unsigned>(std::min<long long>((cw + TPB - 1) / TPB, 1024));
+    for (std::size_t off = 0; off < cells; off += 65535) {
+        const std::size_t m = std::min<std::size_t>(65535, cells - off);
+        dim3 grid(gx, static_cast<unsigned>(m));
+        k_gather_cells<<<grid, TPB, 0, L.stream>>>(x, idx + off, y + off * cell_words, cw);
+        L.count();
+    }
+    check_launch("gather_cells");
+}
+
+}  // namespace hecnn_b200

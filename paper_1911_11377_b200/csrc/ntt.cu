@@ -1,0 +1,324 @@
+// Batched negacyclic NTT / INTT over RNS limbs (K1/K2 in SURVEY.md §2.3).
+//
+// Transform: the reference's merged Cooley-Tukey forward NTT
+// (NttTables::forward, ring.hpp:83-108), whose output is in bit-reversed
+// evaluation order a_hat[j] = a(psi^(2*bitrev(j)+1)), and its exact inverse
+// (NttTables::inverse, ring.hpp:110-137, Gentleman-Sande + n^-1). Twiddles are
+// the reference's tables roots[m+i] = psi^bitrev(m+i) (Shoup pairs). The
+// butterfly network is the same; only the schedule differs:
+//
+//   * one CTA per (poly, limb, block); a block of 2^LOGB words lives in
+//     shared memory (<= 128 KB),
+//   * stages are grouped into rounds of up to 4; in a round each thread holds
+//     2^R words in registers and runs R butterfly stages on them, so shared
+//     memory is touched once per round, not once per stage,
+//   * shared-memory addresses use a GF(2)-linear XOR swizzle chosen (by
+//     exhaustive search) so every round's access pattern is bank-conflict free,
+//   * for N > 2^13 the first (forward) / last (inverse) LOGN-13 stages run in a
+//     separate column pass over HBM, leaving 2^13-word independent blocks.
+//
+// Values stay lazily reduced ([0,4q) forward, [0,2q) inverse) and are made
+// canonical at the end, so results are word-identical to the CPU reference.
+
+#include <stdexcept>
+
+#include "kernels.hpp"
+
+namespace hecnn_b200 {
+
+namespace {
+
+// 16-nibble table of the XOR swizzle: bits 4..7 of the index select a 4-bit
+// mask for bits 0..3 (images of bit 4,5,6,7: 1111, 1010, 1100, 1000).
+__device__ __forceinline__ int swz(int i) {
+    return i ^ static_cast<int>((0x1eb4d278963c5af0ull >> (4 * ((i >> 4) & 15))) & 15);
+}
+
+__device__ __forceinline__ void ct_butterfly(u64& a, u64& b, ulonglong2 w, u64 q, u64 two_q) {
+    u64 u = a;
+    if (u >= two_q) u -= two_q;
+    u64 v = mul_shoup_lazy(b, w.x, w.y, q);
+    a = u + v;
+    b = u + two_q - v;
+}
+
+__device__ __forceinline__ void gs_butterfly(u64& a, u64& b, ulonglong2 w, u64 q, u64 two_q) {
+    u64 u = a, v = b;
+    u64 s = u + v;
+    if (s >= two_q) s -= two_q;
+    a = s;
+    b = mul_shoup_lazy(u + two_q - v, w.x, w.y, q);
+}
+
+__host__ __device__ constexpr int ceil_div(int a, int b) { return (a + b - 1) / b; }
+// Size of the round that starts at local stage s of a LOGB-stage block when
+// rounds hold at most LOGE stages (balanced split, e.g. 13 -> 4,3,3,3).
+__host__ __device__ constexpr int round_size(int LOGB, int LOGE, int s) {
+    return ceil_div(LOGB - s, ceil_div(LOGB - s, LOGE));
+}
+
+// One forward round: local stages S0..S0+R-1 of block `b`, whose first global
+// stage is `c` (c = LOGN - LOGB). FROM_GLOBAL reads the block from `g`
+// instead of shared memory.
+template <int LOGB, int R, int S0, bool FROM_GLOBAL>
+__device__ __forceinline__ void fwd_round(u64* s, const u64* __restrict__ g, const ulonglong2* __restrict__ tw, u64 q,
+                                          int b, int c) {
+    constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R;
+    const u64 two_q = q << 1;
+    for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
+        const int grp = u / STRIDE, col = u % STRIDE;
+        const int base = grp * G + col;
+        u64 x[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) x[k] = FROM_GLOBAL ? g[base + k * STRIDE] : s[swz(base + k * STRIDE)];
+#pragma unroll
+        for (int rho = 0; rho < R; ++rho) {
+            const int st = c + S0 + rho;  // global stage
+            const int half = E >> (rho + 1);
+            const int tbase = (1 << st) + (b << (S0 + rho)) + (grp << rho);
+#pragma unroll
+            for (int blk = 0; blk < (1 << rho); ++blk) {
+                const ulonglong2 w = tw[tbase + blk];
+#pragma unroll
+                for (int kk = 0; kk < half; ++kk) ct_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < E; ++k) s[swz(base + k * STRIDE)] = x[k];
+    }
+}
+
+template <int LOGB, int LOGE, int S0, bool FIRST>
+__device__ __forceinline__ void fwd_rounds(u64* s, const u64* g, const ulonglong2* tw, u64 q, int b, int c) {
+    if constexpr (S0 < LOGB) {
+        constexpr int R = round_size(LOGB, LOGE, S0);
+        fwd_round<LOGB, R, S0, FIRST>(s, g, tw, q, b, c);
+        __syncthreads();
+        fwd_rounds<LOGB, LOGE, S0 + R, false>(s, g, tw, q, b, c);
+    }
+}
+
+// One inverse round: stages S0+R-1 down to S0 (GS order).
+template <int LOGB, int R, int S0>
+__device__ __forceinline__ void inv_round(u64* s, const ulonglong2* __restrict__ tw, u64 q, int b, int c) {
+    constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R;
+    const u64 two_q = q << 1;
+    for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
+        const int grp = u / STRIDE, col = u % STRIDE;
+        const int base = grp * G + col;
+        u64 x[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) x[k] = s[swz(base + k * STRIDE)];
+#pragma unroll
+        for (int rho = R - 1; rho >= 0; --rho) {
+            const int st = c + S0 + rho;
+            const int half = E >> (rho + 1);
+            const int tbase = (1 << st) + (b << (S0 + rho)) + (grp << rho);
+#pragma unroll
+            for (int blk = 0; blk < (1 << rho); ++blk) {
+                const ulonglong2 w = tw[tbase + blk];
+#pragma unroll
+                for (int kk = 0; kk < half; ++kk) gs_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < E; ++k) s[swz(base + k * STRIDE)] = x[k];
+    }
+}
+
+// Inverse rounds are the forward decomposition traversed backwards.
+template <int LOGB, int LOGE, int S0>
+__device__ __forceinline__ void inv_rounds(u64* s, const ulonglong2* tw, u64 q, int b, int c) {
+    if constexpr (S0 < LOGB) {
+        constexpr int R = round_size(LOGB, LOGE, S0);
+        inv_rounds<LOGB, LOGE, S0 + R>(s, tw, q, b, c);
+        inv_round<LOGB, R, S0>(s, tw, q, b, c);
+        __syncthreads();
+    }
+}
+
+// Block kernels: blockIdx.x = (poly * nblocks + block); limb = poly % limbs.
+template <int LOGN, int LOGB, int LOGE, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_ntt_fwd_block(DevRing R, u64* __restrict__ data, int limbs) {
+    extern __shared__ u64 smem[];
+    constexpr int B = 1 << LOGB, C = LOGN - LOGB;
+    const long long cta = blockIdx.x;
+    const long long poly = cta >> C;
+    const int b = static_cast<int>(cta & ((1 << C) - 1));
+    const int limb = static_cast<int>(poly % limbs);
+    const u64 q = R.mod[limb].q;
+    u64* g = data + (poly << LOGN) + (static_cast<long long>(b) << LOGB);
+    const ulonglong2* tw = R.fwd + (static_cast<long long>(limb) << LOGN);
+    fwd_rounds<LOGB, LOGE, 0, true>(smem, g, tw, q, b, C);
+    for (int i = threadIdx.x; i < B; i += THREADS) g[i] = reduce_4q(smem[swz(i)], q);
+}
+
+template <int LOGN, int LOGB, int LOGE, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_ntt_inv_block(DevRing R, u64* __restrict__ data, int limbs) {
+    extern __shared__ u64 smem[];
+    constexpr int B = 1 << LOGB, C = LOGN - LOGB;
+    const long long cta = blockIdx.x;
+    const long long poly = cta >> C;
+    const int b = static_cast<int>(cta & ((1 << C) - 1));
+    const int limb = static_cast<int>(poly % limbs);
+    const u64 q = R.mod[limb].q;
+    u64* g = data + (poly << LOGN) + (static_cast<long long>(b) << LOGB);
+    const ulonglong2* tw = R.inv + (static_cast<long long>(limb) << LOGN);
+    for (int i = threadIdx.x; i < B; i += THREADS) smem[swz(i)] = g[i];
+    __syncthreads();
+    inv_rounds<LOGB, LOGE, 0>(smem, tw, q, b, C);
+    if constexpr (C == 0) {
+        const ulonglong2 ni = R.n_inv[limb];
+        for (int i = threadIdx.x; i < B; i += THREADS) g[i] = reduce_2q(mul_shoup_lazy(smem[swz(i)], ni.x, ni.y, q), q);
+    } else {
+        for (int i = threadIdx.x; i < B; i += THREADS) g[i] = smem[swz(i)];  // [0,2q), columns finish
+    }
+}
+
+// Column passes for N > 2^LOGB: the C stages that couple the 2^C blocks.
+// Thread = one column (poly, col), elements col + k * (N >> C).
+template <int LOGN, int C>
+__global__ void __launch_bounds__(256) k_ntt_fwd_cols(DevRing R, u64* __restrict__ data, int limbs, long long total) {
+    constexpr int E = 1 << C, STRIDE = 1 << (LOGN - C);
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const long long poly = t >> (LOGN - C);
+    const int col = static_cast<int>(t & (STRIDE - 1));
+    const int limb = static_cast<int>(poly % limbs);
+    const u64 q = R.mod[limb].q, two_q = q << 1;
+    const ulonglong2* tw = R.fwd + (static_cast<long long>(limb) << LOGN);
+    u64* g = data + (poly << LOGN) + col;
+    u64 x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = g[static_cast<long long>(k) * STRIDE];
+#pragma unroll
+    for (int rho = 0; rho < C; ++rho) {
+        const int half = E >> (rho + 1);
+#pragma unroll
+        for (int blk = 0; blk < (1 << rho); ++blk) {
+            const ulonglong2 w = tw[(1 << rho) + blk];
+#pragma unroll
+            for (int kk = 0; kk < half; ++kk) ct_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < E; ++k) g[static_cast<long long>(k) * STRIDE] = x[k];
+}
+
+template <int LOGN, int C>
+__global__ void __launch_bounds__(256) k_ntt_inv_cols(DevRing R, u64* __restrict__ data, int limbs, long long total) {
+    constexpr int E = 1 << C, STRIDE = 1 << (LOGN - C);
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const long long poly = t >> (LOGN - C);
+    const int col = static_cast<int>(t & (STRIDE - 1));
+    const int limb = static_cast<int>(poly % limbs);
+    const u64 q = R.mod[limb].q, two_q = q << 1;
+    const ulonglong2* tw = R.inv + (static_cast<long long>(limb) << LOGN);
+    u64* g = data + (poly << LOGN) + col;
+    u64 x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = g[static_cast<long long>(k) * STRIDE];
+#pragma unroll
+    for (int rho = C - 1; rho >= 0; --rho) {
+        const int half = E >> (rho + 1);
+#pragma unroll
+        for (int blk = 0; blk < (1 << rho); ++blk) {
+            const ulonglong2 w = tw[(1 << rho) + blk];
+#pragma unroll
+            for (int kk = 0; kk < half; ++kk) gs_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
+        }
+    }
+    const ulonglong2 ni = R.n_inv[limb];
+#pragma unroll
+    for (int k = 0; k < E; ++k) g[static_cast<long long>(k) * STRIDE] = reduce_2q(mul_shoup_lazy(x[k], ni.x, ni.y, q), q);
+}
+
+template <class K>
+void set_smem(K kernel, int bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+template <int LOGN>
+struct NttPlan {
+    static constexpr int LOGB = LOGN <= 14 ? LOGN : 13;
+    static constexpr int C = LOGN - LOGB;
+    static constexpr int LOGE = LOGB >= 8 ? 4 : 3;
+    static constexpr int UNITS = (1 << LOGB) >> LOGE;
+    static constexpr int THREADS = UNITS >= 512 ? 512 : (UNITS >= 32 ? UNITS : 32);
+};
+
+template <int LOGN>
+void run_forward(const DevRing& R, u64* data, int limbs, std::size_t polys, const Launch& L) {
+    using P = NttPlan<LOGN>;
+    if constexpr (P::C > 0) {
+        long long total = static_cast<long long>(polys) << (LOGN - P::C);
+        k_ntt_fwd_cols<LOGN, P::C><<<static_cast<unsigned>((total + 255) / 256), 256, 0, L.stream>>>(R, data, limbs, total);
+        L.count();
+    }
+    auto kern = k_ntt_fwd_block<LOGN, P::LOGB, P::LOGE, P::THREADS>;
+    const int smem = (1 << P::LOGB) * 8;
+    static bool init = (set_smem(kern, smem), true);
+    (void)init;
+    kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, data, limbs);
+    L.count();
+}
+
+template <int LOGN>
+void run_inverse(const DevRing& R, u64* data, int limbs, std::size_t polys, const Launch& L) {
+    using P = NttPlan<LOGN>;
+    auto kern = k_ntt_inv_block<LOGN, P::LOGB, P::LOGE, P::THREADS>;
+    const int smem = (1 << P::LOGB) * 8;
+    static bool init = (set_smem(kern, smem), true);
+    (void)init;
+    kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, data, limbs);
+    L.count();
+    if constexpr (P::C > 0) {
+        long long total = static_cast<long long>(polys) << (LOGN - P::C);
+        k_ntt_inv_cols<LOGN, P::C><<<static_cast<unsigned>((total + 255) / 256), 256, 0, L.stream>>>(R, data, limbs, total);
+        L.count();
+    }
+}
+
+template <bool FWD>
+void dispatch(const DevRing& R, u64* data, int level, std::size_t count, const Launch& L) {
+    const int limbs = level + 1;
+    const std::size_t polys = count * static_cast<std::size_t>(limbs);
+    if (polys == 0) return;
+#define HECNN_NTT_CASE(LG)                                             \
+    case LG:                                                          \
+        if (FWD) run_forward<LG>(R, data, limbs, polys, L);           \
+        else run_inverse<LG>(R, data, limbs, polys, L);               \
+        break;
+    switch (R.logn) {
+        HECNN_NTT_CASE(3)
+        HECNN_NTT_CASE(4)
+        HECNN_NTT_CASE(5)
+        HECNN_NTT_CASE(6)
+        HECNN_NTT_CASE(7)
+        HECNN_NTT_CASE(8)
+        HECNN_NTT_CASE(9)
+        HECNN_NTT_CASE(10)
+        HECNN_NTT_CASE(11)
+        HECNN_NTT_CASE(12)
+        HECNN_NTT_CASE(13)
+        HECNN_NTT_CASE(14)
+        HECNN_NTT_CASE(15)
+        HECNN_NTT_CASE(16)
+        default: throw std::invalid_argument("ntt: ring degree outside 2^3..2^16 is not supported on the device");
+    }
+#undef HECNN_NTT_CASE
+    check_launch(FWD ? "ntt_forward" : "ntt_inverse");
+}
+
+}  // namespace
+
+void ntt_forward(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L) {
+    dispatch<true>(R, polys, level, count, L);
+}
+
+void ntt_inverse(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L) {
+    dispatch<false>(R, polys, level, count, L);
+}
+
+}  // namespace hecnn_b200

@@ -1,0 +1,342 @@
+// Elementwise RNS kernels (K3, K7, K9, K11/K12 pieces in SURVEY.md §2.3).
+//
+// All of these are HBM-bound streams over limb-major polynomials. Grid:
+// blockIdx.x = (poly, limb) row, blockIdx.y * 256 + threadIdx.x = coefficient,
+// so a warp reads 256 contiguous bytes of one limb and the limb's modulus
+// constants are uniform across the CTA.
+
+#include <stdexcept>
+#include <string>
+
+#include "kernels.hpp"
+
+namespace hecnn_b200 {
+
+void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA launch failed in ") + what + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+constexpr int TPB = 256;
+
+inline dim3 rows_grid(std::size_t rows, int n) {
+    return dim3(static_cast<unsigned>(rows), static_cast<unsigned>((n + TPB - 1) / TPB));
+}
+
+__global__ void k_elementwise(DevRing R, int op, const u64* __restrict__ a, const u64* __restrict__ b,
+                              u64* __restrict__ out, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const ModConst m = R.mod[row % limbs];
+    const long long e = row * R.n + j;
+    u64 r;
+    switch (op) {
+        case 0: r = add_mod(a[e], b[e], m.q); break;
+        case 1: r = sub_mod(a[e], b[e], m.q); break;
+        case 2: r = neg_mod(a[e], m.q); break;
+        case 3: r = mul_mod(a[e], b[e], m); break;
+        default: r = add_mod(out[e], mul_mod(a[e], b[e], m), m.q); break;
+    }
+    out[e] = r;
+}
+
+// rescale_poly (ring.hpp:419-442): out_i = (a_i - centre(a_l)) * p_l^{-1} mod q_i,
+// centre(v) = v if v <= floor(p_l/2) else v - p_l. One thread per (poly, j)
+// walks the l output limbs; a_l is read once.
+__global__ void k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long poly = blockIdx.x;
+    const u64* src = in + poly * (level + 1) * R.n;
+    u64* dst = out + poly * level * R.n;
+    const u64 p = R.mod[level].q;
+    const u64 v = src[static_cast<long long>(level) * R.n + j];
+    const bool upper = v > (p >> 1);
+    for (int i = 0; i < level; ++i) {
+        const ModConst m = R.mod[i];
+        u64 centred = v < m.q ? v : reduce128(v, 0, m);
+        if (upper) centred = sub_mod(centred, R.p_mod[level * R.limbs + i], m.q);
+        const ulonglong2 inv = R.inv_dropped[level * R.limbs + i];
+        dst[static_cast<long long>(i) * R.n + j] = mul_shoup(sub_mod(src[static_cast<long long>(i) * R.n + j], centred, m.q), inv.x, inv.y, m.q);
+    }
+}
+
+__global__ void k_drop_limbs(const u64* __restrict__ in, u64* __restrict__ out, int n, int limbs_in, int limbs_out) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= n) return;
+    const long long row = blockIdx.x;  // output row = poly * limbs_out + i
+    const long long poly = row / limbs_out;
+    const int i = static_cast<int>(row % limbs_out);
+    out[row * n + j] = in[(poly * limbs_in + i) * n + j];
+}
+
+// CkksEngine::mul tensor step (ckks.hpp:320-327): d0 = x0 y0, d1 = x0 y1 + x1 y0, d2 = x1 y1
+__global__ void k_tensor_mul(DevRing R, const u64* __restrict__ fx, const u64* __restrict__ fy, u64* __restrict__ d01,
+                             u64* __restrict__ d2, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;  // ct * limbs + i
+    const long long ct = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    const ModConst m = R.mod[i];
+    const long long o0 = ((ct * 2) * limbs + i) * R.n + j, o1 = o0 + static_cast<long long>(limbs) * R.n;
+    const u64 x0 = fx[o0], x1 = fx[o1], y0 = fy[o0], y1 = fy[o1];
+    d01[o0] = mul_mod(x0, y0, m);
+    d01[o1] = add_mod(mul_mod(x0, y1, m), mul_mod(x1, y0, m), m.q);
+    d2[row * R.n + j] = mul_mod(x1, y1, m);
+}
+
+// CkksEngine::square tensor step (ckks.hpp:349-354): d1 = 2 x0 x1
+__global__ void k_tensor_square(DevRing R, const u64* __restrict__ fx, u64* __restrict__ d01, u64* __restrict__ d2,
+                                int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const long long ct = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    const ModConst m = R.mod[i];
+    const long long o0 = ((ct * 2) * limbs + i) * R.n + j, o1 = o0 + static_cast<long long>(limbs) * R.n;
+    const u64 x0 = fx[o0], x1 = fx[o1];
+    d01[o0] = mul_mod(x0, x0, m);
+    const u64 c = mul_mod(x0, x1, m);
+    d01[o1] = add_mod(c, c, m.q);
+    d2[row * R.n + j] = mul_mod(x1, x1, m);
+}
+
+__global__ void k_scalar_mul(DevRing R, const u64* __restrict__ in, const ulonglong2* __restrict__ consts,
+                             u64* __restrict__ out, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const int i = static_cast<int>(row % limbs);
+    const u64 q = R.mod[i].q;
+    const ulonglong2 c = consts[i];
+    out[row * R.n + j] = mul_shoup(in[row * R.n + j], c.x, c.y, q);
+}
+
+__global__ void k_add_coeff0(DevRing R, u64* __restrict__ cts, const u64* __restrict__ consts, int limbs,
+                             long long count) {
+    const long long t = static_cast<long long>(blockIdx.x) * TPB + threadIdx.x;
+    if (t >= count * limbs) return;
+    const long long ct = t / limbs;
+    const int i = static_cast<int>(t % limbs);
+    u64* p = cts + ((ct * 2) * limbs + i) * R.n;
+    p[0] = add_mod(p[0], consts[i], R.mod[i].q);
+}
+
+__global__ void k_small_to_rns(DevRing R, const signed char* __restrict__ s, u64* __restrict__ out, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const long long poly = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    const u64 q = R.mod[i].q;
+    const int v = s[poly * R.n + j];
+    out[row * R.n + j] = v >= 0 ? static_cast<u64>(v) : q - static_cast<u64>(-v);
+}
+
+__global__ void k_i64_to_rns(DevRing R, const long long* __restrict__ s, u64* __restrict__ out, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const long long poly = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    out[row * R.n + j] = from_signed(s[poly * R.n + j], R.mod[i].q);
+}
+
+// encrypt (ckks.hpp:252-259): (r_hat * pk.b, r_hat * pk.a), NTT domain
+__global__ void k_mul_by_key(DevRing R, const u64* __restrict__ rt, const u64* __restrict__ pk, long long pk_limbs,
+                             u64* __restrict__ out, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const long long ct = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    const ModConst m = R.mod[i];
+    const u64 r = rt[row * R.n + j];
+    const long long o0 = ((ct * 2) * limbs + i) * R.n + j;
+    out[o0] = mul_mod(r, pk[static_cast<long long>(i) * R.n + j], m);
+    out[o0 + static_cast<long long>(limbs) * R.n] = mul_mod(r, pk[(pk_limbs + i) * R.n + j], m);
+}
+
+__device__ __forceinline__ u64 small_res(int v, u64 q) { return v >= 0 ? static_cast<u64>(v) : q - static_cast<u64>(-v); }
+
+// encrypt (ckks.hpp:255-259): c0 += e0 (+ m), c1 += e1
+__global__ void k_add_noise_msg(DevRing R, u64* __restrict__ cts, const signed char* __restrict__ e0,
+                                const signed char* __restrict__ e1, const u64* __restrict__ msg, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const long long ct = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    const u64 q = R.mod[i].q;
+    const long long o0 = ((ct * 2) * limbs + i) * R.n + j, o1 = o0 + static_cast<long long>(limbs) * R.n;
+    u64 c0 = add_mod(cts[o0], small_res(e0[ct * R.n + j], q), q);
+    if (msg) c0 = add_mod(c0, msg[row * R.n + j], q);
+    cts[o0] = c0;
+    cts[o1] = add_mod(cts[o1], small_res(e1[ct * R.n + j], q), q);
+}
+
+__global__ void k_mul_secret(DevRing R, u64* __restrict__ t, const u64* __restrict__ s_ntt, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const int i = static_cast<int>(row % limbs);
+    t[row * R.n + j] = mul_mod(t[row * R.n + j], s_ntt[static_cast<long long>(i) * R.n + j], R.mod[i]);
+}
+
+__global__ void k_add_c0(DevRing R, const u64* __restrict__ cts, u64* __restrict__ t, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const long long ct = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    const long long o0 = ((ct * 2) * limbs + i) * R.n + j;
+    t[row * R.n + j] = add_mod(cts[o0], t[row * R.n + j], R.mod[i].q);
+}
+
+// floor(w 2^64 / q): Barrett estimate (w * ratio) >> 64, then exact correction
+__global__ void k_shoup(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const ModConst m = R.mod[row % limbs];
+    const u64 w = in[row * R.n + j];
+    u64 est = w * m.ratio_hi + mulhi(w, m.ratio_lo);
+    for (int it = 0; it < 4; ++it) {
+        // remainder r = w*2^64 - est*q as a 128-bit value; bump est while r >= q
+        const u64 plo = est * m.q, phi = mulhi(est, m.q);
+        const u64 rlo = 0 - plo;
+        const u64 rhi = w - phi - (plo != 0 ? 1 : 0);
+        if (rhi == 0 && rlo < m.q) break;
+        ++est;
+    }
+    out[row * R.n + j] = est;
+}
+
+}  // namespace
+
+void shoup_table(const DevRing& R, const u64* in, u64* out, int limbs, std::size_t count, const Launch& L) {
+    const std::size_t rows = count * limbs;
+    if (!rows) return;
+    k_shoup<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, in, out, limbs);
+    L.count();
+    check_launch("shoup_table");
+}
+
+void poly_elementwise(const DevRing& R, EwOp op, const u64* a, const u64* b, u64* out, int level, std::size_t count,
+                      const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_elementwise<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, static_cast<int>(op), a, b, out, level + 1);
+    L.count();
+    check_launch("poly_elementwise");
+}
+
+void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L) {
+    if (!count) return;
+    k_rescale<<<rows_grid(count, R.n), TPB, 0, L.stream>>>(R, in, out, level);
+    L.count();
+    check_launch("rescale");
+}
+
+void drop_limbs(const DevRing& R, const u64* in, u64* out, int level, int to_level, std::size_t count,
+                const Launch& L) {
+    const std::size_t rows = count * (to_level + 1);
+    if (!rows) return;
+    k_drop_limbs<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(in, out, R.n, level + 1, to_level + 1);
+    L.count();
+    check_launch("drop_limbs");
+}
+
+void tensor_mul(const DevRing& R, const u64* fx, const u64* fy, u64* d01, u64* d2, int level, std::size_t count,
+                const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_tensor_mul<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, fx, fy, d01, d2, level + 1);
+    L.count();
+    check_launch("tensor_mul");
+}
+
+void tensor_square(const DevRing& R, const u64* fx, u64* d01, u64* d2, int level, std::size_t count,
+                   const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_tensor_square<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, fx, d01, d2, level + 1);
+    L.count();
+    check_launch("tensor_square");
+}
+
+void scalar_mul(const DevRing& R, const u64* in, const ulonglong2* consts, u64* out, int level, std::size_t count,
+                const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_scalar_mul<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, in, consts, out, level + 1);
+    L.count();
+    check_launch("scalar_mul");
+}
+
+void add_coeff0(const DevRing& R, u64* cts, const u64* consts, int level, std::size_t count, const Launch& L) {
+    const long long total = static_cast<long long>(count) * (level + 1);
+    if (!total) return;
+    k_add_coeff0<<<static_cast<unsigned>((total + TPB - 1) / TPB), TPB, 0, L.stream>>>(R, cts, consts, level + 1,
+                                                                                       static_cast<long long>(count));
+    L.count();
+    check_launch("add_coeff0");
+}
+
+void small_to_rns(const DevRing& R, const signed char* s, u64* out, int level, std::size_t count, const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_small_to_rns<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, s, out, level + 1);
+    L.count();
+    check_launch("small_to_rns");
+}
+
+void i64_to_rns(const DevRing& R, const long long* s, u64* out, int level, std::size_t count, const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_i64_to_rns<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, s, out, level + 1);
+    L.count();
+    check_launch("i64_to_rns");
+}
+
+void mul_by_key(const DevRing& R, const u64* rt, const u64* pk, std::size_t pk_limbs, u64* out, int level,
+                std::size_t count, const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_mul_by_key<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, rt, pk, static_cast<long long>(pk_limbs), out,
+                                                             level + 1);
+    L.count();
+    check_launch("mul_by_key");
+}
+
+void add_noise_msg(const DevRing& R, u64* ct, const signed char* e0, const signed char* e1, const u64* m, int level,
+                   std::size_t count, const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_add_noise_msg<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, ct, e0, e1, m, level + 1);
+    L.count();
+    check_launch("add_noise_msg");
+}
+
+void mul_secret(const DevRing& R, u64* t, const u64* s_ntt, int level, std::size_t count, const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_mul_secret<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, t, s_ntt, level + 1);
+    L.count();
+    check_launch("mul_secret");
+}
+
+void add_c0(const DevRing& R, const u64* ct, u64* t, int level, std::size_t count, const Launch& L) {
+    const std::size_t rows = count * (level + 1);
+    if (!rows) return;
+    k_add_c0<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, ct, t, level + 1);
+    L.count();
+    check_launch("add_c0");
+}
+
+}  // namespace hecnn_b200
