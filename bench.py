@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the encrypted-CNN hot path (BASELINE.json north_star).
+
+Default workload (N=1): SURVEY §8(d) C4 -- the CIFAR-10-shaped CNN with the
+degree-2 polynomial ReLU on encrypted synthetic 32x32x3 images, preset
+net-n8192-d8 (4096 images packed in the slots of one ciphertext set). C5
+(AlexNet-like at 64x64) does not fit one GPU without the streaming executor
+(DESIGN.md §7), so C4 is the largest single-GPU config; C2's NTT and HE-mul
+ops/s are reported alongside in the same line.
+
+A step = forward_encrypted over one set (4096 images) with the input
+ciphertexts resident in HBM (`value`); `e2e` repeats it through the public
+API from pinned host buffers: H2D of the input ciphertexts, forward, D2H of
+the output ciphertexts. Under torchrun each rank evaluates its own set (batch
+sharding, weak scaling) and the output ciphertexts are gathered to rank 0 with
+one NCCL all_gather -- the only collective.
+
+--impl reference times the reference's own CPU path (oracle/_ref, compiled
+from the unmodified reference headers) on the host cores: the same C4 stack
+on an 8x8 crop of the images, extrapolated to the full 32x32 set layer by
+layer from the reference's own per-layer timings and exact op-count ratios.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "encrypted images/sec (AlexNet-like COWC) at 1/2/4/8 B200; NTT & HE-mul ops/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def c4_spec(hb, image=32):
+    spec = hb.ModelSpec(hb.Shape.spatial(image, image, 3))
+    spec.activations["relu-poly2"] = hb.relu_default_surrogate()
+    spec.layers = [hb.LayerSpec.conv2d(16, 3, 3), hb.LayerSpec.activation("relu-poly2"), hb.LayerSpec.avg_pool2d(2),
+                   hb.LayerSpec.conv2d(32, 3, 3), hb.LayerSpec.activation("relu-poly2"), hb.LayerSpec.dense(10)]
+    return hb.glorot_weights(spec, 4)
+
+
+def c3_spec(hb):
+    spec = hb.ModelSpec(hb.Shape.spatial(28, 28, 1))
+    spec.activations["square"] = hb.PolyActivation([0.0, 0.0, 1.0], 1.0, "square")
+    spec.layers = [hb.LayerSpec.zero_pad2d(1), hb.LayerSpec.conv2d(5, 5, 5, stride=2, valid=True),
+                   hb.LayerSpec.activation("square"), hb.LayerSpec.dense(100), hb.LayerSpec.activation("square"),
+                   hb.LayerSpec.dense(10)]
+    spec = hb.glorot_weights(spec, 4)
+    for i in (1, 3, 5):
+        spec.weights[i] = spec.weights[i] * 0.5
+    return spec
+
+
+# ---------------------------------------------------------------- helpers
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "200"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# ---------------------------------------------------------------- reference (CPU) path
+
+def reference_c4_images_per_s(threads):
+    """The reference's forward_encrypted on an 8x8 crop of the C4 images,
+    extrapolated per layer to the full 32x32 set by exact op-count ratios
+    (conv: output cells x valid taps; activation/pool: cells; dense: inputs)."""
+    import paper_1911_11377_b200 as hb
+    from oracle import ref
+
+    p = hb.preset_params("net-n8192-d8")
+    crop, full = 8, 32
+    spec = c4_spec(hb, crop)
+    r = ref.RefEngine.from_params(p).keygen(1)
+    rng = np.random.default_rng(3)
+    data = rng.uniform(0, 1, size=(p.n // 2, spec.input.positions()))
+    x = r.encrypt_tensor(data, spec.input, seed=11, threads=threads)
+    t0 = time.perf_counter()
+    _, secs = r.forward_encrypted(spec, x, seed=13, threads=threads)
+    wall = time.perf_counter() - t0
+
+    def taps(side):  # valid 3x3 same-conv taps summed over output pixels of a side x side map
+        per = [min(3, i + 2, side - i + 1, side) for i in range(side)]
+        return sum(per) ** 2
+
+    ratios = [16.0 * taps(full) / (16.0 * taps(crop)) * 1.0,   # conv1 (cells x taps, c_out same)
+              (full * full) / (crop * crop),                 # act1
+              (full * full) / (crop * crop),                 # pool1
+              taps(full // 2) / taps(crop // 2),             # conv2
+              (full * full) / (crop * crop),                 # act2
+              (full * full) / (crop * crop)]                 # dense: in_f ratio
+    est = float(sum(s * k for s, k in zip(secs, ratios)))
+    return p.n // 2 / est, est, wall, [float(s) for s in secs]
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, est, wall, secs = reference_c4_images_per_s(threads)
+        if i >= args.warmup:
+            vals.append((v, est, wall))
+    value = float(np.median([v for v, _, _ in vals]))
+    ms = float(np.median([e for _, e, _ in vals])) * 1e3
+    sample = "C4 stack on an 8x8 crop (1/16 of the cells), per-layer op-count extrapolation to 32x32; 4096 images/set"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "C4 CIFAR-10-shaped CNN + poly ReLU, net-n8192-d8, 4096 encrypted 32x32x3 "
+                                   "images per set", "parallelism": "host threads (reference parallel_for)"},
+            "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our path
+
+def microbench(hb, eng_dev, n=16384, count=256):
+    """C2: NTT/INTT and HE-mul (tensor + relinearize + rescale) throughput at
+    chain [60, 40 x 8], uniform-random residues as synthetic ciphertexts."""
+    import torch
+    p = hb.CkksParams(n, hb.find_chain(n, [60] + [40] * 8), 2.0 ** 40)
+    eng = hb.CkksEngine(p, device=eng_dev).keygen(1)
+    eng.set_stream(torch.cuda.current_stream().cuda_stream)
+    L = p.top_level
+    rng = np.random.default_rng(5)
+    words = np.empty((count, 2, L + 1, n), dtype=np.uint64)
+    for i, q in enumerate(p.primes):
+        words[:, :, i, :] = rng.integers(0, q, size=(count, 2, n), dtype=np.uint64)
+    x = eng.tensor_from_words(words, L, p.scale)
+    y = eng.tensor_from_words(words[::-1].copy(), L, p.scale)
+    dptr = x.device_ptr()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import ctypes
+    polys = 2 * count
+    for _ in range(2):
+        hb._check(hb.lib().hecnn_ntt_forward(eng.ctx, ctypes.c_void_p(dptr), ctypes.c_size_t(L), ctypes.c_size_t(polys)))
+        hb._check(hb.lib().hecnn_ntt_inverse(eng.ctx, ctypes.c_void_p(dptr), ctypes.c_size_t(L), ctypes.c_size_t(polys)))
+    torch.cuda.synchronize()
+    reps = 5
+    s.record()
+    for _ in range(reps):
+        hb._check(hb.lib().hecnn_ntt_forward(eng.ctx, ctypes.c_void_p(dptr), ctypes.c_size_t(L), ctypes.c_size_t(polys)))
+        hb._check(hb.lib().hecnn_ntt_inverse(eng.ctx, ctypes.c_void_p(dptr), ctypes.c_size_t(L), ctypes.c_size_t(polys)))
+    e.record()
+    torch.cuda.synchronize()
+    ntt_s = s.elapsed_time(e) / 1e3
+    ntt_ops = reps * 2 * polys * (L + 1) / ntt_s
+    eng.mul(x, y)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(2):
+        z = eng.mul(x, y)
+    e.record()
+    torch.cuda.synchronize()
+    mul_s = s.elapsed_time(e) / 1e3
+    del z
+    res = {"n": n, "chain": "[60,40x8]", "level": L, "ciphertexts": count,
+           "ntt_ops_per_s": ntt_ops, "he_mul_ops_per_s": 2 * count / mul_s}
+    eng.close()
+    return res
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1911_11377_b200 as hb
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+
+    p = hb.preset_params("net-n8192-d8")
+    batch = p.n // 2
+    spec = c4_spec(hb)
+    eng = hb.CkksEngine(p, device=local).keygen(1)
+    eng.set_stream(stream.cuda_stream)
+    model = eng.model(spec)
+    rng = np.random.default_rng(3 + rank)
+    data = rng.uniform(0, 1, size=(batch, spec.input.positions()))
+    x = eng.encrypt_tensor(data, seed=11 + rank, shape=spec.input)     # client side, untimed
+    in_words = x.words()
+    host_in = torch.from_numpy(in_words.reshape(-1).view(np.int64)).pin_memory()
+    h2d_bytes = in_words.nbytes
+
+    for _ in range(args.warmup):
+        y = hb.forward_encrypted(model, x, eng, seed=13)
+    torch.cuda.synchronize()
+    out_cells, out_level = y.cells, y.level
+    out_words_n = y.words().size
+    host_out = torch.empty(out_words_n, dtype=torch.int64).pin_memory()
+
+    # ---- device-resident timed region
+    launches0 = eng.launches()
+    eng.profile_reset()
+    eng.profile(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        s.record(stream)
+        for _ in range(args.steps):
+            y = hb.forward_encrypted(model, x, eng, seed=13)
+        e.record(stream)
+        torch.cuda.synchronize()
+    eng.profile(False)
+    prof = eng.profile_read()
+    launches = eng.launches() - launches0
+    dev_s = s.elapsed_time(e) / 1e3
+    gather_words = torch.empty(out_words_n, dtype=torch.int64, device=f"cuda:{local}")
+    eng.copy_to_device(y, gather_words.data_ptr())
+    if world > 1:
+        t = torch.tensor([dev_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+        # the only collective: gather every rank's output ciphertexts (NCCL)
+        gathered = [torch.empty_like(gather_words) for _ in range(world)]
+        dist.all_gather(gathered, gather_words)
+        torch.cuda.synchronize()
+
+    # ---- end to end through the public API from pinned host memory
+    xe = eng.empty_tensor(x.cells, x.level, x.scale)
+    xe.set_shape(spec.input, batch)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s.record(stream)
+    for _ in range(args.steps):
+        eng.upload_into(xe, host_in.data_ptr())
+        ye = hb.forward_encrypted(model, xe, eng, seed=13)
+        eng.download_into(ye, host_out.data_ptr())
+    e.record(stream)
+    torch.cuda.synchronize()
+    e2e_s = s.elapsed_time(e) / 1e3
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    assert np.array_equal(host_out.numpy().view(np.uint64), y.words().reshape(-1)), "e2e output differs"
+
+    images = world * batch * args.steps
+    line = None
+    if rank == 0:
+        # dominant kernel and its roofline
+        pk = peaks()
+        int_peak = eng.modmul_peak()
+        top = max(prof.items(), key=lambda kv: kv[1]["ms"])
+        name, st = top
+        avg_ms = st["ms"] / max(st["launches"], 1)
+        ops_per_launch = st["ops"] / max(st["launches"], 1)
+        bytes_per_launch = st["bytes"] / max(st["launches"], 1)
+        achieved_ops = ops_per_launch / (avg_ms / 1e3)
+        achieved_gbs = bytes_per_launch / (avg_ms / 1e3) / 1e9
+        int_bound = achieved_ops / int_peak >= achieved_gbs / pk["hbm_gbs"]
+        roofline = {
+            "kernel": name, "bound": "int" if int_bound else "hbm",
+            "achieved": achieved_ops / 1e9 if int_bound else achieved_gbs,
+            "peak": int_peak / 1e9 if int_bound else pk["hbm_gbs"],
+            "unit": "Gmodmul/s" if int_bound else "GB/s",
+            "frac": (achieved_ops / int_peak) if int_bound else achieved_gbs / pk["hbm_gbs"],
+            "traffic": None,
+            "ops_per_launch": ops_per_launch, "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+            "share_of_step": st["ms"] / 1e3 / dev_s,
+            "peak_source": "int: live chained-Shoup-modmul probe (hecnn_modmul_peak); hbm: MEASURED_PEAKS.json",
+            "hbm_view": {"achieved_gbs": achieved_gbs, "peak_gbs": pk["hbm_gbs"], "frac": achieved_gbs / pk["hbm_gbs"]},
+        }
+        kernels = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                       "gmodmul_s": (v["ops"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0,
+                       "gb_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0}
+                   for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+        mb = microbench(hb, local) if not args.no_micro else None
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import ref
+            if ref.available():
+                v, est, wall, _ = reference_c4_images_per_s(os.cpu_count() or 1)
+                cpu = {"value": v, "unit": "images/s", "cores": os.cpu_count() or 1, "kind": "reference",
+                       "sample": f"reference forward_encrypted on an 8x8 crop of C4 ({wall:.1f}s wall), per-layer "
+                                 "op-count extrapolation to the 32x32 set"}
+        line = {"metric": METRIC, "value": images / dev_s, "unit": "images/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic (uniform [0,1] 32x32x3 images, numpy Glorot weights)",
+                "config": {"workload": "C4 CIFAR-10-shaped CNN + poly ReLU (conv16-act-pool-conv32-act-dense10), "
+                                       "net-n8192-d8, 4096 encrypted images per set per GPU",
+                           "preset": "net-n8192-d8", "images_per_set": batch, "sets_per_gpu_per_step": 1,
+                           "parallelism": f"dp{world} (batch sharding; NCCL all_gather of output ciphertexts only)",
+                           "l2": f"inputs larger than L2 ({in_words.nbytes / 2**30:.2f} GiB of input ciphertexts)",
+                           "profiling": "per-kernel CUDA events on the launching stream inside the timed region"},
+                "clocks": clk.summary(),
+                "e2e": {"value": images / e2e_s, "unit": "images/s", "h2d_bytes_per_step": h2d_bytes,
+                        "d2h_bytes_per_step": out_words_n * 8},
+                "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+                "output": {"cells": out_cells, "level": out_level},
+                "microbench_c2": mb, "kernels": kernels}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-micro", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

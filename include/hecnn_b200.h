@@ -53,6 +53,17 @@ int hecnn_abi_version(void);
  * p == 1 (mod 2n) not already taken. */
 int hecnn_find_chain(size_t n, const int* prime_bits, size_t count, uint64_t* primes_out);
 
+/* ---- host-only numerics (no device needed) -----------------------------
+ * encode_real (ckks.hpp:105-129): residues [(level+1)][n] of the encoding. */
+int hecnn_host_encode_real(size_t n, const uint64_t* primes, size_t nprimes, const double* values, size_t len,
+                           double scale, size_t level, uint64_t* out);
+/* decode (ckks.hpp:142-154): real parts of the first `count` slots. */
+int hecnn_host_decode_real(size_t n, const uint64_t* primes, size_t nprimes, const uint64_t* poly, size_t level,
+                           double scale, double* out, size_t count);
+/* make_encryption_randomness (ckks.hpp:238-244): signed coefficients [n]. */
+int hecnn_host_encryption_randomness(size_t n, double sigma, int degenerate_noise, uint64_t seed, int64_t* r,
+                                     int64_t* e0, int64_t* e1);
+
 /* ---- context: RingContext (ring.hpp:171-237) + CkksEngine ctor
  * (ckks.hpp:79-93). Builds NTT/CRT/rescale tables on the host and uploads
  * them to `device`. */
@@ -66,6 +77,15 @@ int hecnn_context_info(const hecnn_context* ctx, size_t* n, size_t* top_level, d
 int hecnn_relin_digits(const hecnn_context* ctx, size_t level, size_t* digits);
 /* Number of kernel launches issued by this context since creation. */
 int hecnn_launch_count(const hecnn_context* ctx, uint64_t* launches);
+
+/* ---- measurement (no reference analogue) ------------------------------
+ * Per-kernel timing with CUDA events on the context stream (enabled region
+ * only); read returns JSON {"kernel": {"ms": total, "launches": k}, ...}. */
+int hecnn_profile_enable(hecnn_context* ctx, int on);
+int hecnn_profile_reset(hecnn_context* ctx);
+int hecnn_profile_read(hecnn_context* ctx, char* buf, size_t len);
+/* Integer-pipe roofline probe: chained 64-bit Shoup modular multiplies/s. */
+int hecnn_modmul_peak(hecnn_context* ctx, double* modmul_per_s);
 
 /* ---- keys: CkksEngine::keygen (ckks.hpp:200-236). Randomness is sampled on
  * the host (mt19937_64 + libm, bit-identical to the reference); NTTs and
@@ -121,6 +141,8 @@ int hecnn_tensor_shape(const hecnn_tensor* t, int* flat, size_t* h, size_t* w, s
 int hecnn_tensor_data(const hecnn_tensor* t, uint64_t** dptr);
 int hecnn_tensor_upload(hecnn_context* ctx, hecnn_tensor* t, const uint64_t* host);
 int hecnn_tensor_download(hecnn_context* ctx, const hecnn_tensor* t, uint64_t* host);
+/* device-to-device copy of the words (e.g. into an NCCL buffer) */
+int hecnn_tensor_copy_to_device(hecnn_context* ctx, const hecnn_tensor* t, void* dst);
 
 /* encrypt_tensor (tensor.hpp:77-94): data is [batch][positions] (TensorPlain
  * layout). Encode on the host (ckks.hpp:105-123), randomness on the host

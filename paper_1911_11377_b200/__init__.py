@@ -44,9 +44,85 @@ EXPORTED_SYMBOLS = (
     "hecnn_decrypt_tensor", "hecnn_ct_add", "hecnn_ct_sub", "hecnn_ct_mul", "hecnn_ct_square", "hecnn_ct_rescale",
     "hecnn_ct_mod_switch", "hecnn_ct_mul_const", "hecnn_ct_add_const", "hecnn_eval_activation",
     "hecnn_model_create", "hecnn_model_destroy", "hecnn_model_depth_cost", "hecnn_forward_encrypted",
+    "hecnn_profile_enable", "hecnn_profile_reset", "hecnn_profile_read", "hecnn_modmul_peak",
+    "hecnn_tensor_copy_to_device", "hecnn_host_encode_real", "hecnn_host_decode_real",
+    "hecnn_host_encryption_randomness",
 )
 
 _lib = None
+
+_V, _SZ, _U32, _U64, _D, _I = (ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double,
+                                ctypes.c_int)
+_PV = ctypes.POINTER(ctypes.c_void_p)
+_PSZ = ctypes.POINTER(ctypes.c_size_t)
+_PU64 = ctypes.POINTER(ctypes.c_uint64)
+_PD = ctypes.POINTER(ctypes.c_double)
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+# argument types of every C-ABI entry (include/hecnn_b200.h); pointers to
+# opaque handles and device memory travel as void*
+_SIGNATURES = {
+    "hecnn_abi_version": [],
+    "hecnn_host_encode_real": [_SZ, _PU64, _SZ, _PD, _SZ, _D, _SZ, _PU64],
+    "hecnn_host_decode_real": [_SZ, _PU64, _SZ, _PU64, _SZ, _D, _PD, _SZ],
+    "hecnn_host_encryption_randomness": [_SZ, _D, _I, _U64, _PI64, _PI64, _PI64],
+    "hecnn_find_chain": [_SZ, ctypes.POINTER(ctypes.c_int), _SZ, _PU64],
+    "hecnn_context_create": [_SZ, _PU64, _SZ, _D, _D, _I, _I, _PV],
+    "hecnn_context_destroy": [_V],
+    "hecnn_context_set_stream": [_V, _V],
+    "hecnn_context_synchronize": [_V],
+    "hecnn_context_info": [_V, _PSZ, _PSZ, _PD],
+    "hecnn_relin_digits": [_V, _SZ, _PSZ],
+    "hecnn_launch_count": [_V, _PU64],
+    "hecnn_profile_enable": [_V, _I],
+    "hecnn_profile_reset": [_V],
+    "hecnn_profile_read": [_V, ctypes.c_char_p, _SZ],
+    "hecnn_modmul_peak": [_V, _PD],
+    "hecnn_keygen": [_V, _U64],
+    "hecnn_import_keys": [_V, _PU64, _PU64, _PU64, _PU64, _SZ],
+    "hecnn_export_secret_key": [_V, _PU64],
+    "hecnn_export_public_key": [_V, _PU64, _PU64],
+    "hecnn_eval_key_digits": [_V, _PSZ],
+    "hecnn_export_eval_key": [_V, _PU64],
+    "hecnn_device_alloc": [_V, _SZ, _PV],
+    "hecnn_device_free": [_V, _V],
+    "hecnn_memcpy_h2d": [_V, _V, _V, _SZ],
+    "hecnn_memcpy_d2h": [_V, _V, _V, _SZ],
+    "hecnn_ntt_forward": [_V, _V, _SZ, _SZ],
+    "hecnn_ntt_inverse": [_V, _V, _SZ, _SZ],
+    "hecnn_poly_add": [_V, _V, _V, _V, _SZ, _SZ],
+    "hecnn_poly_sub": [_V, _V, _V, _V, _SZ, _SZ],
+    "hecnn_poly_neg": [_V, _V, _V, _SZ, _SZ],
+    "hecnn_poly_pointwise_mul": [_V, _V, _V, _V, _SZ, _SZ],
+    "hecnn_poly_pointwise_mac": [_V, _V, _V, _V, _SZ, _SZ],
+    "hecnn_rescale_poly": [_V, _V, _V, _SZ, _SZ],
+    "hecnn_key_switch": [_V, _V, _V, _SZ, _SZ],
+    "hecnn_tensor_create": [_V, _SZ, _U32, _D, _PV],
+    "hecnn_tensor_destroy": [_V],
+    "hecnn_tensor_info": [_V, _PSZ, ctypes.POINTER(ctypes.c_uint32), _PD],
+    "hecnn_tensor_set_shape": [_V, _I, _SZ, _SZ, _SZ, _SZ],
+    "hecnn_tensor_shape": [_V, ctypes.POINTER(ctypes.c_int), _PSZ, _PSZ, _PSZ, _PSZ],
+    "hecnn_tensor_data": [_V, ctypes.POINTER(_PU64)],
+    "hecnn_tensor_upload": [_V, _V, _PU64],
+    "hecnn_tensor_download": [_V, _V, _PU64],
+    "hecnn_tensor_copy_to_device": [_V, _V, _V],
+    "hecnn_encrypt_tensor": [_V, _PD, _SZ, _SZ, _U64, _PV],
+    "hecnn_encrypt_raw": [_V, _PU64, _PI64, _PI64, _PI64, _SZ, _D, _PV],
+    "hecnn_decrypt_raw": [_V, _V, _PU64],
+    "hecnn_decrypt_tensor": [_V, _V, _SZ, _PD],
+    "hecnn_ct_add": [_V, _V, _V, _PV],
+    "hecnn_ct_sub": [_V, _V, _V, _PV],
+    "hecnn_ct_mul": [_V, _V, _V, _PV],
+    "hecnn_ct_square": [_V, _V, _PV],
+    "hecnn_ct_rescale": [_V, _V, _PV],
+    "hecnn_ct_mod_switch": [_V, _V, _U32, _PV],
+    "hecnn_ct_mul_const": [_V, _V, _D, _D, _PV],
+    "hecnn_ct_add_const": [_V, _V, _D, _PV],
+    "hecnn_eval_activation": [_V, _PD, _SZ, _D, _V, _PV],
+    "hecnn_model_create": [_V, _V, _PV],
+    "hecnn_model_destroy": [_V],
+    "hecnn_model_depth_cost": [_V, _PSZ],
+    "hecnn_forward_encrypted": [_V, _V, _V, _U64, _PV, _PD],
+}
 
 
 def lib() -> ctypes.CDLL:
@@ -57,6 +133,11 @@ def lib() -> ctypes.CDLL:
             raise RuntimeError(f"hecnn_b200 CUDA extension not built: {LIB_PATH} (run __graft_entry__.build())")
         L = ctypes.CDLL(LIB_PATH)
         L.hecnn_last_error.restype = ctypes.c_char_p
+        L.hecnn_last_error.argtypes = []
+        for name, args in _SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = ctypes.c_int
+            fn.argtypes = args
         _lib = L
     return _lib
 
@@ -91,6 +172,36 @@ def find_chain(n: int, prime_bits: Sequence[int]) -> List[int]:
     out = np.zeros(len(prime_bits), dtype=np.uint64)
     _check(lib().hecnn_find_chain(ctypes.c_size_t(n), bits, ctypes.c_size_t(len(prime_bits)), _ptr(out)))
     return [int(v) for v in out]
+
+
+def host_encode_real(params: "CkksParams", values, level: int, scale: Optional[float] = None) -> np.ndarray:
+    """encode_real (ckks.hpp:105-129) on the host: residues [(level+1)][n]."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    pr = np.asarray(params.primes, dtype=np.uint64)
+    out = np.empty((level + 1, params.n), dtype=np.uint64)
+    _check(lib().hecnn_host_encode_real(params.n, _ptr(pr), len(pr), _ptr(v, ctypes.c_double), v.size,
+                                        scale or params.scale, level, _ptr(out)))
+    return out
+
+
+def host_decode_real(params: "CkksParams", poly: np.ndarray, level: int, scale: float, count: Optional[int] = None):
+    """decode (ckks.hpp:142-154) on the host: real parts of the slots."""
+    poly = np.ascontiguousarray(poly, dtype=np.uint64)
+    pr = np.asarray(params.primes, dtype=np.uint64)
+    count = count or params.n // 2
+    out = np.empty(count, dtype=np.float64)
+    _check(lib().hecnn_host_decode_real(params.n, _ptr(pr), len(pr), _ptr(poly), level, scale,
+                                        _ptr(out, ctypes.c_double), count))
+    return out
+
+
+def host_encryption_randomness(params: "CkksParams", seed: int):
+    """make_encryption_randomness (ckks.hpp:238-244): (r, e0, e1) signed coefficients."""
+    r, e0, e1 = (np.empty(params.n, dtype=np.int64) for _ in range(3))
+    _check(lib().hecnn_host_encryption_randomness(params.n, params.sigma, int(params.degenerate_noise), seed,
+                                                  _ptr(r, ctypes.c_int64), _ptr(e0, ctypes.c_int64),
+                                                  _ptr(e1, ctypes.c_int64)))
+    return r, e0, e1
 
 
 @dataclass
@@ -531,6 +642,39 @@ class CkksEngine:
 
     def set_stream(self, stream_ptr: int):
         _check(lib().hecnn_context_set_stream(self.ctx, ctypes.c_void_p(stream_ptr)))
+
+    # ---- measurement
+    def profile(self, on: bool):
+        _check(lib().hecnn_profile_enable(self.ctx, int(on)))
+
+    def profile_reset(self):
+        _check(lib().hecnn_profile_reset(self.ctx))
+
+    def profile_read(self) -> dict:
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(lib().hecnn_profile_read(self.ctx, buf, ctypes.c_size_t(len(buf))))
+        return json.loads(buf.value.decode())
+
+    def modmul_peak(self) -> float:
+        v = ctypes.c_double()
+        _check(lib().hecnn_modmul_peak(self.ctx, ctypes.byref(v)))
+        return v.value
+
+    def copy_to_device(self, t: "EncryptedTensor", dst_ptr: int):
+        _check(lib().hecnn_tensor_copy_to_device(self.ctx, t.handle, ctypes.c_void_p(dst_ptr)))
+
+    def upload_into(self, t: "EncryptedTensor", host_ptr: int):
+        """H2D of a [cells][2][level+1][n] host buffer (pinned for full speed)."""
+        _check(lib().hecnn_tensor_upload(self.ctx, t.handle, ctypes.cast(host_ptr, _u64p)))
+
+    def download_into(self, t: "EncryptedTensor", host_ptr: int):
+        _check(lib().hecnn_tensor_download(self.ctx, t.handle, ctypes.cast(host_ptr, _u64p)))
+
+    def empty_tensor(self, cells: int, level: int, scale: float) -> "EncryptedTensor":
+        h = ctypes.c_void_p()
+        _check(lib().hecnn_tensor_create(self.ctx, ctypes.c_size_t(cells), ctypes.c_uint32(level),
+                                         ctypes.c_double(scale), ctypes.byref(h)))
+        return self._wrap(h)
 
     # ---- keys
     def keygen(self, seed: int) -> "CkksEngine":

@@ -2,6 +2,7 @@
 // exceptions into status codes + a thread-local message, mirroring the
 // reference's exception types: std::invalid_argument -> HECNN_EINVAL,
 // std::runtime_error (and anything else) -> HECNN_ERUNTIME.
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -10,13 +11,18 @@
 
 using namespace hecnn_b200;
 
+// Tensors and models share ownership of their context: destroying the
+// context handle only drops one reference, so handles released in any order
+// (e.g. by a garbage collector) never touch a dead context.
 struct hecnn_context {
-    std::unique_ptr<Context> ctx;
+    std::shared_ptr<Context> ctx;
 };
 struct hecnn_tensor {
+    std::shared_ptr<Context> keep;  // destroyed after t (reverse member order)
     TensorPtr t;
 };
 struct hecnn_model {
+    std::shared_ptr<Context> keep;
     Model m;
 };
 
@@ -54,8 +60,11 @@ const Tensor& T(const hecnn_tensor* t) {
     if (!t || !t->t) throw std::invalid_argument("null tensor");
     return *t->t;
 }
-hecnn_tensor* wrap(TensorPtr t) {
+std::shared_ptr<Context> owner(hecnn_context* c) { return c->ctx; }
+
+hecnn_tensor* wrap(hecnn_context* c, TensorPtr t) {
     auto* h = new hecnn_tensor;
+    h->keep = owner(c);
     h->t = std::move(t);
     return h;
 }
@@ -74,11 +83,49 @@ int hecnn_find_chain(size_t n, const int* prime_bits, size_t count, uint64_t* pr
     });
 }
 
+int hecnn_host_encode_real(size_t n, const uint64_t* primes, size_t nprimes, const double* values, size_t len,
+                           double scale, size_t level, uint64_t* out) {
+    return guard([&] {
+        RingTables R;
+        R.build(n, std::vector<u64>(primes, primes + nprimes));
+        Encoder enc(R, scale);
+        EncodedCoeffs e;
+        enc.encode_real(values, len, scale, level, e);
+        for (size_t i = 0; i <= level; ++i)
+            for (size_t j = 0; j < n; ++j)
+                out[i * n + j] = e.small ? R.mods[i].from_signed(e.coeffs[j]) : e.residues[i * n + j];
+    });
+}
+
+int hecnn_host_decode_real(size_t n, const uint64_t* primes, size_t nprimes, const uint64_t* poly, size_t level,
+                           double scale, double* out, size_t count) {
+    return guard([&] {
+        RingTables R;
+        R.build(n, std::vector<u64>(primes, primes + nprimes));
+        Encoder enc(R, scale);
+        enc.decode_real(poly, level, scale, out, count);
+    });
+}
+
+int hecnn_host_encryption_randomness(size_t n, double sigma, int degenerate, uint64_t seed, int64_t* r, int64_t* e0,
+                                     int64_t* e1) {
+    return guard([&] {
+        auto put = [&](const std::vector<long long>& v, int64_t* dst) {
+            for (size_t j = 0; j < n; ++j) dst[j] = v[j];
+        };
+        std::vector<long long> zero(n, 0);
+        put(degenerate ? zero : sample_ternary(n, 0.5, derive_seed(seed, 0x0a01)), r);
+        const bool no_err = degenerate || sigma == 0.0;
+        put(no_err ? zero : sample_gaussian(n, sigma, derive_seed(seed, 0x0a02)), e0);
+        put(no_err ? zero : sample_gaussian(n, sigma, derive_seed(seed, 0x0a03)), e1);
+    });
+}
+
 int hecnn_context_create(size_t n, const uint64_t* primes, size_t nprimes, double scale, double sigma,
                          int degenerate_noise, int device, hecnn_context** out) {
     return guard([&] {
         auto h = std::make_unique<hecnn_context>();
-        h->ctx = std::make_unique<Context>(n, std::vector<u64>(primes, primes + nprimes), scale, sigma,
+        h->ctx = std::make_shared<Context>(n, std::vector<u64>(primes, primes + nprimes), scale, sigma,
                                            degenerate_noise != 0, device);
         *out = h.release();
     });
@@ -121,6 +168,59 @@ int hecnn_relin_digits(const hecnn_context* ctx, size_t level, size_t* digits) {
 
 int hecnn_launch_count(const hecnn_context* ctx, uint64_t* launches) {
     return guard([&] { *launches = C(ctx).launches; });
+}
+
+int hecnn_profile_enable(hecnn_context* ctx, int on) {
+    return guard([&] {
+        Context& c = C(ctx);
+        c.sync();
+        c.prof.collect();
+        c.prof.enabled = on != 0;
+    });
+}
+
+int hecnn_profile_reset(hecnn_context* ctx) {
+    return guard([&] {
+        Context& c = C(ctx);
+        c.sync();
+        c.prof.reset();
+    });
+}
+
+int hecnn_profile_read(hecnn_context* ctx, char* buf, size_t len) {
+    return guard([&] {
+        Context& c = C(ctx);
+        c.sync();
+        c.prof.collect();
+        std::string js = "{";
+        bool first = true;
+        for (const auto& kv : c.prof.stats) {
+            if (!first) js += ",";
+            first = false;
+            char num[160];
+            std::snprintf(num, sizeof num, "{\"ms\":%.6f,\"launches\":%llu,\"ops\":%.6e,\"bytes\":%.6e}",
+                          kv.second.ms, kv.second.launches, kv.second.ops, kv.second.bytes);
+            js += "\"" + kv.first + "\":" + num;
+        }
+        js += "}";
+        if (js.size() + 1 > len) throw std::invalid_argument("profile_read: buffer too small");
+        std::memcpy(buf, js.c_str(), js.size() + 1);
+    });
+}
+
+int hecnn_modmul_peak(hecnn_context* ctx, double* modmul_per_s) {
+    return guard([&] { *modmul_per_s = measure_modmul_peak(C(ctx)); });
+}
+
+int hecnn_tensor_copy_to_device(hecnn_context* ctx, const hecnn_tensor* t, void* dst) {
+    return guard([&] {
+        Context& c = C(ctx);
+        const Tensor& x = T(t);
+        if (cudaMemcpyAsync(dst, x.data(), x.cells * x.cell_words() * 8, cudaMemcpyDeviceToDevice, c.stream) !=
+            cudaSuccess)
+            throw std::runtime_error("tensor_copy_to_device failed");
+        c.sync();
+    });
 }
 
 int hecnn_keygen(hecnn_context* ctx, uint64_t seed) {
@@ -251,7 +351,7 @@ int hecnn_tensor_create(hecnn_context* ctx, size_t cells, uint32_t level, double
     return guard([&] {
         Context& c = C(ctx);
         if (level > c.top()) throw std::invalid_argument("tensor: level out of range");
-        *out = wrap(make_tensor(c, cells, level, scale));
+        *out = wrap(ctx, make_tensor(c, cells, level, scale));
     });
 }
 
@@ -306,13 +406,13 @@ int hecnn_tensor_download(hecnn_context* ctx, const hecnn_tensor* t, uint64_t* h
 
 int hecnn_encrypt_tensor(hecnn_context* ctx, const double* data, size_t batch, size_t positions, uint64_t seed,
                          hecnn_tensor** out) {
-    return guard([&] { *out = wrap(encrypt_tensor(C(ctx), data, batch, positions, seed)); });
+    return guard([&] { *out = wrap(ctx, encrypt_tensor(C(ctx), data, batch, positions, seed)); });
 }
 
 int hecnn_encrypt_raw(hecnn_context* ctx, const uint64_t* m, const int64_t* r, const int64_t* e0, const int64_t* e1,
                       size_t count, double scale, hecnn_tensor** out) {
     return guard([&] {
-        *out = wrap(encrypt_raw(C(ctx), m, reinterpret_cast<const long long*>(r),
+        *out = wrap(ctx, encrypt_raw(C(ctx), m, reinterpret_cast<const long long*>(r),
                                 reinterpret_cast<const long long*>(e0), reinterpret_cast<const long long*>(e1), count,
                                 scale));
     });
@@ -327,35 +427,35 @@ int hecnn_decrypt_tensor(hecnn_context* ctx, const hecnn_tensor* t, size_t batch
 }
 
 int hecnn_ct_add(hecnn_context* ctx, const hecnn_tensor* x, const hecnn_tensor* y, hecnn_tensor** out) {
-    return guard([&] { *out = wrap(ct_add(C(ctx), T(x), T(y), false)); });
+    return guard([&] { *out = wrap(ctx, ct_add(C(ctx), T(x), T(y), false)); });
 }
 int hecnn_ct_sub(hecnn_context* ctx, const hecnn_tensor* x, const hecnn_tensor* y, hecnn_tensor** out) {
-    return guard([&] { *out = wrap(ct_add(C(ctx), T(x), T(y), true)); });
+    return guard([&] { *out = wrap(ctx, ct_add(C(ctx), T(x), T(y), true)); });
 }
 int hecnn_ct_mul(hecnn_context* ctx, const hecnn_tensor* x, const hecnn_tensor* y, hecnn_tensor** out) {
-    return guard([&] { *out = wrap(ct_mul(C(ctx), T(x), T(y))); });
+    return guard([&] { *out = wrap(ctx, ct_mul(C(ctx), T(x), T(y))); });
 }
 int hecnn_ct_square(hecnn_context* ctx, const hecnn_tensor* x, hecnn_tensor** out) {
-    return guard([&] { *out = wrap(ct_square(C(ctx), T(x))); });
+    return guard([&] { *out = wrap(ctx, ct_square(C(ctx), T(x))); });
 }
 int hecnn_ct_rescale(hecnn_context* ctx, const hecnn_tensor* x, hecnn_tensor** out) {
-    return guard([&] { *out = wrap(ct_rescale(C(ctx), T(x))); });
+    return guard([&] { *out = wrap(ctx, ct_rescale(C(ctx), T(x))); });
 }
 int hecnn_ct_mod_switch(hecnn_context* ctx, const hecnn_tensor* x, uint32_t to_level, hecnn_tensor** out) {
-    return guard([&] { *out = wrap(ct_mod_switch(C(ctx), T(x), to_level)); });
+    return guard([&] { *out = wrap(ctx, ct_mod_switch(C(ctx), T(x), to_level)); });
 }
 int hecnn_ct_mul_const(hecnn_context* ctx, const hecnn_tensor* x, double c, double scale, hecnn_tensor** out) {
-    return guard([&] { *out = wrap(ct_mul_const(C(ctx), T(x), c, scale)); });
+    return guard([&] { *out = wrap(ctx, ct_mul_const(C(ctx), T(x), c, scale)); });
 }
 int hecnn_ct_add_const(hecnn_context* ctx, const hecnn_tensor* x, double c, hecnn_tensor** out) {
-    return guard([&] { *out = wrap(ct_add_const(C(ctx), T(x), c)); });
+    return guard([&] { *out = wrap(ctx, ct_add_const(C(ctx), T(x), c)); });
 }
 
 int hecnn_eval_activation(hecnn_context* ctx, const double* coefficients, size_t n_coefficients, double interval_bound,
                           const hecnn_tensor* x, hecnn_tensor** out) {
     return guard([&] {
         Activation a{std::vector<double>(coefficients, coefficients + n_coefficients), interval_bound};
-        *out = wrap(eval_activation(C(ctx), a, T(x)));
+        *out = wrap(ctx, eval_activation(C(ctx), a, T(x)));
     });
 }
 
@@ -363,6 +463,7 @@ int hecnn_model_create(hecnn_context* ctx, const hecnn_model_desc* d, hecnn_mode
     return guard([&] {
         (void)C(ctx);
         auto h = std::make_unique<hecnn_model>();
+        h->keep = owner(ctx);
         Model& m = h->m;
         m.input = d->input_flat ? Shape::flattened(d->input_features)
                                 : Shape::spatial(d->input_h, d->input_w, d->input_c);
@@ -409,7 +510,7 @@ int hecnn_model_depth_cost(const hecnn_model* m, size_t* cost) {
 int hecnn_forward_encrypted(hecnn_context* ctx, const hecnn_model* m, const hecnn_tensor* x, uint64_t seed,
                             hecnn_tensor** out, double* layer_seconds) {
     return guard([&] {
-        *out = wrap(forward_encrypted(C(ctx), const_cast<hecnn_model*>(m)->m, T(x), seed, layer_seconds));
+        *out = wrap(ctx, forward_encrypted(C(ctx), const_cast<hecnn_model*>(m)->m, T(x), seed, layer_seconds));
     });
 }
 

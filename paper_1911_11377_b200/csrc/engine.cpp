@@ -5,7 +5,6 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
-#include <sstream>
 #include <stdexcept>
 #include <thread>
 #include <tuple>
@@ -108,10 +107,57 @@ void DevBuf::reset() {
 }
 
 std::string Shape::str() const {
-    std::ostringstream os;
-    if (flat) os << "(" << feat << ")";
-    else os << "(" << h << "x" << w << "x" << c << ")";
-    return os.str();
+    if (flat) return "(" + std::to_string(feat) + ")";
+    return "(" + std::to_string(h) + "x" + std::to_string(w) + "x" + std::to_string(c) + ")";
+}
+
+// ---------------------------------------------------------------- profiler
+
+cudaEvent_t Profiler::take() {
+    if (pool.empty()) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+}
+
+void Profiler::begin(const char* name, cudaStream_t s, double ops, double bytes) {
+    open_name = name;
+    open_ops = ops;
+    open_bytes = bytes;
+    open_start = take();
+    cudaEventRecord(open_start, s);
+}
+
+void Profiler::end(cudaStream_t s) {
+    if (!open_name) return;
+    cudaEvent_t stop = take();
+    cudaEventRecord(stop, s);
+    pending.push_back({open_name, open_start, stop, open_ops, open_bytes});
+    open_name = nullptr;
+}
+
+void Profiler::collect() {
+    for (auto& p : pending) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p.start, p.stop);
+        Stat& st = stats[p.name];
+        st.ms += ms;
+        st.ops += p.ops;
+        st.bytes += p.bytes;
+        st.launches += 1;
+        pool.push_back(p.start);
+        pool.push_back(p.stop);
+    }
+    pending.clear();
+}
+
+void Profiler::reset() {
+    collect();
+    stats.clear();
 }
 
 // ---------------------------------------------------------------- context
@@ -167,6 +213,9 @@ Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, doubl
 
 Context::~Context() {
     cudaSetDevice(device);
+    cudaStreamSynchronize(stream);
+    prof.collect();
+    for (cudaEvent_t e : prof.pool) cudaEventDestroy(e);
     s_ntt.reset();
     pk.reset();
     evk.reset();
@@ -189,6 +238,25 @@ void Context::download(void* dst, const void* src, std::size_t bytes) {
 }
 
 void Context::sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+
+double measure_modmul_peak(Context& C) {
+    DevBuf sink(&C, 64);
+    Launch L = C.L();
+    modmul_probe(C.dev, 64, sink.as<u64>(), L);  // warm-up
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int iters = 4096;
+    cudaEventRecord(a, C.stream);
+    double ops = modmul_probe(C.dev, iters, sink.as<u64>(), L);
+    cudaEventRecord(b, C.stream);
+    C.sync();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ops / (ms * 1e-3);
+}
 
 TensorPtr make_tensor(Context& C, std::size_t cells, std::uint32_t level, double scale) {
     auto t = std::make_unique<Tensor>();

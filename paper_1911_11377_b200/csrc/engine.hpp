@@ -58,10 +58,11 @@ struct Context {
     std::size_t evk_digits = 0;
     bool has_secret = false, has_pk = false;
     unsigned long long launches = 0;
+    Profiler prof;
 
     Context(std::size_t n, const std::vector<u64>& primes, double scale, double sigma, bool degenerate, int device);
     ~Context();
-    Launch L() { return Launch{stream, &launches}; }
+    Launch L() { return Launch{stream, &launches, &prof}; }
     std::size_t n() const { return ring.n; }
     std::size_t top() const { return ring.limbs - 1; }
     void upload(void* dst, const void* src, std::size_t bytes);
@@ -105,6 +106,8 @@ struct Tensor {
 using TensorPtr = std::unique_ptr<Tensor>;
 
 TensorPtr make_tensor(Context& C, std::size_t cells, std::uint32_t level, double scale);
+// Integer-pipe peak: Shoup modmuls per second measured with CUDA events.
+double measure_modmul_peak(Context& C);
 
 // ---- keys
 void keygen(Context& C, u64 seed);

@@ -6,6 +6,9 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
 
 #include "arith.cuh"
 
@@ -26,11 +29,44 @@ struct DevRing {
     const double* inv_q = nullptr;           // [limbs] 1/q_i
 };
 
+// Optional per-kernel timing: CUDA events recorded on the launching stream
+// around every kernel launch while enabled (see Context::profile).
+struct Profiler {
+    bool enabled = false;
+    struct Pending {
+        const char* name;
+        cudaEvent_t start, stop;
+        double ops, bytes;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> pool;
+    const char* open_name = nullptr;
+    cudaEvent_t open_start = nullptr;
+    double open_ops = 0, open_bytes = 0;
+    // ops: algorithmic 64-bit modular multiply-equivalents (one NTT butterfly =
+    // one Shoup modmul); bytes: algorithmic (minimal) global-memory bytes.
+    struct Stat {
+        double ms = 0, ops = 0, bytes = 0;
+        unsigned long long launches = 0;
+    };
+    std::map<std::string, Stat> stats;
+    cudaEvent_t take();
+    void begin(const char* name, cudaStream_t s, double ops, double bytes);
+    void end(cudaStream_t s);
+    void collect();  // call after the stream is synchronized
+    void reset();
+};
+
 struct Launch {
     cudaStream_t stream = nullptr;
     unsigned long long* counter = nullptr;
+    Profiler* prof = nullptr;
+    void begin(const char* name, double ops = 0, double bytes = 0) const {
+        if (prof && prof->enabled) prof->begin(name, stream, ops, bytes);
+    }
     void count(unsigned long long k = 1) const {
         if (counter) *counter += k;
+        if (prof && prof->enabled) prof->end(stream);
     }
 };
 
@@ -73,6 +109,10 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
 //   evk: [Dtop][2][limbs][n] values, evk_sh: Shoup companions
 void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, u64* acc01, int level,
                    int D, std::size_t count, const Launch& L);
+
+// Integer-pipe peak probe: chained Shoup modmuls (the NTT butterfly's
+// multiply), `iters` per thread over the whole GPU; returns modmuls issued.
+double modmul_probe(const DevRing& R, int iters, u64* sink, const Launch& L);
 
 // ---- linear layers (linear.cu)
 // Gather-MAC for conv/dense: see linear.cu for the table formats.

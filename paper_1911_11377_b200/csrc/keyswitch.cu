@@ -263,6 +263,12 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
     static bool init = (smem > 48 * 1024 ? (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true) : true);
     (void)init;
     const std::size_t ctas = count * static_cast<std::size_t>(level + 1) << (LOGN - P::LOGB);
+    {
+        // per (ct, limb, digit): one N-point NTT + 2N MACs; bytes: evk once + digits + acc r/w
+        const double n = double(1 << LOGN), cl = double(count) * (level + 1);
+        L.begin("k_keyswitch", cl * D * (n / 2 * LOGN + 2 * n),
+                2.0 * D * (level + 1) * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
+    }
     kern<<<static_cast<unsigned>(ctas), P::T, smem, L.stream>>>(R, digits, evk, evk_sh, acc01, level, D);
     L.count();
 }
@@ -275,7 +281,7 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
     const unsigned grid = static_cast<unsigned>((total + 127) / 128);
     const int W = R.crt_words;
 #define HECNN_CRT_CASE(WW) \
-    case WW: k_crt_digits<WW><<<grid, 128, 0, L.stream>>>(R, d2, digits, level, D, static_cast<long long>(count)); break;
+    case WW: L.begin("k_crt_digits", double(count) * R.n * (level + 1) * (WW + 1), double(count) * R.n * ((level + 1) * 8 + D * 4)); k_crt_digits<WW><<<grid, 128, 0, L.stream>>>(R, d2, digits, level, D, static_cast<long long>(count)); break;
     switch (W) {
         HECNN_CRT_CASE(2) HECNN_CRT_CASE(3) HECNN_CRT_CASE(4) HECNN_CRT_CASE(5) HECNN_CRT_CASE(6) HECNN_CRT_CASE(7)
         HECNN_CRT_CASE(8) HECNN_CRT_CASE(9) HECNN_CRT_CASE(10) HECNN_CRT_CASE(11) HECNN_CRT_CASE(12)

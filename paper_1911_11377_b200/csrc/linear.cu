@@ -99,6 +99,8 @@ void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int 
     dim3 grid(static_cast<unsigned>((cell_words + TPB - 1) / TPB), static_cast<unsigned>(g.pixels),
               static_cast<unsigned>((g.oc + OCT - 1) / OCT));
     if (!g.pixels || !g.oc) return;
+    L.begin("k_gather_mac", double(g.pixels) * g.K * g.oc * cell_words,
+            8.0 * cell_words * (double(g.pixels) * g.oc + g.pixels * g.K));
     k_gather_mac<<<grid, TPB, 0, L.stream>>>(R, g, x, y, level);
     L.count();
     check_launch("gather_mac");
@@ -111,6 +113,7 @@ void pool_sum_scale(const DevRing& R, const u64* x, const int* srcs, int taps, c
     for (std::size_t off = 0; off < out_cells; off += 65535) {
         const std::size_t m = std::min<std::size_t>(65535, out_cells - off);
         dim3 grid(static_cast<unsigned>((cell_words + TPB - 1) / TPB), static_cast<unsigned>(m));
+        L.begin("k_pool", double(m) * cell_words, 8.0 * cell_words * m * (taps + 1));
         k_pool<<<grid, TPB, 0, L.stream>>>(R, x, srcs + off * taps, taps, w, y + off * cell_words, level);
         L.count();
     }
@@ -124,6 +127,7 @@ void gather_cells(const u64* x, const int* idx, u64* y, std::size_t cell_words, 
     for (std::size_t off = 0; off < cells; off += 65535) {
         const std::size_t m = std::min<std::size_t>(65535, cells - off);
         dim3 grid(gx, static_cast<unsigned>(m));
+        L.begin("k_gather_cells", 0, 16.0 * cell_words * m);
         k_gather_cells<<<grid, TPB, 0, L.stream>>>(x, idx + off, y + off * cell_words, cw);
         L.count();
     }

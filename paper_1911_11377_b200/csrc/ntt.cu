@@ -253,6 +253,7 @@ void run_forward(const DevRing& R, u64* data, int limbs, std::size_t polys, cons
     using P = NttPlan<LOGN>;
     if constexpr (P::C > 0) {
         long long total = static_cast<long long>(polys) << (LOGN - P::C);
+        L.begin("k_ntt_fwd_cols", double(polys) * (1 << (LOGN - 1)) * P::C, 16.0 * polys * (1 << LOGN));
         k_ntt_fwd_cols<LOGN, P::C><<<static_cast<unsigned>((total + 255) / 256), 256, 0, L.stream>>>(R, data, limbs, total);
         L.count();
     }
@@ -260,6 +261,7 @@ void run_forward(const DevRing& R, u64* data, int limbs, std::size_t polys, cons
     const int smem = (1 << P::LOGB) * 8;
     static bool init = (set_smem(kern, smem), true);
     (void)init;
+    L.begin("k_ntt_fwd_block", double(polys) * (1 << (LOGN - 1)) * P::LOGB, 16.0 * polys * (1 << LOGN));
     kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, data, limbs);
     L.count();
 }
@@ -271,10 +273,12 @@ void run_inverse(const DevRing& R, u64* data, int limbs, std::size_t polys, cons
     const int smem = (1 << P::LOGB) * 8;
     static bool init = (set_smem(kern, smem), true);
     (void)init;
+    L.begin("k_ntt_inv_block", double(polys) * (1 << (LOGN - 1)) * P::LOGB, 16.0 * polys * (1 << LOGN));
     kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, data, limbs);
     L.count();
     if constexpr (P::C > 0) {
         long long total = static_cast<long long>(polys) << (LOGN - P::C);
+        L.begin("k_ntt_inv_cols", double(polys) * (1 << (LOGN - 1)) * P::C, 16.0 * polys * (1 << LOGN));
         k_ntt_inv_cols<LOGN, P::C><<<static_cast<unsigned>((total + 255) / 256), 256, 0, L.stream>>>(R, data, limbs, total);
         L.count();
     }

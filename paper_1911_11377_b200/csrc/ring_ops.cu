@@ -217,11 +217,40 @@ __global__ void k_shoup(DevRing R, const u64* __restrict__ in, u64* __restrict__
     out[row * R.n + j] = est;
 }
 
+// Integer-pipe probe: 8 independent chains of lazy Shoup products per thread.
+__global__ void __launch_bounds__(256) k_modmul_probe(DevRing R, int iters, u64* __restrict__ sink) {
+    const u64 q = R.mod[0].q;
+    const ulonglong2 w = R.fwd[(threadIdx.x * 13 + 1) & (R.n - 1)];
+    u64 x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = (blockIdx.x * 256ull + threadIdx.x) * 8 + k + 1;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = mul_shoup_lazy(x[k], w.x, w.y, q);
+    }
+    u64 acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc ^= x[k];
+    if (acc == 0x5bd1e995ull) sink[0] = acc;  // keeps the chains live
+}
+
 }  // namespace
+
+double modmul_probe(const DevRing& R, int iters, u64* sink, const Launch& L) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int blocks = sms * 8;
+    L.begin("k_modmul_probe");
+    k_modmul_probe<<<blocks, 256, 0, L.stream>>>(R, iters, sink);
+    L.count();
+    check_launch("modmul_probe");
+    return static_cast<double>(blocks) * 256.0 * 8.0 * iters;
+}
 
 void shoup_table(const DevRing& R, const u64* in, u64* out, int limbs, std::size_t count, const Launch& L) {
     const std::size_t rows = count * limbs;
     if (!rows) return;
+    L.begin("k_shoup", double(rows) * R.n, 16.0 * rows * R.n);
     k_shoup<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, in, out, limbs);
     L.count();
     check_launch("shoup_table");
@@ -231,6 +260,7 @@ void poly_elementwise(const DevRing& R, EwOp op, const u64* a, const u64* b, u64
                       const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_elementwise", double(rows) * R.n, 24.0 * rows * R.n);
     k_elementwise<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, static_cast<int>(op), a, b, out, level + 1);
     L.count();
     check_launch("poly_elementwise");
@@ -238,6 +268,7 @@ void poly_elementwise(const DevRing& R, EwOp op, const u64* a, const u64* b, u64
 
 void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L) {
     if (!count) return;
+    L.begin("k_rescale", double(count) * level * R.n, 8.0 * count * R.n * (2 * level + 1));
     k_rescale<<<rows_grid(count, R.n), TPB, 0, L.stream>>>(R, in, out, level);
     L.count();
     check_launch("rescale");
@@ -247,6 +278,7 @@ void drop_limbs(const DevRing& R, const u64* in, u64* out, int level, int to_lev
                 const Launch& L) {
     const std::size_t rows = count * (to_level + 1);
     if (!rows) return;
+    L.begin("k_drop_limbs", 0, 16.0 * rows * R.n);
     k_drop_limbs<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(in, out, R.n, level + 1, to_level + 1);
     L.count();
     check_launch("drop_limbs");
@@ -256,6 +288,7 @@ void tensor_mul(const DevRing& R, const u64* fx, const u64* fy, u64* d01, u64* d
                 const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_tensor_mul", 4.0 * rows * R.n, 56.0 * rows * R.n);
     k_tensor_mul<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, fx, fy, d01, d2, level + 1);
     L.count();
     check_launch("tensor_mul");
@@ -265,6 +298,7 @@ void tensor_square(const DevRing& R, const u64* fx, u64* d01, u64* d2, int level
                    const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_tensor_square", 3.0 * rows * R.n, 40.0 * rows * R.n);
     k_tensor_square<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, fx, d01, d2, level + 1);
     L.count();
     check_launch("tensor_square");
@@ -274,6 +308,7 @@ void scalar_mul(const DevRing& R, const u64* in, const ulonglong2* consts, u64* 
                 const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_scalar_mul", double(rows) * R.n, 16.0 * rows * R.n);
     k_scalar_mul<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, in, consts, out, level + 1);
     L.count();
     check_launch("scalar_mul");
@@ -282,6 +317,7 @@ void scalar_mul(const DevRing& R, const u64* in, const ulonglong2* consts, u64* 
 void add_coeff0(const DevRing& R, u64* cts, const u64* consts, int level, std::size_t count, const Launch& L) {
     const long long total = static_cast<long long>(count) * (level + 1);
     if (!total) return;
+    L.begin("k_add_coeff0");
     k_add_coeff0<<<static_cast<unsigned>((total + TPB - 1) / TPB), TPB, 0, L.stream>>>(R, cts, consts, level + 1,
                                                                                        static_cast<long long>(count));
     L.count();
@@ -291,6 +327,7 @@ void add_coeff0(const DevRing& R, u64* cts, const u64* consts, int level, std::s
 void small_to_rns(const DevRing& R, const signed char* s, u64* out, int level, std::size_t count, const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_small_to_rns", 0, 9.0 * rows * R.n);
     k_small_to_rns<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, s, out, level + 1);
     L.count();
     check_launch("small_to_rns");
@@ -299,6 +336,7 @@ void small_to_rns(const DevRing& R, const signed char* s, u64* out, int level, s
 void i64_to_rns(const DevRing& R, const long long* s, u64* out, int level, std::size_t count, const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_i64_to_rns", 0, 16.0 * rows * R.n);
     k_i64_to_rns<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, s, out, level + 1);
     L.count();
     check_launch("i64_to_rns");
@@ -308,6 +346,7 @@ void mul_by_key(const DevRing& R, const u64* rt, const u64* pk, std::size_t pk_l
                 std::size_t count, const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_mul_by_key", 2.0 * rows * R.n, 40.0 * rows * R.n);
     k_mul_by_key<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, rt, pk, static_cast<long long>(pk_limbs), out,
                                                              level + 1);
     L.count();
@@ -318,6 +357,7 @@ void add_noise_msg(const DevRing& R, u64* ct, const signed char* e0, const signe
                    std::size_t count, const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_add_noise_msg", 0, 40.0 * rows * R.n);
     k_add_noise_msg<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, ct, e0, e1, m, level + 1);
     L.count();
     check_launch("add_noise_msg");
@@ -326,6 +366,7 @@ void add_noise_msg(const DevRing& R, u64* ct, const signed char* e0, const signe
 void mul_secret(const DevRing& R, u64* t, const u64* s_ntt, int level, std::size_t count, const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_mul_secret", double(rows) * R.n, 24.0 * rows * R.n);
     k_mul_secret<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, t, s_ntt, level + 1);
     L.count();
     check_launch("mul_secret");
@@ -334,6 +375,7 @@ void mul_secret(const DevRing& R, u64* t, const u64* s_ntt, int level, std::size
 void add_c0(const DevRing& R, const u64* ct, u64* t, int level, std::size_t count, const Launch& L) {
     const std::size_t rows = count * (level + 1);
     if (!rows) return;
+    L.begin("k_add_c0", 0, 24.0 * rows * R.n);
     k_add_c0<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, ct, t, level + 1);
     L.count();
     check_launch("add_c0");
