@@ -119,6 +119,25 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
+def max_over_ranks(seconds, device):
+    """Max of a per-rank device time over all ranks (the job's time)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([seconds], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_outputs(words):
+    """The only collective of the sharded path: every rank's output ciphertext
+    words gathered to all ranks (NCCL all_gather on GPUs, gloo in the CPU tests)."""
+    import torch
+    import torch.distributed as dist
+    gathered = [torch.empty_like(words) for _ in range(dist.get_world_size())]
+    dist.all_gather(gathered, words)
+    return gathered
+
+
 # ---------------------------------------------------------------- reference (CPU) path
 
 def reference_c4_images_per_s(threads):
@@ -278,13 +297,10 @@ def run_ours(args):
     gather_words = torch.empty(out_words_n, dtype=torch.int64, device=f"cuda:{local}")
     eng.copy_to_device(y, gather_words.data_ptr())
     if world > 1:
-        t = torch.tensor([dev_s], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s = float(t.item())
-        # the only collective: gather every rank's output ciphertexts (NCCL)
-        gathered = [torch.empty_like(gather_words) for _ in range(world)]
-        dist.all_gather(gathered, gather_words)
+        dev_s = max_over_ranks(dev_s, f"cuda:{local}")
+        gathered = gather_outputs(gather_words)
         torch.cuda.synchronize()
+        assert all(g.numel() == gather_words.numel() for g in gathered)
 
     # ---- end to end through the public API from pinned host memory
     xe = eng.empty_tensor(x.cells, x.level, x.scale)
@@ -302,9 +318,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_s = s.elapsed_time(e) / 1e3
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s, f"cuda:{local}")
     assert np.array_equal(host_out.numpy().view(np.uint64), y.words().reshape(-1)), "e2e output differs"
 
     images = world * batch * args.steps

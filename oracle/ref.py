@@ -301,6 +301,12 @@ def forward_plain(model_spec, data: np.ndarray) -> np.ndarray:
     return out
 
 
+def rng_uniform(seed: int, count: int) -> np.ndarray:
+    out = np.empty(count, dtype=np.float64)
+    _check(lib().ref_rng_uniform(ctypes.c_uint64(seed), ctypes.c_size_t(count), _p(out, ctypes.c_double)))
+    return out
+
+
 def gen_synthetic(count: int, image: int, channels: int, seed: int):
     imgs = np.empty((count, image * image * channels), dtype=np.float64)
     labels = np.empty(count, dtype=np.uint8)

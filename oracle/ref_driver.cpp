@@ -424,6 +424,14 @@ int ref_init_random_weights(const hecnn_model_desc* desc, uint64_t seed, double*
     });
 }
 
+// Rng::uniform01 stream (common.hpp:173-179): `count` draws from Rng(seed)
+int ref_rng_uniform(uint64_t seed, size_t count, double* out) {
+    return guard([&] {
+        Rng rng(seed);
+        for (size_t i = 0; i < count; ++i) out[i] = rng.uniform01();
+    });
+}
+
 // gen_synthetic (synthetic.hpp:24-86): images [count][positions], labels
 int ref_gen_synthetic(size_t count, size_t image, size_t channels, uint64_t seed, double* images, uint8_t* labels) {
     return guard([&] {
