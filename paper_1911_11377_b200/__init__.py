@@ -26,7 +26,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhecnn_b200.so")
+LIB_PATH = os.environ.get("HECNN_B200_LIB") or os.path.join(_HERE, "lib", "libhecnn_b200.so")
 
 HECNN_OK, HECNN_EINVAL, HECNN_ERUNTIME, HECNN_ECUDA = 0, 1, 2, 3
 

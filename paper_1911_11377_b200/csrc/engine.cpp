@@ -2,6 +2,9 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -16,6 +19,22 @@ namespace {
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
+
+// HECNN_TRACE=1 prints host wall time of the engine's phases (diagnostics).
+struct Trace {
+    const char* what;
+    std::chrono::steady_clock::time_point t0;
+    static bool on() {
+        static const bool v = std::getenv("HECNN_TRACE") != nullptr;
+        return v;
+    }
+    explicit Trace(const char* w) : what(w), t0(std::chrono::steady_clock::now()) {}
+    ~Trace() {
+        if (on())
+            std::fprintf(stderr, "[hecnn] %-28s %9.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
 
 // Scratch budget per batched scheme op; chunks of ciphertexts are sized to it.
 constexpr std::size_t kScratchBytes = std::size_t(3) << 30;
@@ -84,8 +103,70 @@ void to_int8(const std::vector<long long>& v, signed char* out) {
 
 // ---------------------------------------------------------------- memory
 
+Arena::~Arena() {
+    for (auto& s : segs_) cudaFree(s.first);
+}
+
+void* Arena::alloc(std::size_t bytes) {
+    bytes = (bytes + 255) & ~std::size_t(255);
+    auto best = free_.end();
+    for (auto it = free_.begin(); it != free_.end(); ++it)
+        if (it->second.size >= bytes && (best == free_.end() || it->second.size < best->second.size)) best = it;
+    if (best == free_.end()) {
+        const std::size_t seg = std::max(bytes, std::size_t(1) << 30);
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, seg);
+        if (e != cudaSuccess && seg > bytes) {  // fall back to an exact-size segment
+            cudaGetLastError();
+            e = cudaMalloc(&p, bytes);
+            if (e == cudaSuccess) {
+                segs_.push_back({static_cast<char*>(p), bytes});
+                reserved_ += bytes;
+                best = free_.emplace(static_cast<char*>(p), Block{bytes, static_cast<int>(segs_.size() - 1)}).first;
+            }
+        } else if (e == cudaSuccess) {
+            segs_.push_back({static_cast<char*>(p), seg});
+            reserved_ += seg;
+            best = free_.emplace(static_cast<char*>(p), Block{seg, static_cast<int>(segs_.size() - 1)}).first;
+        }
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw std::runtime_error("device arena: out of memory allocating " + std::to_string(bytes) + " bytes (" +
+                                     std::to_string(reserved_) + " reserved)");
+        }
+    }
+    char* p = best->first;
+    Block blk = best->second;
+    free_.erase(best);
+    if (blk.size > bytes) free_.emplace(p + bytes, Block{blk.size - bytes, blk.seg});
+    used_.emplace(p, Block{bytes, blk.seg});
+    return p;
+}
+
+void Arena::release(void* ptr) {
+    auto it = used_.find(static_cast<char*>(ptr));
+    if (it == used_.end()) return;
+    char* p = it->first;
+    Block blk = it->second;
+    used_.erase(it);
+    auto next = free_.lower_bound(p);
+    if (next != free_.end() && next->second.seg == blk.seg && p + blk.size == next->first) {
+        blk.size += next->second.size;
+        next = free_.erase(next);
+    }
+    if (next != free_.begin()) {
+        auto prev = std::prev(next);
+        if (prev->second.seg == blk.seg && prev->first + prev->second.size == p) {
+            prev->second.size += blk.size;
+            return;
+        }
+    }
+    free_.emplace(p, blk);
+}
+
 DevBuf::DevBuf(Context* ctx, std::size_t bytes) : ctx_(ctx), bytes_(bytes) {
-    if (bytes) cuda_check(cudaMallocAsync(&ptr_, bytes, ctx->stream), "cudaMallocAsync");
+    Trace tr(bytes > (64u << 20) ? "alloc>64MiB" : "alloc");
+    if (bytes) ptr_ = ctx->arena.alloc(bytes);
 }
 
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
@@ -101,7 +182,7 @@ DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
 }
 
 void DevBuf::reset() {
-    if (ptr_) cudaFreeAsync(ptr_, ctx_->stream);
+    if (ptr_) ctx_->arena.release(ptr_);
     ptr_ = nullptr;
     bytes_ = 0;
 }
@@ -173,11 +254,6 @@ Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, doubl
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
     own_stream = true;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        std::uint64_t keep = ~std::uint64_t(0);
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
 
     std::vector<ModConst> mods;
     for (const auto& m : ring.mods) mods.push_back(ModConst{m.q, 2 * m.q, m.ratio_lo, m.ratio_hi});
@@ -393,6 +469,7 @@ void key_switch_raw(Context& C, const u64* d2, u64* out, std::size_t level, std:
 
 // mul / square (ckks.hpp:315-369): tensor -> INTT(d2) -> key switch -> INTT -> rescale.
 static TensorPtr relin_product(Context& C, const Tensor& x, const Tensor* y) {
+    Trace tr("relin_product");
     const bool sq = y == nullptr;
     if (!sq) {
         if (x.level != y->level) throw std::invalid_argument("mul: level mismatch (use rescale/mod_switch first)");
@@ -515,6 +592,7 @@ void Activation::validate() const {
 
 // eval_encrypted (activation.hpp:228-265): power-basis plan over whole tensors.
 TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x) {
+    Trace tr("eval_activation");
     act.validate();
     const std::size_t d = act.degree(), depth = act.encrypted_depth();
     if (x.level < depth) throw std::invalid_argument("eval_encrypted: insufficient depth budget");
@@ -764,6 +842,7 @@ namespace {
 
 // conv2d / dense as a gather-MAC (layers.hpp:174-211, 269-293)
 TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, const Shape& out_shape) {
+    Trace tr("linear_layer");
     const Layer& l = M.layers[li];
     const bool conv = l.kind == 0;
     const Shape& in = x.shape;
@@ -783,12 +862,25 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
         lc.oc = static_cast<int>(oc);
         lc.oc_pad = static_cast<int>((oc + 7) / 8 * 8);
         std::vector<ulonglong2> w(rows * lc.oc_pad * limbs, make_ulonglong2(0, 0));
+        std::vector<uint2> ws(rows * lc.oc_pad * limbs, make_uint2(0, 0));
         for (std::size_t r = 0; r < rows; ++r)
             for (std::size_t o = 0; o < oc; ++o) {
                 std::vector<u64> res = C.enc->scalar_residues(l.w[r * oc + o], wscale, level);
-                for (std::size_t i = 0; i < limbs; ++i)
-                    w[(r * lc.oc_pad + o) * limbs + i] = make_ulonglong2(res[i], shoup_of(res[i], C.ring.primes[i]));
+                for (std::size_t i = 0; i < limbs; ++i) {
+                    const std::size_t at = (r * lc.oc_pad + o) * limbs + i;
+                    w[at] = make_ulonglong2(res[i], shoup_of(res[i], C.ring.primes[i]));
+                    ws[at] = make_uint2(static_cast<unsigned>(res[i] & 0x1FFFFFu), static_cast<unsigned>(res[i] >> 21));
+                }
             }
+        std::vector<ulonglong2> rc(2 * limbs);
+        for (std::size_t i = 0; i < limbs; ++i) {
+            const HostMod& m = C.ring.mods[i];
+            const u64 a = m.pow(2, 21), b = m.pow(2, 42);
+            rc[2 * i] = make_ulonglong2(a, shoup_of(a, m.q));
+            rc[2 * i + 1] = make_ulonglong2(b, shoup_of(b, m.q));
+        }
+        lc.wsplit = C.upload_vec(ws);
+        lc.recomb = C.upload_vec(rc);
         std::vector<int> src, wrow;
         if (conv) {
             const std::size_t need_h = (out_shape.h - 1) * l.stride + l.kh, need_w = (out_shape.w - 1) * l.stride + l.kw;
@@ -849,7 +941,8 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
     for (std::size_t p0 = 0; p0 < static_cast<std::size_t>(lc.pixels); p0 += pix_chunk) {
         const std::size_t m = std::min(pix_chunk, lc.pixels - p0);
         GatherMac g{lc.src.as<int>() + p0 * lc.K, lc.wrow.as<int>() + p0 * lc.K, lc.weights.as<ulonglong2>(),
-                    bit->second.as<u64>(), static_cast<int>(m), lc.K, lc.oc, lc.oc_pad, lc.oc};
+                    bit->second.as<u64>(), lc.wsplit.as<uint2>(), lc.recomb.as<ulonglong2>(),
+                    static_cast<int>(m), lc.K, lc.oc, lc.oc_pad, lc.oc};
         gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), L);
         rescale(C.dev, pre.as<u64>(), out->cell(p0 * oc), static_cast<int>(level), 2 * m * oc, L);
     }

@@ -20,7 +20,30 @@ namespace hecnn_b200 {
 
 struct Context;
 
-// Stream-ordered device allocation (cudaMallocAsync on the context stream).
+// Caching device arena: segments from cudaMalloc (>= 1 GiB, kept until the
+// context dies), sub-allocated best-fit with coalescing. All work of a context
+// runs on its one stream, so a block freed on the host can be handed out again
+// immediately: later kernels on that stream are ordered after earlier users.
+// (cudaMallocAsync's pool re-mapped 17 GB tensors on some steps, costing
+// 0.4-1.6 s per allocation.)
+class Arena {
+public:
+    ~Arena();
+    void* alloc(std::size_t bytes);
+    void release(void* p);
+    std::size_t reserved() const { return reserved_; }
+
+private:
+    struct Block {
+        std::size_t size;
+        int seg;
+    };
+    std::vector<std::pair<char*, std::size_t>> segs_;
+    std::map<char*, Block> free_, used_;
+    std::size_t reserved_ = 0;
+};
+
+// Device allocation from the context's arena.
 class DevBuf {
 public:
     DevBuf() = default;
@@ -59,6 +82,7 @@ struct Context {
     bool has_secret = false, has_pk = false;
     unsigned long long launches = 0;
     Profiler prof;
+    Arena arena;
 
     Context(std::size_t n, const std::vector<u64>& primes, double scale, double sigma, bool degenerate, int device);
     ~Context();
@@ -157,7 +181,7 @@ struct Model {
     std::vector<Shape> shapes;  // per-layer output shapes (shape_infer)
     // integer-weight caches, keyed by (layer, level) and (layer, level, scale)
     struct LinearCache {
-        DevBuf src, wrow, weights;
+        DevBuf src, wrow, weights, wsplit, recomb;
         int pixels = 0, K = 0, oc = 0, oc_pad = 0;
     };
     std::map<std::pair<std::size_t, std::uint32_t>, LinearCache> linear;

@@ -121,6 +121,8 @@ struct GatherMac {
     const int* wrow;           // [pixels][K] weight row per tap
     const ulonglong2* weights; // [rows][oc_pad][limbs] (residue, shoup) at level, oc_pad % 8 == 0
     const u64* bias;           // [oc][level+1] residues (added to c0 coeff 0), or null
+    const uint2* wsplit;       // [rows][oc_pad][limbs] residue split (w mod 2^21, w >> 21) for q < 2^41
+    const ulonglong2* recomb;  // [limbs][2]: (2^21 mod q, shoup), (2^42 mod q, shoup)
     int pixels, K, oc, oc_pad, out_stride_pixel;  // output cell = pixel * out_stride_pixel + oc
 };
 void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, const Launch& L);

@@ -18,15 +18,11 @@
 
 #include <stdexcept>
 
-#include "kernels.hpp"
+#include "ntt_core.cuh"
 
 namespace hecnn_b200 {
 
 namespace {
-
-__device__ __forceinline__ int swz(int i) {
-    return i ^ static_cast<int>((0x1eb4d278963c5af0ull >> (4 * ((i >> 4) & 15))) & 15);
-}
 
 template <int W>
 __global__ void __launch_bounds__(128) k_crt_digits(DevRing R, const u64* __restrict__ d2, u32* __restrict__ digits,
@@ -117,20 +113,10 @@ __global__ void __launch_bounds__(128) k_crt_digits(DevRing R, const u64* __rest
     }
 }
 
-__device__ __forceinline__ void ct_butterfly(u64& a, u64& b, ulonglong2 w, u64 q, u64 two_q) {
-    u64 u = a;
-    if (u >= two_q) u -= two_q;
-    u64 v = mul_shoup_lazy(b, w.x, w.y, q);
-    a = u + v;
-    b = u + two_q - v;
-}
-
-__host__ __device__ constexpr int ceil_div(int a, int b) { return (a + b - 1) / b; }
-__host__ __device__ constexpr int round_size(int LOGB, int LOGE, int s) { return ceil_div(LOGB - s, ceil_div(LOGB - s, LOGE)); }
-
 __device__ __forceinline__ u64 lift_digit(u32 v, u64 q) { return v < q ? v : v % q; }
 
-// Value at block-local position r after the C column stages (block b).
+// Value at block-local position r after the C column stages (block b): only
+// the butterflies on the path to output b are evaluated (2^C - 1 products).
 template <int LOGN, int C>
 __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const ulonglong2* __restrict__ tw, u64 q, int r,
                                             int b) {
@@ -149,7 +135,7 @@ __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const u
             for (int blk = 0; blk < (1 << rho); ++blk) {
                 const ulonglong2 w = tw[(1 << rho) + blk];
 #pragma unroll
-                for (int kk = 0; kk < half; ++kk) ct_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
+                for (int kk = 0; kk < half; ++kk) ntt::ct_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
             }
         }
         u64 v = x[0];
@@ -160,51 +146,18 @@ __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const u
     }
 }
 
-template <int LOGN, int LOGB, int R, int S0, bool FIRST>
-__device__ __forceinline__ void ks_round(u64* s, const u32* __restrict__ dig, const ulonglong2* __restrict__ tw, u64 q,
-                                         int b) {
-    constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R, C = LOGN - LOGB;
-    const u64 two_q = q << 1;
-    for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
-        const int grp = u / STRIDE, col = u % STRIDE;
-        const int base = grp * G + col;
-        u64 x[E];
-#pragma unroll
-        for (int k = 0; k < E; ++k)
-            x[k] = FIRST ? column_value<LOGN, C>(dig, tw, q, base + k * STRIDE, b) : s[swz(base + k * STRIDE)];
-#pragma unroll
-        for (int rho = 0; rho < R; ++rho) {
-            const int st = C + S0 + rho;
-            const int half = E >> (rho + 1);
-            const int tbase = (1 << st) + (b << (S0 + rho)) + (grp << rho);
-#pragma unroll
-            for (int blk = 0; blk < (1 << rho); ++blk) {
-                const ulonglong2 w = tw[tbase + blk];
-#pragma unroll
-                for (int kk = 0; kk < half; ++kk) ct_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < E; ++k) s[swz(base + k * STRIDE)] = x[k];
-    }
-}
-
-template <int LOGN, int LOGB, int LOGE, int S0, bool FIRST>
-__device__ __forceinline__ void ks_rounds(u64* s, const u32* dig, const ulonglong2* tw, u64 q, int b) {
-    if constexpr (S0 < LOGB) {
-        constexpr int R = round_size(LOGB, LOGE, S0);
-        ks_round<LOGN, LOGB, R, S0, FIRST>(s, dig, tw, q, b);
-        __syncthreads();
-        ks_rounds<LOGN, LOGB, LOGE, S0 + R, false>(s, dig, tw, q, b);
-    }
-}
-
-// blockIdx.x = (ct * limbs + i) * nblocks + b
-template <int LOGN, int LOGB, int LOGE, int T>
-__global__ void __launch_bounds__(T) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
+// blockIdx.x = (ct * limbs + i) * nblocks + b. Per digit t: lift -> NTT
+// (shared rounds) -> in the last butterfly round, each thread multiplies its
+// outputs by (b_t, a_t) and accumulates into registers; the accumulator
+// positions are the thread's last-round positions, identical for every t.
+template <int LOGN, int LOGB, int LOGE, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
                                                  const u64* __restrict__ evk_sh, u64* __restrict__ acc01, int level, int D) {
     extern __shared__ u64 smem[];
-    constexpr int B = 1 << LOGB, C = LOGN - LOGB, P = B / T;
+    constexpr int B = 1 << LOGB, C = LOGN - LOGB;
+    constexpr int SL = ntt::last_round_start(LOGB, LOGE);
+    constexpr int RL = LOGB - SL, EL = 1 << RL, UL = B >> RL, PL = (UL + T - 1) / T;
+    constexpr int GL = B >> SL, STRL = GL >> RL;
     const int limbs = level + 1;
     const long long cta = blockIdx.x;
     const int b = static_cast<int>(cta & ((1 << C) - 1));
@@ -215,50 +168,72 @@ __global__ void __launch_bounds__(T) k_keyswitch(DevRing R, const u32* __restric
     const ulonglong2* tw = R.fwd + (static_cast<long long>(i) << LOGN);
     const long long n = 1LL << LOGN;
     const long long key_stride = static_cast<long long>(R.limbs) * n;  // one evk polynomial
+    const long long blk_off = static_cast<long long>(b) << LOGB;
 
-    u64 a0[P], a1[P];
+    u64 a0[PL * EL], a1[PL * EL];
 #pragma unroll
-    for (int k = 0; k < P; ++k) a0[k] = a1[k] = 0;
+    for (int k = 0; k < PL * EL; ++k) a0[k] = a1[k] = 0;
 
     for (int t = 0; t < D; ++t) {
         const u32* dig = digits + (ct * D + t) * n;
-        ks_rounds<LOGN, LOGB, LOGE, 0, true>(smem, dig, tw, q, b);
-        const long long kb = (2LL * t) * key_stride + static_cast<long long>(i) * n + (static_cast<long long>(b) << LOGB);
-        const long long ka = kb + key_stride;
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            const int j = threadIdx.x + k * T;
-            const u64 v = smem[swz(j)];
-            u64 s0 = a0[k] + mul_shoup_lazy(v, evk[kb + j], evk_sh[kb + j], q);
-            u64 s1 = a1[k] + mul_shoup_lazy(v, evk[ka + j], evk_sh[ka + j], q);
-            a0[k] = s0 >= two_q ? s0 - two_q : s0;
-            a1[k] = s1 >= two_q ? s1 - two_q : s1;
-        }
-        __syncthreads();
+        const u64* eb = evk + (2LL * t) * key_stride + static_cast<long long>(i) * n + blk_off;
+        const u64* ebs = evk_sh + (2LL * t) * key_stride + static_cast<long long>(i) * n + blk_off;
+        const u64* ea = eb + key_stride;
+        const u64* eas = ebs + key_stride;
+        ntt::fwd_block<LOGB, LOGE, T>(
+            smem, tw, q, b, C, [=](int r) { return column_value<LOGN, C>(dig, tw, q, r, b); },
+            [&](int idx, u64 v, int uu, int k) {
+                const u64 s0 = a0[uu * EL + k] + mul_shoup_lazy(v, eb[idx], ebs[idx], q);
+                const u64 s1 = a1[uu * EL + k] + mul_shoup_lazy(v, ea[idx], eas[idx], q);
+                a0[uu * EL + k] = s0 >= two_q ? s0 - two_q : s0;
+                a1[uu * EL + k] = s1 >= two_q ? s1 - two_q : s1;
+            });
+        __syncthreads();  // the next digit's first round overwrites shared memory
     }
-    u64* o0 = acc01 + ((ct * 2) * limbs + i) * n + (static_cast<long long>(b) << LOGB);
+    u64* o0 = acc01 + ((ct * 2) * limbs + i) * n + blk_off;
     u64* o1 = o0 + static_cast<long long>(limbs) * n;
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const int j = threadIdx.x + k * T;
-        o0[j] = add_mod(o0[j], reduce_2q(a0[k], q), q);
-        o1[j] = add_mod(o1[j], reduce_2q(a1[k], q), q);
+    for (int uu = 0; uu < PL; ++uu) {
+        const int u = threadIdx.x + uu * T;
+        if (UL % T != 0 && u >= UL) break;
+        const int base = (u / STRL) * GL + (u % STRL);
+#pragma unroll
+        for (int k = 0; k < EL; ++k) {
+            const int idx = base + k * STRL;
+            o0[idx] = add_mod(o0[idx], reduce_2q(a0[uu * EL + k], q), q);
+            o1[idx] = add_mod(o1[idx], reduce_2q(a1[uu * EL + k], q), q);
+        }
     }
 }
 
+#ifndef HECNN_KS_LOGB
+#define HECNN_KS_LOGB 13
+#endif
+#ifndef HECNN_KS_LOGE
+#define HECNN_KS_LOGE 3
+#endif
+#ifndef HECNN_KS_MAXT
+#define HECNN_KS_MAXT 1024
+#endif
+#ifndef HECNN_KS_MINB
+#define HECNN_KS_MINB 1
+#endif
+
 template <int LOGN>
 struct KsPlan {
-    static constexpr int LOGB = LOGN <= 13 ? LOGN : 13;
-    static constexpr int LOGE = LOGB >= 8 ? 4 : 3;
+    static constexpr int LOGB = LOGN <= HECNN_KS_LOGB ? LOGN : HECNN_KS_LOGB;
+    static constexpr int LOGE = LOGB >= 8 ? HECNN_KS_LOGE : 3;
     static constexpr int B = 1 << LOGB;
-    static constexpr int T = B >= 8192 ? 512 : (B >= 64 ? B / 16 : B < 32 ? B : 32);
+    static constexpr int UNITS = B >> LOGE;
+    static constexpr int T = UNITS >= HECNN_KS_MAXT ? HECNN_KS_MAXT : (UNITS >= 32 ? UNITS : (B < 32 ? B : 32));
+    static constexpr int MINB = T >= 256 ? HECNN_KS_MINB : 1;
 };
 
 template <int LOGN>
 void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, u64* acc01, int level,
                    int D, std::size_t count, const Launch& L) {
     using P = KsPlan<LOGN>;
-    auto kern = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T>;
+    auto kern = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB>;
     const int smem = P::B * 8;
     static bool init = (smem > 48 * 1024 ? (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true) : true);
     (void)init;

@@ -22,43 +22,100 @@ namespace {
 constexpr int TPB = 256;
 constexpr int OCT = 8;
 
+// acc += a * b (32 x 32 -> 64, accumulated in one instruction)
+__device__ __forceinline__ void mad_wide(u64& acc, u32 a, u32 b) {
+    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
+}
+
+constexpr int KCHUNK = 128;
+
+// One thread = one (component, limb, coefficient) column of OCT output
+// channels of one pixel. The pixel's taps (source cell, weight row) and the
+// limb's weights for the OCT channels are staged in shared memory per chunk
+// of KCHUNK taps, so the inner loop is: one coalesced HBM/L2 load of the
+// input word, then OCT multiply-accumulates against broadcast shared words.
 __global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, const u64* __restrict__ x,
                                                     u64* __restrict__ y, int level) {
+    __shared__ int s_src[KCHUNK];
+    __shared__ uint2 s_w[KCHUNK][OCT];
+    __shared__ ulonglong2 s_ws[KCHUNK][OCT];
     const int limbs = level + 1;
     const long long poly_words = static_cast<long long>(limbs) * R.n;
     const long long cell_words = 2 * poly_words;
-    const long long col = static_cast<long long>(blockIdx.x) * TPB + threadIdx.x;
-    if (col >= cell_words) return;
+    const int tpb = blockDim.x;  // <= n, so a CTA's columns share one limb
+    const long long col0 = static_cast<long long>(blockIdx.x) * tpb;
+    const long long col = col0 + threadIdx.x;
+    const bool live = col < cell_words;
     const int comp = static_cast<int>(col / poly_words);
-    const int i = static_cast<int>((col / R.n) % limbs);
+    const int i = static_cast<int>(((live ? col : col0) / R.n) % limbs);  // uniform when n >= TPB
     const int j = static_cast<int>(col % R.n);
     const int pixel = blockIdx.y;
     const int oc0 = blockIdx.z * OCT;
-    const u64 q = R.mod[i].q, two_q = q << 1;
-
-    u64 acc[OCT];
-#pragma unroll
-    for (int o = 0; o < OCT; ++o) acc[o] = 0;
-
+    const ModConst m = R.mod[i];
+    const u64 q = m.q, two_q = q << 1;
     const int* src = g.src + static_cast<long long>(pixel) * g.K;
     const int* wrow = g.wrow + static_cast<long long>(pixel) * g.K;
-    for (int k = 0; k < g.K; ++k) {
-        const int s = src[k];
-        if (s < 0) continue;
-        const u64 v = x[s * cell_words + col];
-        const ulonglong2* w = g.weights + (static_cast<long long>(wrow[k]) * g.oc_pad + oc0) * limbs + i;
+    const bool split = q < (1ull << 41);  // x, w < 2^41: 21/20-bit halves, exact 64-bit sums
+
+    u64 s00[OCT], smid[OCT], s11[OCT];
 #pragma unroll
-        for (int o = 0; o < OCT; ++o) {
-            const ulonglong2 c = w[o * limbs];
-            const u64 t = acc[o] + mul_shoup_lazy(v, c.x, c.y, q);
-            acc[o] = t >= two_q ? t - two_q : t;
+    for (int o = 0; o < OCT; ++o) s00[o] = smid[o] = s11[o] = 0;
+
+    for (int k0 = 0; k0 < g.K; k0 += KCHUNK) {
+        const int kn = min(KCHUNK, g.K - k0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < kn * OCT; t += tpb) {
+            const int k = t / OCT, o = t % OCT;
+            const long long at = (static_cast<long long>(wrow[k0 + k]) * g.oc_pad + oc0 + o) * limbs + i;
+            if (split) s_w[k][o] = g.wsplit[at];
+            else s_ws[k][o] = g.weights[at];
+            if (o == 0) s_src[k] = src[k0 + k];
+        }
+        __syncthreads();
+        if (!live) continue;
+        if (split) {
+            for (int k = 0; k < kn; ++k) {
+                const int s = s_src[k];
+                if (s < 0) continue;
+                const u64 v = x[s * cell_words + col];
+                const u32 v0 = static_cast<u32>(v) & 0x1FFFFFu, v1 = static_cast<u32>(v >> 21);
+#pragma unroll
+                for (int o = 0; o < OCT; ++o) {
+                    const uint2 c = s_w[k][o];
+                    mad_wide(s00[o], v0, c.x);
+                    mad_wide(smid[o], v0, c.y);
+                    mad_wide(smid[o], v1, c.x);
+                    mad_wide(s11[o], v1, c.y);
+                }
+            }
+        } else {
+            for (int k = 0; k < kn; ++k) {
+                const int s = s_src[k];
+                if (s < 0) continue;
+                const u64 v = x[s * cell_words + col];
+#pragma unroll
+                for (int o = 0; o < OCT; ++o) {
+                    const ulonglong2 c = s_ws[k][o];
+                    const u64 t = s00[o] + mul_shoup_lazy(v, c.x, c.y, q);
+                    s00[o] = t >= two_q ? t - two_q : t;
+                }
+            }
         }
     }
+    if (!live) return;
+    const ulonglong2 c21 = g.recomb[2 * i], c42 = g.recomb[2 * i + 1];
 #pragma unroll
     for (int o = 0; o < OCT; ++o) {
         const int oc = oc0 + o;
         if (oc >= g.oc) break;
-        u64 v = reduce_2q(acc[o], q);
+        u64 v;
+        if (split) {
+            v = reduce128(s00[o], 0, m);
+            v = add_mod(v, mul_shoup(reduce128(smid[o], 0, m), c21.x, c21.y, q), q);
+            v = add_mod(v, mul_shoup(reduce128(s11[o], 0, m), c42.x, c42.y, q), q);
+        } else {
+            v = reduce_2q(s00[o], q);
+        }
         if (g.bias && comp == 0 && j == 0) v = add_mod(v, g.bias[static_cast<long long>(oc) * limbs + i], q);
         y[(static_cast<long long>(pixel) * g.out_stride_pixel + oc) * cell_words + col] = v;
     }
@@ -96,12 +153,13 @@ __global__ void k_gather_cells(const u64* __restrict__ x, const int* __restrict_
 
 void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, const Launch& L) {
     const long long cell_words = 2LL * (level + 1) * R.n;
-    dim3 grid(static_cast<unsigned>((cell_words + TPB - 1) / TPB), static_cast<unsigned>(g.pixels),
+    const int tpb = std::min(TPB, R.n);
+    dim3 grid(static_cast<unsigned>((cell_words + tpb - 1) / tpb), static_cast<unsigned>(g.pixels),
               static_cast<unsigned>((g.oc + OCT - 1) / OCT));
     if (!g.pixels || !g.oc) return;
     L.begin("k_gather_mac", double(g.pixels) * g.K * g.oc * cell_words,
             8.0 * cell_words * (double(g.pixels) * g.oc + g.pixels * g.K));
-    k_gather_mac<<<grid, TPB, 0, L.stream>>>(R, g, x, y, level);
+    k_gather_mac<<<grid, tpb, 0, L.stream>>>(R, g, x, y, level);
     L.count();
     check_launch("gather_mac");
 }

@@ -22,126 +22,22 @@
 
 #include <stdexcept>
 
-#include "kernels.hpp"
+#include "ntt_core.cuh"
 
 namespace hecnn_b200 {
 
 namespace {
 
-// 16-nibble table of the XOR swizzle: bits 4..7 of the index select a 4-bit
-// mask for bits 0..3 (images of bit 4,5,6,7: 1111, 1010, 1100, 1000).
-__device__ __forceinline__ int swz(int i) {
-    return i ^ static_cast<int>((0x1eb4d278963c5af0ull >> (4 * ((i >> 4) & 15))) & 15);
-}
-
-__device__ __forceinline__ void ct_butterfly(u64& a, u64& b, ulonglong2 w, u64 q, u64 two_q) {
-    u64 u = a;
-    if (u >= two_q) u -= two_q;
-    u64 v = mul_shoup_lazy(b, w.x, w.y, q);
-    a = u + v;
-    b = u + two_q - v;
-}
-
-__device__ __forceinline__ void gs_butterfly(u64& a, u64& b, ulonglong2 w, u64 q, u64 two_q) {
-    u64 u = a, v = b;
-    u64 s = u + v;
-    if (s >= two_q) s -= two_q;
-    a = s;
-    b = mul_shoup_lazy(u + two_q - v, w.x, w.y, q);
-}
-
-__host__ __device__ constexpr int ceil_div(int a, int b) { return (a + b - 1) / b; }
-// Size of the round that starts at local stage s of a LOGB-stage block when
-// rounds hold at most LOGE stages (balanced split, e.g. 13 -> 4,3,3,3).
-__host__ __device__ constexpr int round_size(int LOGB, int LOGE, int s) {
-    return ceil_div(LOGB - s, ceil_div(LOGB - s, LOGE));
-}
-
-// One forward round: local stages S0..S0+R-1 of block `b`, whose first global
-// stage is `c` (c = LOGN - LOGB). FROM_GLOBAL reads the block from `g`
-// instead of shared memory.
-template <int LOGB, int R, int S0, bool FROM_GLOBAL>
-__device__ __forceinline__ void fwd_round(u64* s, const u64* __restrict__ g, const ulonglong2* __restrict__ tw, u64 q,
-                                          int b, int c) {
-    constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R;
-    const u64 two_q = q << 1;
-    for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
-        const int grp = u / STRIDE, col = u % STRIDE;
-        const int base = grp * G + col;
-        u64 x[E];
-#pragma unroll
-        for (int k = 0; k < E; ++k) x[k] = FROM_GLOBAL ? g[base + k * STRIDE] : s[swz(base + k * STRIDE)];
-#pragma unroll
-        for (int rho = 0; rho < R; ++rho) {
-            const int st = c + S0 + rho;  // global stage
-            const int half = E >> (rho + 1);
-            const int tbase = (1 << st) + (b << (S0 + rho)) + (grp << rho);
-#pragma unroll
-            for (int blk = 0; blk < (1 << rho); ++blk) {
-                const ulonglong2 w = tw[tbase + blk];
-#pragma unroll
-                for (int kk = 0; kk < half; ++kk) ct_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < E; ++k) s[swz(base + k * STRIDE)] = x[k];
-    }
-}
-
-template <int LOGB, int LOGE, int S0, bool FIRST>
-__device__ __forceinline__ void fwd_rounds(u64* s, const u64* g, const ulonglong2* tw, u64 q, int b, int c) {
-    if constexpr (S0 < LOGB) {
-        constexpr int R = round_size(LOGB, LOGE, S0);
-        fwd_round<LOGB, R, S0, FIRST>(s, g, tw, q, b, c);
-        __syncthreads();
-        fwd_rounds<LOGB, LOGE, S0 + R, false>(s, g, tw, q, b, c);
-    }
-}
-
-// One inverse round: stages S0+R-1 down to S0 (GS order).
-template <int LOGB, int R, int S0>
-__device__ __forceinline__ void inv_round(u64* s, const ulonglong2* __restrict__ tw, u64 q, int b, int c) {
-    constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R;
-    const u64 two_q = q << 1;
-    for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
-        const int grp = u / STRIDE, col = u % STRIDE;
-        const int base = grp * G + col;
-        u64 x[E];
-#pragma unroll
-        for (int k = 0; k < E; ++k) x[k] = s[swz(base + k * STRIDE)];
-#pragma unroll
-        for (int rho = R - 1; rho >= 0; --rho) {
-            const int st = c + S0 + rho;
-            const int half = E >> (rho + 1);
-            const int tbase = (1 << st) + (b << (S0 + rho)) + (grp << rho);
-#pragma unroll
-            for (int blk = 0; blk < (1 << rho); ++blk) {
-                const ulonglong2 w = tw[tbase + blk];
-#pragma unroll
-                for (int kk = 0; kk < half; ++kk) gs_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < E; ++k) s[swz(base + k * STRIDE)] = x[k];
-    }
-}
-
-// Inverse rounds are the forward decomposition traversed backwards.
-template <int LOGB, int LOGE, int S0>
-__device__ __forceinline__ void inv_rounds(u64* s, const ulonglong2* tw, u64 q, int b, int c) {
-    if constexpr (S0 < LOGB) {
-        constexpr int R = round_size(LOGB, LOGE, S0);
-        inv_rounds<LOGB, LOGE, S0 + R>(s, tw, q, b, c);
-        inv_round<LOGB, R, S0>(s, tw, q, b, c);
-        __syncthreads();
-    }
-}
+using ntt::ct_butterfly;
+using ntt::gs_butterfly;
 
 // Block kernels: blockIdx.x = (poly * nblocks + block); limb = poly % limbs.
-template <int LOGN, int LOGB, int LOGE, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_ntt_fwd_block(DevRing R, u64* __restrict__ data, int limbs) {
+// The first forward round reads HBM and the last round writes HBM directly
+// (canonical values); the inverse likewise, with n^-1 folded into the store.
+template <int LOGN, int LOGB, int LOGE, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_ntt_fwd_block(DevRing R, u64* __restrict__ data, int limbs) {
     extern __shared__ u64 smem[];
-    constexpr int B = 1 << LOGB, C = LOGN - LOGB;
+    constexpr int C = LOGN - LOGB;
     const long long cta = blockIdx.x;
     const long long poly = cta >> C;
     const int b = static_cast<int>(cta & ((1 << C) - 1));
@@ -149,14 +45,15 @@ __global__ void __launch_bounds__(THREADS) k_ntt_fwd_block(DevRing R, u64* __res
     const u64 q = R.mod[limb].q;
     u64* g = data + (poly << LOGN) + (static_cast<long long>(b) << LOGB);
     const ulonglong2* tw = R.fwd + (static_cast<long long>(limb) << LOGN);
-    fwd_rounds<LOGB, LOGE, 0, true>(smem, g, tw, q, b, C);
-    for (int i = threadIdx.x; i < B; i += THREADS) g[i] = reduce_4q(smem[swz(i)], q);
+    ntt::fwd_block<LOGB, LOGE, THREADS>(
+        smem, tw, q, b, C, [=](int i) { return g[i]; },
+        [=](int i, u64 v, int, int) { g[i] = reduce_4q(v, q); });
 }
 
-template <int LOGN, int LOGB, int LOGE, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_ntt_inv_block(DevRing R, u64* __restrict__ data, int limbs) {
+template <int LOGN, int LOGB, int LOGE, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_block(DevRing R, u64* __restrict__ data, int limbs) {
     extern __shared__ u64 smem[];
-    constexpr int B = 1 << LOGB, C = LOGN - LOGB;
+    constexpr int C = LOGN - LOGB;
     const long long cta = blockIdx.x;
     const long long poly = cta >> C;
     const int b = static_cast<int>(cta & ((1 << C) - 1));
@@ -164,15 +61,13 @@ __global__ void __launch_bounds__(THREADS) k_ntt_inv_block(DevRing R, u64* __res
     const u64 q = R.mod[limb].q;
     u64* g = data + (poly << LOGN) + (static_cast<long long>(b) << LOGB);
     const ulonglong2* tw = R.inv + (static_cast<long long>(limb) << LOGN);
-    for (int i = threadIdx.x; i < B; i += THREADS) smem[swz(i)] = g[i];
-    __syncthreads();
-    inv_rounds<LOGB, LOGE, 0>(smem, tw, q, b, C);
-    if constexpr (C == 0) {
-        const ulonglong2 ni = R.n_inv[limb];
-        for (int i = threadIdx.x; i < B; i += THREADS) g[i] = reduce_2q(mul_shoup_lazy(smem[swz(i)], ni.x, ni.y, q), q);
-    } else {
-        for (int i = threadIdx.x; i < B; i += THREADS) g[i] = smem[swz(i)];  // [0,2q), columns finish
-    }
+    const ulonglong2 ni = R.n_inv[limb];
+    ntt::inv_block<LOGB, LOGE, THREADS>(
+        smem, tw, q, b, C, [=](int i) { return g[i]; },
+        [=](int i, u64 v, int, int) {
+            if constexpr (C == 0) g[i] = reduce_2q(mul_shoup_lazy(v, ni.x, ni.y, q), q);
+            else g[i] = v;  // [0,2q); the column pass finishes
+        });
 }
 
 // Column passes for N > 2^LOGB: the C stages that couple the 2^C blocks.
@@ -239,13 +134,24 @@ void set_smem(K kernel, int bytes) {
     if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
+#ifndef HECNN_NTT_LOGE
+#define HECNN_NTT_LOGE 3
+#endif
+#ifndef HECNN_NTT_MAXT
+#define HECNN_NTT_MAXT 512
+#endif
+#ifndef HECNN_NTT_MINB
+#define HECNN_NTT_MINB 2
+#endif
+
 template <int LOGN>
 struct NttPlan {
     static constexpr int LOGB = LOGN <= 14 ? LOGN : 13;
     static constexpr int C = LOGN - LOGB;
-    static constexpr int LOGE = LOGB >= 8 ? 4 : 3;
+    static constexpr int LOGE = LOGB >= 8 ? HECNN_NTT_LOGE : 3;
     static constexpr int UNITS = (1 << LOGB) >> LOGE;
-    static constexpr int THREADS = UNITS >= 512 ? 512 : (UNITS >= 32 ? UNITS : 32);
+    static constexpr int THREADS = UNITS >= HECNN_NTT_MAXT ? HECNN_NTT_MAXT : (UNITS >= 32 ? UNITS : 32);
+    static constexpr int MINB = THREADS >= 256 ? HECNN_NTT_MINB : 1;
 };
 
 template <int LOGN>
@@ -257,7 +163,7 @@ void run_forward(const DevRing& R, u64* data, int limbs, std::size_t polys, cons
         k_ntt_fwd_cols<LOGN, P::C><<<static_cast<unsigned>((total + 255) / 256), 256, 0, L.stream>>>(R, data, limbs, total);
         L.count();
     }
-    auto kern = k_ntt_fwd_block<LOGN, P::LOGB, P::LOGE, P::THREADS>;
+    auto kern = k_ntt_fwd_block<LOGN, P::LOGB, P::LOGE, P::THREADS, P::MINB>;
     const int smem = (1 << P::LOGB) * 8;
     static bool init = (set_smem(kern, smem), true);
     (void)init;
@@ -269,7 +175,7 @@ void run_forward(const DevRing& R, u64* data, int limbs, std::size_t polys, cons
 template <int LOGN>
 void run_inverse(const DevRing& R, u64* data, int limbs, std::size_t polys, const Launch& L) {
     using P = NttPlan<LOGN>;
-    auto kern = k_ntt_inv_block<LOGN, P::LOGB, P::LOGE, P::THREADS>;
+    auto kern = k_ntt_inv_block<LOGN, P::LOGB, P::LOGE, P::THREADS, P::MINB>;
     const int smem = (1 << P::LOGB) * 8;
     static bool init = (set_smem(kern, smem), true);
     (void)init;
