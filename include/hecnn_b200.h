@@ -86,6 +86,9 @@ int hecnn_profile_reset(hecnn_context* ctx);
 int hecnn_profile_read(hecnn_context* ctx, char* buf, size_t len);
 /* Integer-pipe roofline probe: chained 64-bit Shoup modular multiplies/s. */
 int hecnn_modmul_peak(hecnn_context* ctx, double* modmul_per_s);
+/* FP64-pipe roofline probe: chained exact FP64 modular multiplies/s (the
+ * arithmetic the NTT/key-switch kernels use for primes below 2^42). */
+int hecnn_fp64_modmul_peak(hecnn_context* ctx, double* modmul_per_s);
 
 /* ---- keys: CkksEngine::keygen (ckks.hpp:200-236). Randomness is sampled on
  * the host (mt19937_64 + libm, bit-identical to the reference); NTTs and

@@ -46,7 +46,7 @@ EXPORTED_SYMBOLS = (
     "hecnn_model_create", "hecnn_model_destroy", "hecnn_model_depth_cost", "hecnn_forward_encrypted",
     "hecnn_profile_enable", "hecnn_profile_reset", "hecnn_profile_read", "hecnn_modmul_peak",
     "hecnn_tensor_copy_to_device", "hecnn_host_encode_real", "hecnn_host_decode_real",
-    "hecnn_host_encryption_randomness",
+    "hecnn_host_encryption_randomness", "hecnn_fp64_modmul_peak",
 )
 
 _lib = None
@@ -77,6 +77,7 @@ _SIGNATURES = {
     "hecnn_profile_reset": [_V],
     "hecnn_profile_read": [_V, ctypes.c_char_p, _SZ],
     "hecnn_modmul_peak": [_V, _PD],
+    "hecnn_fp64_modmul_peak": [_V, _PD],
     "hecnn_keygen": [_V, _U64],
     "hecnn_import_keys": [_V, _PU64, _PU64, _PU64, _PU64, _SZ],
     "hecnn_export_secret_key": [_V, _PU64],
@@ -658,6 +659,11 @@ class CkksEngine:
     def modmul_peak(self) -> float:
         v = ctypes.c_double()
         _check(lib().hecnn_modmul_peak(self.ctx, ctypes.byref(v)))
+        return v.value
+
+    def fp64_modmul_peak(self) -> float:
+        v = ctypes.c_double()
+        _check(lib().hecnn_fp64_modmul_peak(self.ctx, ctypes.byref(v)))
         return v.value
 
     def copy_to_device(self, t: "EncryptedTensor", dst_ptr: int):

@@ -212,6 +212,10 @@ int hecnn_modmul_peak(hecnn_context* ctx, double* modmul_per_s) {
     return guard([&] { *modmul_per_s = measure_modmul_peak(C(ctx)); });
 }
 
+int hecnn_fp64_modmul_peak(hecnn_context* ctx, double* modmul_per_s) {
+    return guard([&] { *modmul_per_s = measure_modmul_peak(C(ctx), true); });
+}
+
 int hecnn_tensor_copy_to_device(hecnn_context* ctx, const hecnn_tensor* t, void* dst) {
     return guard([&] {
         Context& c = C(ctx);

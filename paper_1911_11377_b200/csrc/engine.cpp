@@ -280,6 +280,12 @@ Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, doubl
     dev.modulus = tables.back().as<u64>();
     tables.push_back(upload_vec(inv_q));
     dev.inv_q = tables.back().as<double>();
+    tables.push_back(upload_vec(ring.fwd_f));
+    dev.fwd_f = tables.back().as<double>();
+    tables.push_back(upload_vec(ring.inv_f));
+    dev.inv_f = tables.back().as<double>();
+    tables.push_back(upload_vec(ring.n_inv_f));
+    dev.n_inv_f = tables.back().as<double>();
     dev.n = static_cast<int>(ring.n);
     dev.logn = static_cast<int>(ring.logn);
     dev.limbs = static_cast<int>(ring.limbs);
@@ -296,6 +302,7 @@ Context::~Context() {
     pk.reset();
     evk.reset();
     evk_sh.reset();
+    evk_f.reset();
     tables.clear();
     cudaStreamSynchronize(stream);
     if (own_stream) cudaStreamDestroy(stream);
@@ -315,16 +322,17 @@ void Context::download(void* dst, const void* src, std::size_t bytes) {
 
 void Context::sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
 
-double measure_modmul_peak(Context& C) {
+double measure_modmul_peak(Context& C, bool fp64) {
     DevBuf sink(&C, 64);
     Launch L = C.L();
-    modmul_probe(C.dev, 64, sink.as<u64>(), L);  // warm-up
+    auto probe = fp64 ? fp64_modmul_probe : modmul_probe;
+    probe(C.dev, 64, sink.as<u64>(), L);  // warm-up
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     const int iters = 4096;
     cudaEventRecord(a, C.stream);
-    double ops = modmul_probe(C.dev, iters, sink.as<u64>(), L);
+    double ops = probe(C.dev, iters, sink.as<u64>(), L);
     cudaEventRecord(b, C.stream);
     C.sync();
     float ms = 0;
@@ -406,6 +414,8 @@ void keygen(Context& C, u64 seed) {
         poly_elementwise(C.dev, EwOp::Add, bt, et_dev.as<u64>(), bt, static_cast<int>(top), 1, L);
     }
     shoup_table(C.dev, C.evk.as<u64>(), C.evk_sh.as<u64>(), static_cast<int>(limbs), 2 * D, L);
+    C.evk_f = DevBuf(&C, D * 2 * poly * sizeof(double));
+    fp_table(C.dev, C.evk.as<u64>(), C.evk_f.as<double>(), static_cast<int>(limbs), 2 * D, L);
     C.evk_digits = D;
     C.has_secret = C.has_pk = true;
     C.sync();
@@ -431,6 +441,8 @@ void import_keys(Context& C, const u64* secret, const u64* pk_b, const u64* pk_a
         C.evk_sh = DevBuf(&C, digits * 2 * poly * sizeof(u64));
         C.upload(C.evk.get(), evk, digits * 2 * poly * sizeof(u64));
         shoup_table(C.dev, C.evk.as<u64>(), C.evk_sh.as<u64>(), static_cast<int>(C.top() + 1), 2 * digits, L);
+        C.evk_f = DevBuf(&C, digits * 2 * poly * sizeof(double));
+        fp_table(C.dev, C.evk.as<u64>(), C.evk_f.as<double>(), static_cast<int>(C.top() + 1), 2 * digits, L);
         C.evk_digits = digits;
     }
     C.sync();
@@ -463,8 +475,8 @@ void key_switch_raw(Context& C, const u64* d2, u64* out, std::size_t level, std:
     cuda_check(cudaMemcpyAsync(tmp.get(), d2, count * limbs * n * sizeof(u64), cudaMemcpyDeviceToDevice, C.stream), "copy");
     crt_digits(C.dev, tmp.as<u64>(), dig.as<u32>(), static_cast<int>(level), static_cast<int>(D), count, L);
     cuda_check(cudaMemsetAsync(out, 0, count * 2 * limbs * n * sizeof(u64), C.stream), "memset");
-    keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), out, static_cast<int>(level),
-                  static_cast<int>(D), count, L);
+    keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), C.evk_f.as<double>(), out,
+                  static_cast<int>(level), static_cast<int>(D), count, L);
 }
 
 // mul / square (ckks.hpp:315-369): tensor -> INTT(d2) -> key switch -> INTT -> rescale.
@@ -507,8 +519,8 @@ static TensorPtr relin_product(Context& C, const Tensor& x, const Tensor* y) {
         }
         ntt_inverse(C.dev, d2.as<u64>(), lv, m, L);
         crt_digits(C.dev, d2.as<u64>(), dig.as<u32>(), lv, static_cast<int>(D), m, L);
-        keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), d01.as<u64>(), lv,
-                      static_cast<int>(D), m, L);
+        keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), C.evk_f.as<double>(),
+                      d01.as<u64>(), lv, static_cast<int>(D), m, L);
         ntt_inverse(C.dev, d01.as<u64>(), lv, 2 * m, L);
         rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L);
     }

@@ -77,7 +77,7 @@ struct Context {
     std::vector<DevBuf> tables;
     // keys (device resident; the secret also kept on the host for export)
     std::vector<u64> secret_host;  // [(L+1)][n] coefficient domain
-    DevBuf s_ntt, pk, evk, evk_sh;
+    DevBuf s_ntt, pk, evk, evk_sh, evk_f;
     std::size_t evk_digits = 0;
     bool has_secret = false, has_pk = false;
     unsigned long long launches = 0;
@@ -131,7 +131,7 @@ using TensorPtr = std::unique_ptr<Tensor>;
 
 TensorPtr make_tensor(Context& C, std::size_t cells, std::uint32_t level, double scale);
 // Integer-pipe peak: Shoup modmuls per second measured with CUDA events.
-double measure_modmul_peak(Context& C);
+double measure_modmul_peak(Context& C, bool fp64 = false);
 
 // ---- keys
 void keygen(Context& C, u64 seed);

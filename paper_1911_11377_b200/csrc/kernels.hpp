@@ -27,6 +27,10 @@ struct DevRing {
     const u64* punct = nullptr;              // [limbs][limbs][crt_words] Q_l/q_i
     const u64* modulus = nullptr;            // [limbs][crt_words] Q_l
     const double* inv_q = nullptr;           // [limbs] 1/q_i
+    // FP64-path tables (limbs with q < 2^42): residues as exact doubles
+    const double* fwd_f = nullptr;           // [limbs][n]
+    const double* inv_f = nullptr;           // [limbs][n]
+    const double* n_inv_f = nullptr;         // [limbs]
 };
 
 // Optional per-kernel timing: CUDA events recorded on the launching stream
@@ -100,6 +104,8 @@ void add_coeff0(const DevRing& R, u64* cts, const u64* consts, int level, std::s
 
 // Shoup companions floor(w * 2^64 / q_i) of a [count][limbs][n] table (evk)
 void shoup_table(const DevRing& R, const u64* in, u64* out, int limbs, std::size_t count, const Launch& L);
+// FP64-path copy (exact doubles) of a [count][limbs][n] residue table (evk)
+void fp_table(const DevRing& R, const u64* in, double* out, int limbs, std::size_t count, const Launch& L);
 
 // ---- key switching (keyswitch.cu)
 // CRT reconstruction + base-2^20 digits of d2 (coefficient domain): digits [count][D][n] u32
@@ -107,12 +113,15 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
                 const Launch& L);
 // acc01[ct] (NTT domain, [count][2][level+1][n]) += sum_t NTT(digit_t) * evk_t
 //   evk: [Dtop][2][limbs][n] values, evk_sh: Shoup companions
-void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, u64* acc01, int level,
-                   int D, std::size_t count, const Launch& L);
+//   evk_f: FP64-path copy (used for limbs with q < 2^42)
+void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
+                   u64* acc01, int level, int D, std::size_t count, const Launch& L);
 
 // Integer-pipe peak probe: chained Shoup modmuls (the NTT butterfly's
 // multiply), `iters` per thread over the whole GPU; returns modmuls issued.
 double modmul_probe(const DevRing& R, int iters, u64* sink, const Launch& L);
+// FP64-pipe peak probe: chained exact FP64 modmuls (ntt_core.cuh fmodmul).
+double fp64_modmul_probe(const DevRing& R, int iters, u64* sink, const Launch& L);
 
 // ---- linear layers (linear.cu)
 // Gather-MAC for conv/dense: see linear.cu for the table formats.

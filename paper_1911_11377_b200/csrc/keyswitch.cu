@@ -17,6 +17,7 @@
 //   block directly from the (L2-resident) u32 digits.
 
 #include <stdexcept>
+#include <type_traits>
 
 #include "ntt_core.cuh"
 
@@ -146,50 +147,51 @@ __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const u
     }
 }
 
-// blockIdx.x = (ct * limbs + i) * nblocks + b. Per digit t: lift -> NTT
-// (shared rounds) -> in the last butterfly round, each thread multiplies its
-// outputs by (b_t, a_t) and accumulates into registers; the accumulator
-// positions are the thread's last-round positions, identical for every t.
-template <int LOGN, int LOGB, int LOGE, int T, int MINB>
-__global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
-                                                 const u64* __restrict__ evk_sh, u64* __restrict__ acc01, int level, int D) {
+// Per digit t: lift -> forward NTT (shared rounds) -> in the last butterfly
+// round each thread multiplies its outputs by (b_t, a_t) and accumulates into
+// registers; accumulator positions are the thread's last-round positions,
+// identical for every t. A = IntArith (u64 Shoup, evk + evk_sh) or FpArith
+// (exact FP64, evk_f = e as doubles). The block's twiddles are staged once in
+// shared memory as a block-local table TL[2^s + m] = tw[2^(s+C) + b 2^s + m]
+// and reused by all D digit transforms (round code indexes it with b = c = 0).
+template <int LOGN, int LOGB, int LOGE, int T, class A, class KeyAt>
+__device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typename A::TW* tw, const u32* digits,
+                                        KeyAt key, u64* acc01, int level, int D, long long ct, int i, int b, u64 q) {
+    using V = typename A::V;
+    using TW = typename A::TW;
     extern __shared__ u64 smem[];
     constexpr int B = 1 << LOGB, C = LOGN - LOGB;
     constexpr int SL = ntt::last_round_start(LOGB, LOGE);
     constexpr int RL = LOGB - SL, EL = 1 << RL, UL = B >> RL, PL = (UL + T - 1) / T;
     constexpr int GL = B >> SL, STRL = GL >> RL;
-    const int limbs = level + 1;
-    const long long cta = blockIdx.x;
-    const int b = static_cast<int>(cta & ((1 << C) - 1));
-    const long long row = cta >> C;  // ct * limbs + i
-    const long long ct = row / limbs;
-    const int i = static_cast<int>(row % limbs);
-    const u64 q = R.mod[i].q, two_q = q << 1;
-    const ulonglong2* tw = R.fwd + (static_cast<long long>(i) << LOGN);
     const long long n = 1LL << LOGN;
-    const long long key_stride = static_cast<long long>(R.limbs) * n;  // one evk polynomial
     const long long blk_off = static_cast<long long>(b) << LOGB;
+    const ulonglong2* itw = R.fwd + (static_cast<long long>(i) << LOGN);  // integer twiddles for the column stages
 
-    u64 a0[PL * EL], a1[PL * EL];
+    TW* stw = reinterpret_cast<TW*>(smem + B);
+    for (int j = threadIdx.x + 1; j < B; j += T) {
+        const int s = 31 - __clz(j), m = j - (1 << s);
+        stw[j] = tw[(1 << (s + C)) + (b << s) + m];
+    }
+    __syncthreads();  // table complete before the first round reads it
+
+    V a0[PL * EL], a1[PL * EL];
 #pragma unroll
-    for (int k = 0; k < PL * EL; ++k) a0[k] = a1[k] = 0;
+    for (int k = 0; k < PL * EL; ++k) a0[k] = a1[k] = V(0);
 
     for (int t = 0; t < D; ++t) {
         const u32* dig = digits + (ct * D + t) * n;
-        const u64* eb = evk + (2LL * t) * key_stride + static_cast<long long>(i) * n + blk_off;
-        const u64* ebs = evk_sh + (2LL * t) * key_stride + static_cast<long long>(i) * n + blk_off;
-        const u64* ea = eb + key_stride;
-        const u64* eas = ebs + key_stride;
         ntt::fwd_block<LOGB, LOGE, T>(
-            smem, tw, q, b, C, [=](int r) { return column_value<LOGN, C>(dig, tw, q, r, b); },
-            [&](int idx, u64 v, int uu, int k) {
-                const u64 s0 = a0[uu * EL + k] + mul_shoup_lazy(v, eb[idx], ebs[idx], q);
-                const u64 s1 = a1[uu * EL + k] + mul_shoup_lazy(v, ea[idx], eas[idx], q);
-                a0[uu * EL + k] = s0 >= two_q ? s0 - two_q : s0;
-                a1[uu * EL + k] = s1 >= two_q ? s1 - two_q : s1;
-            });
+            reinterpret_cast<V*>(smem), ar, stw, 0, 0,
+            [=](int r) {
+                const u64 v = column_value<LOGN, C>(dig, itw, q, r, b);
+                if constexpr (std::is_same<V, double>::value) return ntt::to_fp(v);
+                else return v;
+            },
+            [&](int idx, V v, int uu, int k) { key(t, blk_off + idx, v, a0[uu * EL + k], a1[uu * EL + k]); });
         __syncthreads();  // the next digit's first round overwrites shared memory
     }
+    const int limbs = level + 1;
     u64* o0 = acc01 + ((ct * 2) * limbs + i) * n + blk_off;
     u64* o1 = o0 + static_cast<long long>(limbs) * n;
 #pragma unroll
@@ -200,9 +202,56 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
 #pragma unroll
         for (int k = 0; k < EL; ++k) {
             const int idx = base + k * STRL;
-            o0[idx] = add_mod(o0[idx], reduce_2q(a0[uu * EL + k], q), q);
-            o1[idx] = add_mod(o1[idx], reduce_2q(a1[uu * EL + k], q), q);
+            u64 r0, r1;
+            if constexpr (std::is_same<V, double>::value) {
+                r0 = ntt::fcanon(a0[uu * EL + k], ar.q, ar.qinv);
+                r1 = ntt::fcanon(a1[uu * EL + k], ar.q, ar.qinv);
+            } else {
+                r0 = reduce_2q(a0[uu * EL + k], q);
+                r1 = reduce_2q(a1[uu * EL + k], q);
+            }
+            o0[idx] = add_mod(o0[idx], r0, q);
+            o1[idx] = add_mod(o1[idx], r1, q);
         }
+    }
+}
+
+// blockIdx.x = (ct * limbs + i) * nblocks + b
+template <int LOGN, int LOGB, int LOGE, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
+                                                 const u64* __restrict__ evk_sh, const double* __restrict__ evk_f,
+                                                 u64* __restrict__ acc01, int level, int D) {
+    constexpr int C = LOGN - LOGB;
+    const int limbs = level + 1;
+    const long long cta = blockIdx.x;
+    const int b = static_cast<int>(cta & ((1 << C) - 1));
+    const long long row = cta >> C;  // ct * limbs + i
+    const long long ct = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    const u64 q = R.mod[i].q;
+    const long long n = 1LL << LOGN;
+    const long long key_stride = static_cast<long long>(R.limbs) * n;  // one evk polynomial
+    const long long ioff = static_cast<long long>(i) * n;
+    if (ntt::fp_limb(q)) {
+        const ntt::FpArith ar{static_cast<double>(q), R.inv_q[i]};
+        auto key = [=](int t, long long pos, double v, double& s0, double& s1) {
+            const double kb = evk_f[(2LL * t) * key_stride + ioff + pos];
+            const double ka = evk_f[(2LL * t + 1) * key_stride + ioff + pos];
+            s0 += ntt::fmodmul(v, kb, ar.q, ar.qinv);  // |s| < D q < 2^48: exact sums
+            s1 += ntt::fmodmul(v, ka, ar.q, ar.qinv);
+        };
+        ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd_f + ioff, digits, key, acc01, level, D, ct, i, b, q);
+    } else {
+        const ntt::IntArith ar{q, q << 1};
+        const u64 two_q = q << 1;
+        auto key = [=](int t, long long pos, u64 v, u64& s0, u64& s1) {
+            const long long kb = (2LL * t) * key_stride + ioff + pos, ka = kb + key_stride;
+            const u64 x0 = s0 + mul_shoup_lazy(v, evk[kb], evk_sh[kb], q);
+            const u64 x1 = s1 + mul_shoup_lazy(v, evk[ka], evk_sh[ka], q);
+            s0 = x0 >= two_q ? x0 - two_q : x0;
+            s1 = x1 >= two_q ? x1 - two_q : x1;
+        };
+        ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd + ioff, digits, key, acc01, level, D, ct, i, b, q);
     }
 }
 
@@ -213,7 +262,7 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
 #define HECNN_KS_LOGE 3
 #endif
 #ifndef HECNN_KS_MAXT
-#define HECNN_KS_MAXT 1024
+#define HECNN_KS_MAXT 512
 #endif
 #ifndef HECNN_KS_MINB
 #define HECNN_KS_MINB 1
@@ -230,11 +279,11 @@ struct KsPlan {
 };
 
 template <int LOGN>
-void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, u64* acc01, int level,
-                   int D, std::size_t count, const Launch& L) {
+void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
+                   u64* acc01, int level, int D, std::size_t count, const Launch& L) {
     using P = KsPlan<LOGN>;
     auto kern = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB>;
-    const int smem = P::B * 8;
+    const int smem = P::B * (8 + 16);  // data + staged twiddles (u64 Shoup pairs on the integer path)
     static bool init = (smem > 48 * 1024 ? (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true) : true);
     (void)init;
     const std::size_t ctas = count * static_cast<std::size_t>(level + 1) << (LOGN - P::LOGB);
@@ -244,7 +293,7 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
         L.begin("k_keyswitch", cl * D * (n / 2 * LOGN + 2 * n),
                 2.0 * D * (level + 1) * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
     }
-    kern<<<static_cast<unsigned>(ctas), P::T, smem, L.stream>>>(R, digits, evk, evk_sh, acc01, level, D);
+    kern<<<static_cast<unsigned>(ctas), P::T, smem, L.stream>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D);
     L.count();
 }
 
@@ -269,11 +318,11 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
     check_launch("crt_digits");
 }
 
-void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, u64* acc01, int level,
-                   int D, std::size_t count, const Launch& L) {
+void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
+                   u64* acc01, int level, int D, std::size_t count, const Launch& L) {
     if (!count) return;
 #define HECNN_KS_CASE(LG) \
-    case LG: run_keyswitch<LG>(R, digits, evk, evk_sh, acc01, level, D, count, L); break;
+    case LG: run_keyswitch<LG>(R, digits, evk, evk_sh, evk_f, acc01, level, D, count, L); break;
     switch (R.logn) {
         HECNN_KS_CASE(3) HECNN_KS_CASE(4) HECNN_KS_CASE(5) HECNN_KS_CASE(6) HECNN_KS_CASE(7) HECNN_KS_CASE(8)
         HECNN_KS_CASE(9) HECNN_KS_CASE(10) HECNN_KS_CASE(11) HECNN_KS_CASE(12) HECNN_KS_CASE(13)

@@ -13,7 +13,7 @@
 
 #include <algorithm>
 
-#include "kernels.hpp"
+#include "ntt_core.cuh"
 
 namespace hecnn_b200 {
 
@@ -21,11 +21,6 @@ namespace {
 
 constexpr int TPB = 256;
 constexpr int OCT = 8;
-
-// acc += a * b (32 x 32 -> 64, accumulated in one instruction)
-__device__ __forceinline__ void mad_wide(u64& acc, u32 a, u32 b) {
-    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
-}
 
 constexpr int KCHUNK = 128;
 
@@ -37,7 +32,7 @@ constexpr int KCHUNK = 128;
 __global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, const u64* __restrict__ x,
                                                     u64* __restrict__ y, int level) {
     __shared__ int s_src[KCHUNK];
-    __shared__ uint2 s_w[KCHUNK][OCT];
+    __shared__ double2 s_w[KCHUNK][OCT];
     __shared__ ulonglong2 s_ws[KCHUNK][OCT];
     const int limbs = level + 1;
     const long long poly_words = static_cast<long long>(limbs) * R.n;
@@ -55,11 +50,19 @@ __global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, cons
     const u64 q = m.q, two_q = q << 1;
     const int* src = g.src + static_cast<long long>(pixel) * g.K;
     const int* wrow = g.wrow + static_cast<long long>(pixel) * g.K;
-    const bool split = q < (1ull << 41);  // x, w < 2^41: 21/20-bit halves, exact 64-bit sums
+    // q < 2^42: x, w split at bit 21 into exact doubles; every partial product
+    // is < 2^42 and a chunk of KCHUNK taps sums below 2^51, so the FP64 pipe
+    // accumulates exactly; accumulators are centred mod q after each chunk.
+    const bool split = ntt::fp_limb(q);
+    const double qd = static_cast<double>(q), qinv = R.inv_q[i];
 
-    u64 s00[OCT], smid[OCT], s11[OCT];
+    u64 s00[OCT];
+    double f00[OCT], fmid[OCT], f11[OCT];
 #pragma unroll
-    for (int o = 0; o < OCT; ++o) s00[o] = smid[o] = s11[o] = 0;
+    for (int o = 0; o < OCT; ++o) {
+        s00[o] = 0;
+        f00[o] = fmid[o] = f11[o] = 0.0;
+    }
 
     for (int k0 = 0; k0 < g.K; k0 += KCHUNK) {
         const int kn = min(KCHUNK, g.K - k0);
@@ -67,8 +70,12 @@ __global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, cons
         for (int t = threadIdx.x; t < kn * OCT; t += tpb) {
             const int k = t / OCT, o = t % OCT;
             const long long at = (static_cast<long long>(wrow[k0 + k]) * g.oc_pad + oc0 + o) * limbs + i;
-            if (split) s_w[k][o] = g.wsplit[at];
-            else s_ws[k][o] = g.weights[at];
+            if (split) {
+                const uint2 w = g.wsplit[at];
+                s_w[k][o] = make_double2(static_cast<double>(w.x), static_cast<double>(w.y));
+            } else {
+                s_ws[k][o] = g.weights[at];
+            }
             if (o == 0) s_src[k] = src[k0 + k];
         }
         __syncthreads();
@@ -78,15 +85,21 @@ __global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, cons
                 const int s = s_src[k];
                 if (s < 0) continue;
                 const u64 v = x[s * cell_words + col];
-                const u32 v0 = static_cast<u32>(v) & 0x1FFFFFu, v1 = static_cast<u32>(v >> 21);
+                const double v0 = ntt::to_fp(v & 0x1FFFFFull), v1 = ntt::to_fp(v >> 21);
 #pragma unroll
                 for (int o = 0; o < OCT; ++o) {
-                    const uint2 c = s_w[k][o];
-                    mad_wide(s00[o], v0, c.x);
-                    mad_wide(smid[o], v0, c.y);
-                    mad_wide(smid[o], v1, c.x);
-                    mad_wide(s11[o], v1, c.y);
+                    const double2 c = s_w[k][o];
+                    f00[o] = fma(v0, c.x, f00[o]);
+                    fmid[o] = fma(v0, c.y, fmid[o]);
+                    fmid[o] = fma(v1, c.x, fmid[o]);
+                    f11[o] = fma(v1, c.y, f11[o]);
                 }
+            }
+#pragma unroll
+            for (int o = 0; o < OCT; ++o) {
+                f00[o] = ntt::fcentre(f00[o], qd, qinv);
+                fmid[o] = ntt::fcentre(fmid[o], qd, qinv);
+                f11[o] = ntt::fcentre(f11[o], qd, qinv);
             }
         } else {
             for (int k = 0; k < kn; ++k) {
@@ -110,9 +123,9 @@ __global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, cons
         if (oc >= g.oc) break;
         u64 v;
         if (split) {
-            v = reduce128(s00[o], 0, m);
-            v = add_mod(v, mul_shoup(reduce128(smid[o], 0, m), c21.x, c21.y, q), q);
-            v = add_mod(v, mul_shoup(reduce128(s11[o], 0, m), c42.x, c42.y, q), q);
+            const double t = f00[o] + ntt::fmodmul(fmid[o], static_cast<double>(c21.x), qd, qinv) +
+                             ntt::fmodmul(f11[o], static_cast<double>(c42.x), qd, qinv);
+            v = ntt::fcanon(t, qd, qinv);
         } else {
             v = reduce_2q(s00[o], q);
         }

@@ -44,10 +44,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_ntt_fwd_block(DevRing R, u64*
     const int limb = static_cast<int>(poly % limbs);
     const u64 q = R.mod[limb].q;
     u64* g = data + (poly << LOGN) + (static_cast<long long>(b) << LOGB);
-    const ulonglong2* tw = R.fwd + (static_cast<long long>(limb) << LOGN);
-    ntt::fwd_block<LOGB, LOGE, THREADS>(
-        smem, tw, q, b, C, [=](int i) { return g[i]; },
-        [=](int i, u64 v, int, int) { g[i] = reduce_4q(v, q); });
+    const long long toff = static_cast<long long>(limb) << LOGN;
+    if (ntt::fp_limb(q)) {
+        const ntt::FpArith ar{static_cast<double>(q), R.inv_q[limb]};
+        ntt::fwd_block<LOGB, LOGE, THREADS>(
+            reinterpret_cast<double*>(smem), ar, R.fwd_f + toff, b, C, [=](int i) { return ntt::to_fp(g[i]); },
+            [=](int i, double v, int, int) { g[i] = ntt::fcanon(v, ar.q, ar.qinv); });
+    } else {
+        const ntt::IntArith ar{q, q << 1};
+        ntt::fwd_block<LOGB, LOGE, THREADS>(
+            smem, ar, R.fwd + toff, b, C, [=](int i) { return g[i]; },
+            [=](int i, u64 v, int, int) { g[i] = reduce_4q(v, q); });
+    }
 }
 
 template <int LOGN, int LOGB, int LOGE, int THREADS, int MINB>
@@ -60,14 +68,26 @@ __global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_block(DevRing R, u64*
     const int limb = static_cast<int>(poly % limbs);
     const u64 q = R.mod[limb].q;
     u64* g = data + (poly << LOGN) + (static_cast<long long>(b) << LOGB);
-    const ulonglong2* tw = R.inv + (static_cast<long long>(limb) << LOGN);
-    const ulonglong2 ni = R.n_inv[limb];
-    ntt::inv_block<LOGB, LOGE, THREADS>(
-        smem, tw, q, b, C, [=](int i) { return g[i]; },
-        [=](int i, u64 v, int, int) {
-            if constexpr (C == 0) g[i] = reduce_2q(mul_shoup_lazy(v, ni.x, ni.y, q), q);
-            else g[i] = v;  // [0,2q); the column pass finishes
-        });
+    const long long toff = static_cast<long long>(limb) << LOGN;
+    if (ntt::fp_limb(q)) {
+        const ntt::FpArith ar{static_cast<double>(q), R.inv_q[limb]};
+        const double ni = R.n_inv_f[limb];
+        ntt::inv_block<LOGB, LOGE, THREADS>(
+            reinterpret_cast<double*>(smem), ar, R.inv_f + toff, b, C, [=](int i) { return ntt::to_fp(g[i]); },
+            [=](int i, double v, int, int) {
+                if constexpr (C == 0) v = ntt::fmodmul(v, ni, ar.q, ar.qinv);
+                g[i] = ntt::fcanon(v, ar.q, ar.qinv);  // [0,q) is inside the column pass's [0,2q) contract
+            });
+    } else {
+        const ntt::IntArith ar{q, q << 1};
+        const ulonglong2 ni = R.n_inv[limb];
+        ntt::inv_block<LOGB, LOGE, THREADS>(
+            smem, ar, R.inv + toff, b, C, [=](int i) { return g[i]; },
+            [=](int i, u64 v, int, int) {
+                if constexpr (C == 0) g[i] = reduce_2q(mul_shoup_lazy(v, ni.x, ni.y, q), q);
+                else g[i] = v;  // [0,2q); the column pass finishes
+            });
+    }
 }
 
 // Column passes for N > 2^LOGB: the C stages that couple the 2^C blocks.

@@ -12,8 +12,14 @@
 //
 // Butterflies follow the reference's networks exactly (NttTables::forward /
 // inverse, ring.hpp:83-137): forward CT with twiddle psi^bitrev(2^s + i),
-// inverse GS with psi^-bitrev(2^s + i); lazy ranges [0,4q) forward and
-// [0,2q) inverse, made canonical by the caller's epilogue.
+// inverse GS with psi^-bitrev(2^s + i). Two arithmetic policies:
+//   IntArith -- 64-bit Shoup on the integer pipes, lazy [0,4q) / [0,2q)
+//               (any q < 2^61; used for the 60-bit chain prime),
+//   FpArith  -- exact modular arithmetic on the FP64 pipe for q < 2^42:
+//               signed doubles, fmodmul() below, no per-stage corrections in
+//               the forward network, one centring per inverse round. B200
+//               runs it 2.7x faster than integer Shoup (tools/modmul_probe.cu).
+// Both produce the same residues; the caller's epilogue makes them canonical.
 #pragma once
 #include "kernels.hpp"
 
@@ -40,6 +46,70 @@ __device__ __forceinline__ void gs_butterfly(u64& a, u64& b, ulonglong2 w, u64 q
     b = mul_shoup_lazy(u + two_q - v, w.x, w.y, q);
 }
 
+// ---- exact FP64 modular arithmetic (q < 2^42) -------------------------------
+constexpr double kMagicRound = 6755399441055744.0;  // 1.5 * 2^52: x + M - M == rint(x), |x| < 2^51
+constexpr double kTwo52 = 4503599627370496.0;
+
+// x * w mod q in (-q, q) for |x| < 2^45, 0 <= w < q < 2^42, qinv = fl(1/q):
+// h + l == x*w exactly (FMA error-free product); t = rint(h * qinv) is within
+// 0.5 + 2^-6 of x*w/q (|h - xw| <= 2^35, relative error of qinv 2^-53), so
+// h - t*q and (h - t*q) + l are integers below 2^52 and both steps are exact.
+// Verified exhaustively on 2^26 signed inputs by tools/modmul_probe.cu.
+__device__ __forceinline__ double fmodmul(double x, double w, double q, double qinv) {
+    const double h = x * w;
+    const double l = fma(x, w, -h);
+    const double t = fma(h, qinv, kMagicRound) - kMagicRound;
+    return fma(-t, q, h) + l;
+}
+
+// |v| < 2^51 -> centred residue in (-q/2 - 1, q/2 + 1)
+__device__ __forceinline__ double fcentre(double v, double q, double qinv) {
+    const double t = fma(v, qinv, kMagicRound) - kMagicRound;
+    return fma(-t, q, v);
+}
+
+// |v| < 2^51 -> canonical residue as u64
+__device__ __forceinline__ u64 fcanon(double v, double q, double qinv) {
+    double r = fcentre(v, q, qinv);
+    if (r < 0) r += q;
+    if (r >= q) r -= q;
+    return static_cast<u64>(__double_as_longlong(r + kTwo52) - __double_as_longlong(kTwo52));
+}
+
+// u64 < 2^52 -> exact double
+__device__ __forceinline__ double to_fp(u64 v) {
+    return __longlong_as_double(static_cast<long long>(v | 0x4330000000000000ull)) - kTwo52;
+}
+
+struct IntArith {
+    using V = u64;
+    using TW = ulonglong2;
+    u64 q, two_q;
+    __device__ void ct(V& a, V& b, TW w) const { ct_butterfly(a, b, w, q, two_q); }
+    __device__ void gs(V& a, V& b, TW w) const { gs_butterfly(a, b, w, q, two_q); }
+    __device__ void round_end_inv(V&) const {}
+};
+
+struct FpArith {
+    using V = double;
+    using TW = double;  // the twiddle as an exact double
+    double q, qinv;
+    __device__ void ct(V& a, V& b, TW w) const {
+        const double v = fmodmul(b, w, q, qinv);
+        const double u = a;
+        a = u + v;
+        b = u - v;
+    }
+    __device__ void gs(V& a, V& b, TW w) const {
+        const double u = a, v = b;
+        a = u + v;
+        b = fmodmul(u - v, w, q, qinv);
+    }
+    // GS sums double per stage; centre once per round (<= 4 stages) so every
+    // value stays below 2^45 in magnitude.
+    __device__ void round_end_inv(V& x) const { x = fcentre(x, q, qinv); }
+};
+
 __host__ __device__ constexpr int ceil_div(int a, int b) { return (a + b - 1) / b; }
 // Balanced split of the remaining LOGB - s stages into rounds of <= LOGE.
 __host__ __device__ constexpr int round_size(int LOGB, int LOGE, int s) {
@@ -50,30 +120,32 @@ __host__ __device__ constexpr int last_round_start(int LOGB, int LOGE, int s = 0
     return s + round_size(LOGB, LOGE, s) >= LOGB ? s : last_round_start(LOGB, LOGE, s + round_size(LOGB, LOGE, s));
 }
 
+template <class V>
 struct SmemLoad {
-    const u64* s;
-    __device__ u64 operator()(int idx) const { return s[swz(idx)]; }
+    const V* s;
+    __device__ V operator()(int idx) const { return s[swz(idx)]; }
 };
+template <class V>
 struct SmemStore {
-    u64* s;
-    __device__ void operator()(int idx, u64 v, int, int) const { s[swz(idx)] = v; }
+    V* s;
+    __device__ void operator()(int idx, V v, int, int) const { s[swz(idx)] = v; }
 };
 
 // Forward round: block-local stages S0..S0+R-1; global stage = c + local;
 // `b` is the block index inside the N-point transform (twiddle offset).
-template <int LOGB, int R, int S0, int T, class Load, class Store>
-__device__ __forceinline__ void fwd_round(const ulonglong2* __restrict__ tw, u64 q, int b, int c, Load load,
+template <int LOGB, int R, int S0, int T, class A, class Load, class Store>
+__device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __restrict__ tw, int b, int c, Load load,
                                           Store store) {
+    using V = typename A::V;
     constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R;
     constexpr int PER = (UNITS + T - 1) / T;
-    const u64 two_q = q << 1;
 #pragma unroll
     for (int uu = 0; uu < PER; ++uu) {
         const int u = threadIdx.x + uu * T;
         if (UNITS % T != 0 && u >= UNITS) break;
         const int grp = u / STRIDE, col = u % STRIDE;
         const int base = grp * G + col;
-        u64 x[E];
+        V x[E];
 #pragma unroll
         for (int k = 0; k < E; ++k) x[k] = load(base + k * STRIDE);
 #pragma unroll
@@ -82,10 +154,9 @@ __device__ __forceinline__ void fwd_round(const ulonglong2* __restrict__ tw, u64
             const int tbase = (1 << (c + S0 + rho)) + (b << (S0 + rho)) + (grp << rho);
 #pragma unroll
             for (int blk = 0; blk < (1 << rho); ++blk) {
-                const ulonglong2 w = tw[tbase + blk];
+                const typename A::TW w = tw[tbase + blk];
 #pragma unroll
-                for (int kk = 0; kk < half; ++kk)
-                    ct_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
+                for (int kk = 0; kk < half; ++kk) ar.ct(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w);
             }
         }
 #pragma unroll
@@ -95,40 +166,42 @@ __device__ __forceinline__ void fwd_round(const ulonglong2* __restrict__ tw, u64
 
 // All forward rounds of a block: first round loads with `first`, last round
 // stores with `last`, the rest go through shared memory `s`.
-template <int LOGB, int LOGE, int T, int S0 = 0, class First, class Last>
-__device__ __forceinline__ void fwd_block(u64* s, const ulonglong2* tw, u64 q, int b, int c, First first, Last last) {
+template <int LOGB, int LOGE, int T, class A, int S0 = 0, class First, class Last>
+__device__ __forceinline__ void fwd_block(typename A::V* s, const A& ar, const typename A::TW* tw, int b, int c,
+                                          First first, Last last) {
+    using V = typename A::V;
     if constexpr (S0 < LOGB) {
         constexpr int R = round_size(LOGB, LOGE, S0);
         constexpr bool is_first = S0 == 0, is_last = S0 + R >= LOGB;
         if constexpr (is_first && is_last) {
-            fwd_round<LOGB, R, S0, T>(tw, q, b, c, first, last);
+            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, first, last);
         } else if constexpr (is_first) {
-            fwd_round<LOGB, R, S0, T>(tw, q, b, c, first, SmemStore{s});
+            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, first, SmemStore<V>{s});
             __syncthreads();
         } else if constexpr (is_last) {
-            fwd_round<LOGB, R, S0, T>(tw, q, b, c, SmemLoad{s}, last);
+            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, last);
         } else {
-            fwd_round<LOGB, R, S0, T>(tw, q, b, c, SmemLoad{s}, SmemStore{s});
+            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, SmemStore<V>{s});
             __syncthreads();
         }
-        fwd_block<LOGB, LOGE, T, S0 + R>(s, tw, q, b, c, first, last);
+        fwd_block<LOGB, LOGE, T, A, S0 + R>(s, ar, tw, b, c, first, last);
     }
 }
 
 // Inverse round: stages S0+R-1 down to S0.
-template <int LOGB, int R, int S0, int T, class Load, class Store>
-__device__ __forceinline__ void inv_round(const ulonglong2* __restrict__ tw, u64 q, int b, int c, Load load,
+template <int LOGB, int R, int S0, int T, class A, class Load, class Store>
+__device__ __forceinline__ void inv_round(const A& ar, const typename A::TW* __restrict__ tw, int b, int c, Load load,
                                           Store store) {
+    using V = typename A::V;
     constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R;
     constexpr int PER = (UNITS + T - 1) / T;
-    const u64 two_q = q << 1;
 #pragma unroll
     for (int uu = 0; uu < PER; ++uu) {
         const int u = threadIdx.x + uu * T;
         if (UNITS % T != 0 && u >= UNITS) break;
         const int grp = u / STRIDE, col = u % STRIDE;
         const int base = grp * G + col;
-        u64 x[E];
+        V x[E];
 #pragma unroll
         for (int k = 0; k < E; ++k) x[k] = load(base + k * STRIDE);
 #pragma unroll
@@ -137,39 +210,46 @@ __device__ __forceinline__ void inv_round(const ulonglong2* __restrict__ tw, u64
             const int tbase = (1 << (c + S0 + rho)) + (b << (S0 + rho)) + (grp << rho);
 #pragma unroll
             for (int blk = 0; blk < (1 << rho); ++blk) {
-                const ulonglong2 w = tw[tbase + blk];
+                const typename A::TW w = tw[tbase + blk];
 #pragma unroll
-                for (int kk = 0; kk < half; ++kk)
-                    gs_butterfly(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w, q, two_q);
+                for (int kk = 0; kk < half; ++kk) ar.gs(x[blk * 2 * half + kk], x[blk * 2 * half + kk + half], w);
             }
         }
 #pragma unroll
-        for (int k = 0; k < E; ++k) store(base + k * STRIDE, x[k], uu, k);
+        for (int k = 0; k < E; ++k) {
+            ar.round_end_inv(x[k]);
+            store(base + k * STRIDE, x[k], uu, k);
+        }
     }
 }
 
 // All inverse rounds: the forward decomposition traversed backwards; the
 // round with the highest S0 runs first and loads with `first`, the S0 = 0
 // round runs last and stores with `last`.
-template <int LOGB, int LOGE, int T, int S0 = 0, class First, class Last>
-__device__ __forceinline__ void inv_block(u64* s, const ulonglong2* tw, u64 q, int b, int c, First first, Last last) {
+template <int LOGB, int LOGE, int T, class A, int S0 = 0, class First, class Last>
+__device__ __forceinline__ void inv_block(typename A::V* s, const A& ar, const typename A::TW* tw, int b, int c,
+                                          First first, Last last) {
+    using V = typename A::V;
     if constexpr (S0 < LOGB) {
         constexpr int R = round_size(LOGB, LOGE, S0);
         constexpr bool runs_first = S0 + R >= LOGB, runs_last = S0 == 0;
-        inv_block<LOGB, LOGE, T, S0 + R>(s, tw, q, b, c, first, last);
+        inv_block<LOGB, LOGE, T, A, S0 + R>(s, ar, tw, b, c, first, last);
         if constexpr (runs_first && runs_last) {
-            inv_round<LOGB, R, S0, T>(tw, q, b, c, first, last);
+            inv_round<LOGB, R, S0, T>(ar, tw, b, c, first, last);
         } else if constexpr (runs_first) {
-            inv_round<LOGB, R, S0, T>(tw, q, b, c, first, SmemStore{s});
+            inv_round<LOGB, R, S0, T>(ar, tw, b, c, first, SmemStore<V>{s});
             __syncthreads();
         } else if constexpr (runs_last) {
-            inv_round<LOGB, R, S0, T>(tw, q, b, c, SmemLoad{s}, last);
+            inv_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, last);
         } else {
-            inv_round<LOGB, R, S0, T>(tw, q, b, c, SmemLoad{s}, SmemStore{s});
+            inv_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, SmemStore<V>{s});
             __syncthreads();
         }
     }
 }
+
+// Limbs whose prime fits the FP64 path.
+__device__ __forceinline__ bool fp_limb(u64 q) { return q < (1ull << 42); }
 
 }  // namespace ntt
 }  // namespace hecnn_b200

@@ -152,6 +152,9 @@ void RingTables::build(std::size_t degree, const std::vector<u64>& chain) {
     fwd.assign(limbs * n * 2, 0);
     inv.assign(limbs * n * 2, 0);
     n_inv.assign(limbs * 2, 0);
+    fwd_f.assign(limbs * n, 0.0);
+    inv_f.assign(limbs * n, 0.0);
+    n_inv_f.assign(limbs, 0.0);
     for (std::size_t l = 0; l < limbs; ++l) {
         const HostMod& m = mods[l];
         u64 psi = primitive_2n_root(m, n);
@@ -163,10 +166,13 @@ void RingTables::build(std::size_t degree, const std::vector<u64>& chain) {
             fwd[(l * n + i) * 2 + 1] = shoup_of(w, m.q);
             inv[(l * n + i) * 2] = wi;
             inv[(l * n + i) * 2 + 1] = shoup_of(wi, m.q);
+            fwd_f[l * n + i] = static_cast<double>(w);
+            inv_f[l * n + i] = static_cast<double>(wi);
         }
         u64 ni = m.inv(static_cast<u64>(n % m.q));
         n_inv[2 * l] = ni;
         n_inv[2 * l + 1] = shoup_of(ni, m.q);
+        n_inv_f[l] = static_cast<double>(ni);
     }
 
     inv_dropped.assign(limbs * limbs * 2, 0);

@@ -44,6 +44,7 @@ struct RingTables {
     // [limb][n] pairs (value, shoup): forward roots psi^bitrev(i), inverse roots
     std::vector<u64> fwd, inv;
     std::vector<u64> n_inv;          // [limb][2]
+    std::vector<double> fwd_f, inv_f, n_inv_f;  // FP64 path: [limb][n] / [limb] residues as doubles
     std::vector<u64> inv_dropped;    // [l][i][2]: p_l^{-1} mod q_i and Shoup
     std::vector<u64> p_mod;          // [l][i]: p_l mod q_i
     // CRT per level l (ring.hpp:165-169, 185-200)

@@ -8,7 +8,7 @@
 #include <stdexcept>
 #include <string>
 
-#include "kernels.hpp"
+#include "ntt_core.cuh"
 
 namespace hecnn_b200 {
 
@@ -236,6 +236,39 @@ __global__ void __launch_bounds__(256) k_modmul_probe(DevRing R, int iters, u64*
 
 }  // namespace
 
+namespace {
+// FP64-pipe probe: 8 chains of the exact FP64 modmul (ntt_core.cuh fmodmul).
+__global__ void __launch_bounds__(256) k_fp64_probe(DevRing R, int limb, int iters, u64* __restrict__ sink) {
+    const double q = static_cast<double>(R.mod[limb].q), qinv = R.inv_q[limb];
+    const double w = R.fwd_f[static_cast<long long>(limb) * R.n + ((threadIdx.x * 13 + 1) & (R.n - 1))];
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = static_cast<double>((blockIdx.x * 256u + threadIdx.x) * 8u + k + 1u);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = ntt::fmodmul(x[k], w, q, qinv);
+    }
+    double acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += x[k];
+    if (acc == 12345.0) sink[0] = 1;  // keeps the chains live
+}
+}  // namespace
+
+double fp64_modmul_probe(const DevRing& R, int iters, u64* sink, const Launch& L) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int limb = -1;
+    // any limb with q < 2^42 (mod table is device-resident; chains use limb 1 when present)
+    limb = R.limbs > 1 ? 1 : 0;
+    const int blocks = sms * 8;
+    L.begin("k_fp64_probe");
+    k_fp64_probe<<<blocks, 256, 0, L.stream>>>(R, limb, iters, sink);
+    L.count();
+    check_launch("fp64_modmul_probe");
+    return static_cast<double>(blocks) * 256.0 * 8.0 * iters;
+}
+
 double modmul_probe(const DevRing& R, int iters, u64* sink, const Launch& L) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -245,6 +278,24 @@ double modmul_probe(const DevRing& R, int iters, u64* sink, const Launch& L) {
     L.count();
     check_launch("modmul_probe");
     return static_cast<double>(blocks) * 256.0 * 8.0 * iters;
+}
+
+namespace {
+__global__ void k_fp_table(DevRing R, const u64* __restrict__ in, double* __restrict__ out, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    out[row * R.n + j] = static_cast<double>(in[row * R.n + j]);  // exact: residues < 2^53
+}
+}  // namespace
+
+void fp_table(const DevRing& R, const u64* in, double* out, int limbs, std::size_t count, const Launch& L) {
+    const std::size_t rows = count * limbs;
+    if (!rows) return;
+    L.begin("k_fp_table", 0, 16.0 * rows * R.n);
+    k_fp_table<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, in, out, limbs);
+    L.count();
+    check_launch("fp_table");
 }
 
 void shoup_table(const DevRing& R, const u64* in, u64* out, int limbs, std::size_t count, const Launch& L) {

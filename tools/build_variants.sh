@@ -3,12 +3,11 @@
 set -e
 cd "$(dirname "$0")/.."
 declare -A V
-V[v0]=""
-V[v1]="-DHECNN_NTT_MINB=2 -DHECNN_KS_MINB=1"
-V[v2]="-DHECNN_NTT_LOGE=3 -DHECNN_NTT_MAXT=1024"
-V[v3]="-DHECNN_KS_LOGE=3 -DHECNN_KS_MAXT=1024"
-V[v4]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT=256 -DHECNN_KS_MINB=2"
-V[v5]="-DHECNN_KS_LOGB=12 -DHECNN_KS_LOGE=3 -DHECNN_KS_MAXT=512 -DHECNN_KS_MINB=2 -DHECNN_NTT_LOGE=3 -DHECNN_NTT_MAXT=512 -DHECNN_NTT_MINB=2"
+V[k1]=""
+V[k2]="-DHECNN_KS_MAXT=512"
+V[k3]="-DHECNN_KS_MAXT=512 -DHECNN_KS_LOGE=4"
+V[k4]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT=512 -DHECNN_KS_MINB=2"
+V[n2]="-DHECNN_NTT_LOGE=4 -DHECNN_NTT_MINB=1 -DHECNN_KS_MAXT=512"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
