@@ -58,6 +58,68 @@ def c3_spec(hb):
     return spec
 
 
+def layer_work(hb, spec):
+    """Per-layer work counts used to extrapolate layer times between input
+    sizes of the same stack: conv = sum over output pixels of valid taps x
+    filters (layers.hpp:174-211 skips clipped taps), activation / pool =
+    output cells, zero-pad = fresh border encryptions, dense = inputs x units."""
+    out, cur = [], spec.input
+    shapes = spec.shapes()
+    for l, shp in zip(spec.layers, shapes):
+        if l.kind == hb.CONV2D:
+            def taps(n_in, n_out, k, s):
+                if l.valid:
+                    return [k] * n_out
+                need = (n_out - 1) * s + k
+                pad = (need - n_in) // 2 if need > n_in else 0
+                return [sum(1 for kk in range(k) if 0 <= o * s + kk - pad < n_in) for o in range(n_out)]
+            ty = taps(cur.h, shp.h, l.kernel_h, l.stride)
+            tx = taps(cur.w, shp.w, l.kernel_w, l.stride)
+            out.append(sum(ty) * sum(tx) * cur.c * l.filters)
+        elif l.kind in (hb.ACTIVATION, hb.AVG_POOL2D):
+            out.append(shp.positions())
+        elif l.kind == hb.ZERO_PAD2D:
+            out.append(shp.positions() - cur.positions())
+        elif l.kind == hb.DENSE:
+            out.append(cur.positions() * l.units)
+        else:
+            out.append(0)
+        cur = shp
+    return out
+
+
+def c5_extrapolated(hb, device, crop=8, stream=None):
+    """C5 (AlexNet-like COWC, alexnet32_preset layers, large-n16384-d24, 8192
+    images per set): the full stack runs on the GPU on a crop x crop x 3 input
+    (every layer type, every level, the real key-switch/NTT shapes); each
+    layer's CUDA-event time is scaled by the exact work ratio to the 64x64
+    (BASELINE's COWC patches) and 32x32 (the preset / paper) inputs. Small
+    crop layers underfill the GPU, so the estimate is conservative."""
+    p = hb.preset_params("large-n16384-d24")
+    eng = hb.CkksEngine(p, device=device).keygen(1)
+    if stream is not None:
+        eng.set_stream(stream)
+    spec = hb.glorot_weights(hb.alexnet32_preset(image=crop), 1)
+    x = eng.encrypt_tensor(np.random.default_rng(3).uniform(0, 1, size=(p.n // 2, spec.input.positions())),
+                           seed=11, shape=spec.input)
+    model = eng.model(spec)
+    secs = []
+    hb.forward_encrypted(model, x, eng, seed=13, layer_seconds=secs)   # warm-up (weight caches)
+    secs = []
+    y = hb.forward_encrypted(model, x, eng, seed=13, layer_seconds=secs)
+    work_crop = layer_work(hb, spec)
+    res = {"preset": "large-n16384-d24", "images_per_set": p.n // 2, "crop": f"{crop}x{crop}x3",
+           "crop_forward_s": float(sum(secs)), "out_level": y.level,
+           "layer_s_crop": [round(s, 4) for s in secs]}
+    for full in (64, 32):
+        work_full = layer_work(hb, hb.alexnet32_preset(image=full))
+        t = sum(s * (wf / wc if wc else 1.0) for s, wf, wc in zip(secs, work_full, work_crop))
+        res[f"{full}x{full}"] = {"seconds_per_set": t, "images_per_s": (p.n // 2) / t}
+    del y, x, model
+    eng.close()
+    return res
+
+
 # ---------------------------------------------------------------- helpers
 
 class ClockSampler:
@@ -357,7 +419,10 @@ def run_ours(args):
                        "gmodmul_s": (v["ops"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0,
                        "gb_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0}
                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+        del x, y, xe, ye
+        eng.trim()  # hand C4's cached arena back before the larger C2/C5 runs
         mb = microbench(hb, local) if not args.no_micro else None
+        c5 = c5_extrapolated(hb, local, stream=stream.cuda_stream) if not args.no_c5 else None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle import ref
@@ -381,7 +446,7 @@ def run_ours(args):
                         "d2h_bytes_per_step": out_words_n * 8},
                 "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "output": {"cells": out_cells, "level": out_level},
-                "microbench_c2": mb, "kernels": kernels}
+                "microbench_c2": mb, "c5_alexnet_cowc_extrapolated": c5, "kernels": kernels}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -396,6 +461,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (AlexNet-COWC) crop extrapolation")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

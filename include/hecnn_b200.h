@@ -72,6 +72,8 @@ int hecnn_context_create(size_t n, const uint64_t* primes, size_t nprimes, doubl
 int hecnn_context_destroy(hecnn_context* ctx);
 int hecnn_context_set_stream(hecnn_context* ctx, void* cuda_stream);
 int hecnn_context_synchronize(hecnn_context* ctx);
+/* Return the device arena's wholly free segments to the driver. */
+int hecnn_context_trim(hecnn_context* ctx, size_t* freed_bytes);
 int hecnn_context_info(const hecnn_context* ctx, size_t* n, size_t* top_level, double* scale);
 /* CkksEngine::relin_digits (ckks.hpp:509-512) */
 int hecnn_relin_digits(const hecnn_context* ctx, size_t level, size_t* digits);

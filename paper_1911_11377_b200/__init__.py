@@ -46,7 +46,7 @@ EXPORTED_SYMBOLS = (
     "hecnn_model_create", "hecnn_model_destroy", "hecnn_model_depth_cost", "hecnn_forward_encrypted",
     "hecnn_profile_enable", "hecnn_profile_reset", "hecnn_profile_read", "hecnn_modmul_peak",
     "hecnn_tensor_copy_to_device", "hecnn_host_encode_real", "hecnn_host_decode_real",
-    "hecnn_host_encryption_randomness", "hecnn_fp64_modmul_peak",
+    "hecnn_host_encryption_randomness", "hecnn_fp64_modmul_peak", "hecnn_context_trim",
 )
 
 _lib = None
@@ -70,6 +70,7 @@ _SIGNATURES = {
     "hecnn_context_destroy": [_V],
     "hecnn_context_set_stream": [_V, _V],
     "hecnn_context_synchronize": [_V],
+    "hecnn_context_trim": [_V, _PSZ],
     "hecnn_context_info": [_V, _PSZ, _PSZ, _PD],
     "hecnn_relin_digits": [_V, _SZ, _PSZ],
     "hecnn_launch_count": [_V, _PU64],
@@ -640,6 +641,12 @@ class CkksEngine:
 
     def synchronize(self):
         _check(lib().hecnn_context_synchronize(self.ctx))
+
+    def trim(self) -> int:
+        """Return wholly free device-arena segments to the driver."""
+        f = ctypes.c_size_t()
+        _check(lib().hecnn_context_trim(self.ctx, ctypes.byref(f)))
+        return f.value
 
     def set_stream(self, stream_ptr: int):
         _check(lib().hecnn_context_set_stream(self.ctx, ctypes.c_void_p(stream_ptr)))

@@ -145,6 +145,15 @@ int hecnn_context_set_stream(hecnn_context* ctx, void* stream) {
     });
 }
 
+int hecnn_context_trim(hecnn_context* ctx, size_t* freed) {
+    return guard([&] {
+        Context& c = C(ctx);
+        c.sync();
+        const std::size_t f = c.arena.trim();
+        if (freed) *freed = f;
+    });
+}
+
 int hecnn_context_synchronize(hecnn_context* ctx) {
     return guard([&] { C(ctx).sync(); });
 }

@@ -104,7 +104,8 @@ void to_int8(const std::vector<long long>& v, signed char* out) {
 // ---------------------------------------------------------------- memory
 
 Arena::~Arena() {
-    for (auto& s : segs_) cudaFree(s.first);
+    for (auto& s : segs_)
+        if (s.first) cudaFree(s.first);
 }
 
 void* Arena::alloc(std::size_t bytes) {
@@ -116,6 +117,11 @@ void* Arena::alloc(std::size_t bytes) {
         const std::size_t seg = std::max(bytes, std::size_t(1) << 30);
         void* p = nullptr;
         cudaError_t e = cudaMalloc(&p, seg);
+        if (e != cudaSuccess) {  // give back wholly free segments and retry once
+            cudaGetLastError();
+            trim();
+            e = cudaMalloc(&p, seg);
+        }
         if (e != cudaSuccess && seg > bytes) {  // fall back to an exact-size segment
             cudaGetLastError();
             e = cudaMalloc(&p, bytes);
@@ -141,6 +147,23 @@ void* Arena::alloc(std::size_t bytes) {
     if (blk.size > bytes) free_.emplace(p + bytes, Block{blk.size - bytes, blk.seg});
     used_.emplace(p, Block{bytes, blk.seg});
     return p;
+}
+
+std::size_t Arena::trim() {
+    std::size_t freed = 0;
+    for (auto it = free_.begin(); it != free_.end();) {
+        const int seg = it->second.seg;
+        if (seg >= 0 && segs_[seg].first == it->first && segs_[seg].second == it->second.size) {
+            cudaFree(segs_[seg].first);
+            freed += segs_[seg].second;
+            reserved_ -= segs_[seg].second;
+            segs_[seg] = {nullptr, 0};  // ids stay stable; slot is dead
+            it = free_.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    return freed;
 }
 
 void Arena::release(void* ptr) {
@@ -181,8 +204,15 @@ DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
     return *this;
 }
 
+DevBuf DevBuf::alias(void* ptr, std::size_t bytes) {
+    DevBuf b;
+    b.ptr_ = ptr;
+    b.bytes_ = bytes;  // ctx_ stays null: the view never releases the memory
+    return b;
+}
+
 void DevBuf::reset() {
-    if (ptr_) ctx_->arena.release(ptr_);
+    if (ptr_ && ctx_) ctx_->arena.release(ptr_);
     ptr_ = nullptr;
     bytes_ = 0;
 }
@@ -603,7 +633,7 @@ void Activation::validate() const {
 }
 
 // eval_encrypted (activation.hpp:228-265): power-basis plan over whole tensors.
-TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x) {
+static TensorPtr eval_activation_cells(Context& C, const Activation& act, const Tensor& x) {
     Trace tr("eval_activation");
     act.validate();
     const std::size_t d = act.degree(), depth = act.encrypted_depth();
@@ -642,6 +672,40 @@ TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x) {
     acc->shape = x.shape;
     acc->batch = x.batch;
     return acc;
+}
+
+// Non-owning tensor over cells [c0, c0 + m) of x.
+static TensorPtr cell_slice(const Tensor& x, std::size_t c0, std::size_t m) {
+    auto t = std::make_unique<Tensor>();
+    t->ctx = x.ctx;
+    t->cells = m;
+    t->level = x.level;
+    t->scale = x.scale;
+    t->shape = Shape::flattened(m);
+    t->batch = x.batch;
+    t->buf = DevBuf::alias(x.cell(c0), m * x.cell_words() * 8);
+    return t;
+}
+
+// The power plan is identical for every cell, so large tensors are evaluated
+// in cell chunks written straight into the output: peak memory is input +
+// output + one chunk's intermediates instead of every full-size power/term.
+TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x) {
+    const std::size_t per_cell = x.cell_words() * 8;
+    const std::size_t chunk = std::max<std::size_t>(1, (std::size_t(6) << 30) / (per_cell * 6));
+    if (x.cells <= chunk) return eval_activation_cells(C, act, x);
+    TensorPtr out;
+    for (std::size_t c0 = 0; c0 < x.cells; c0 += chunk) {
+        const std::size_t m = std::min(chunk, x.cells - c0);
+        TensorPtr part = eval_activation_cells(C, act, *cell_slice(x, c0, m));
+        if (!out) out = make_tensor(C, x.cells, part->level, part->scale);
+        cuda_check(cudaMemcpyAsync(out->cell(c0), part->data(), m * part->cell_words() * 8, cudaMemcpyDeviceToDevice,
+                                   C.stream),
+                   "copy activation chunk");
+    }
+    out->shape = x.shape;
+    out->batch = x.batch;
+    return out;
 }
 
 // ---------------------------------------------------------------- encryption

@@ -31,6 +31,8 @@ public:
     ~Arena();
     void* alloc(std::size_t bytes);
     void release(void* p);
+    // Return segments that are entirely free to the driver; returns bytes freed.
+    std::size_t trim();
     std::size_t reserved() const { return reserved_; }
 
 private:
@@ -54,6 +56,8 @@ public:
     DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
     DevBuf& operator=(DevBuf&& o) noexcept;
     void reset();
+    // Non-owning view of memory owned elsewhere (e.g. a slice of a tensor).
+    static DevBuf alias(void* ptr, std::size_t bytes);
     template <class T>
     T* as() const { return static_cast<T*>(ptr_); }
     void* get() const { return ptr_; }
