@@ -943,7 +943,7 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
             for (std::size_t o = 0; o < oc; ++o) {
                 std::vector<u64> res = C.enc->scalar_residues(l.w[r * oc + o], wscale, level);
                 for (std::size_t i = 0; i < limbs; ++i) {
-                    const std::size_t at = (r * lc.oc_pad + o) * limbs + i;
+                    const std::size_t at = (i * rows + r) * lc.oc_pad + o;  // limb-major: OCT channels contiguous
                     w[at] = make_ulonglong2(res[i], shoup_of(res[i], C.ring.primes[i]));
                     ws[at] = make_uint2(static_cast<unsigned>(res[i] & 0x1FFFFFu), static_cast<unsigned>(res[i] >> 21));
                 }
@@ -1018,7 +1018,7 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
         const std::size_t m = std::min(pix_chunk, lc.pixels - p0);
         GatherMac g{lc.src.as<int>() + p0 * lc.K, lc.wrow.as<int>() + p0 * lc.K, lc.weights.as<ulonglong2>(),
                     bit->second.as<u64>(), lc.wsplit.as<uint2>(), lc.recomb.as<ulonglong2>(),
-                    static_cast<int>(m), lc.K, lc.oc, lc.oc_pad, lc.oc};
+                    static_cast<int>(m), lc.K, lc.oc, lc.oc_pad, lc.oc, static_cast<int>(rows)};
         gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), L);
         rescale(C.dev, pre.as<u64>(), out->cell(p0 * oc), static_cast<int>(level), 2 * m * oc, L);
     }

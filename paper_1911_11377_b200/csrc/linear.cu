@@ -12,6 +12,7 @@
 // word-identical to the reference's sequential accumulation.
 
 #include <algorithm>
+#include <stdexcept>
 
 #include "ntt_core.cuh"
 
@@ -23,14 +24,19 @@ constexpr int TPB = 256;
 constexpr int OCT = 8;
 
 constexpr int KCHUNK = 128;
+constexpr int TAPB = 4;  // input words in flight per thread
 
 // One thread = one (component, limb, coefficient) column of OCT output
 // channels of one pixel. The pixel's taps (source cell, weight row) and the
 // limb's weights for the OCT channels are staged in shared memory per chunk
-// of KCHUNK taps, so the inner loop is: one coalesced HBM/L2 load of the
-// input word, then OCT multiply-accumulates against broadcast shared words.
-__global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, const u64* __restrict__ x,
-                                                    u64* __restrict__ y, int level) {
+// of KCHUNK taps, so the inner loop is: TAPB independent coalesced loads of
+// input words, then OCT multiply-accumulates each against broadcast shared
+// words. The grid is column-block major (blockIdx.x = (column block, pixel,
+// channel tile), channel tile fastest), so while one column block is in
+// flight every input cell's slice of it (cells x TPB words) stays in L2 and
+// is reused by all pixels whose window covers it and by all channel tiles.
+__global__ void __launch_bounds__(TPB, 2) k_gather_mac(DevRing R, GatherMac g, const u64* __restrict__ x,
+                                                    u64* __restrict__ y, int level, int oc_tiles) {
     __shared__ int s_src[KCHUNK];
     __shared__ double2 s_w[KCHUNK][OCT];
     __shared__ ulonglong2 s_ws[KCHUNK][OCT];
@@ -38,18 +44,24 @@ __global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, cons
     const long long poly_words = static_cast<long long>(limbs) * R.n;
     const long long cell_words = 2 * poly_words;
     const int tpb = blockDim.x;  // <= n, so a CTA's columns share one limb
-    const long long col0 = static_cast<long long>(blockIdx.x) * tpb;
+    const long long per_block = static_cast<long long>(g.pixels) * oc_tiles;
+    const long long bid = blockIdx.x;
+    const long long cb = bid / per_block;
+    const int pz = static_cast<int>(bid - cb * per_block);
+    const int pixel = pz / oc_tiles;
+    const int oc0 = (pz - pixel * oc_tiles) * OCT;
+    const long long col0 = cb * tpb;
     const long long col = col0 + threadIdx.x;
     const bool live = col < cell_words;
     const int comp = static_cast<int>(col / poly_words);
     const int i = static_cast<int>(((live ? col : col0) / R.n) % limbs);  // uniform when n >= TPB
     const int j = static_cast<int>(col % R.n);
-    const int pixel = blockIdx.y;
-    const int oc0 = blockIdx.z * OCT;
     const ModConst m = R.mod[i];
     const u64 q = m.q, two_q = q << 1;
     const int* src = g.src + static_cast<long long>(pixel) * g.K;
     const int* wrow = g.wrow + static_cast<long long>(pixel) * g.K;
+    const long long wbase = static_cast<long long>(i) * g.rows;
+    const u64* xc = x + (live ? col : 0);
     // q < 2^42: x, w split at bit 21 into exact doubles; every partial product
     // is < 2^42 and a chunk of KCHUNK taps sums below 2^51, so the FP64 pipe
     // accumulates exactly; accumulators are centred mod q after each chunk.
@@ -66,33 +78,43 @@ __global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, cons
 
     for (int k0 = 0; k0 < g.K; k0 += KCHUNK) {
         const int kn = min(KCHUNK, g.K - k0);
+        const int kpad = (kn + TAPB - 1) / TAPB * TAPB;  // taps kn..kpad: src -1, weight 0
         __syncthreads();
-        for (int t = threadIdx.x; t < kn * OCT; t += tpb) {
+        for (int t = threadIdx.x; t < kpad * OCT; t += tpb) {
             const int k = t / OCT, o = t % OCT;
-            const long long at = (static_cast<long long>(wrow[k0 + k]) * g.oc_pad + oc0 + o) * limbs + i;
+            const bool ok = k < kn;
+            const long long at = ok ? (wbase + wrow[k0 + k]) * g.oc_pad + oc0 + o : 0;
             if (split) {
-                const uint2 w = g.wsplit[at];
+                const uint2 w = ok ? g.wsplit[at] : make_uint2(0, 0);
                 s_w[k][o] = make_double2(static_cast<double>(w.x), static_cast<double>(w.y));
             } else {
-                s_ws[k][o] = g.weights[at];
+                s_ws[k][o] = ok ? g.weights[at] : make_ulonglong2(0, 0);
             }
-            if (o == 0) s_src[k] = src[k0 + k];
+            if (o == 0) s_src[k] = ok ? src[k0 + k] : -1;
         }
         __syncthreads();
         if (!live) continue;
+        // invalid taps (s < 0, zero padding) load nothing and contribute 0
         if (split) {
-            for (int k = 0; k < kn; ++k) {
-                const int s = s_src[k];
-                if (s < 0) continue;
-                const u64 v = x[s * cell_words + col];
-                const double v0 = ntt::to_fp(v & 0x1FFFFFull), v1 = ntt::to_fp(v >> 21);
+            for (int kb = 0; kb < kpad; kb += TAPB) {
+                u64 v[TAPB];
 #pragma unroll
-                for (int o = 0; o < OCT; ++o) {
-                    const double2 c = s_w[k][o];
-                    f00[o] = fma(v0, c.x, f00[o]);
-                    fmid[o] = fma(v0, c.y, fmid[o]);
-                    fmid[o] = fma(v1, c.x, fmid[o]);
-                    f11[o] = fma(v1, c.y, f11[o]);
+                for (int u = 0; u < TAPB; ++u) {
+                    const int s = s_src[kb + u];
+                    v[u] = s >= 0 ? __ldg(xc + s * cell_words) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < TAPB; ++u) {
+                    const int k = kb + u;
+                    const double v0 = ntt::to_fp(v[u] & 0x1FFFFFull), v1 = ntt::to_fp(v[u] >> 21);
+#pragma unroll
+                    for (int o = 0; o < OCT; ++o) {
+                        const double2 c = s_w[k][o];
+                        f00[o] = fma(v0, c.x, f00[o]);
+                        fmid[o] = fma(v0, c.y, fmid[o]);
+                        fmid[o] = fma(v1, c.x, fmid[o]);
+                        f11[o] = fma(v1, c.y, f11[o]);
+                    }
                 }
             }
 #pragma unroll
@@ -102,15 +124,22 @@ __global__ void __launch_bounds__(TPB) k_gather_mac(DevRing R, GatherMac g, cons
                 f11[o] = ntt::fcentre(f11[o], qd, qinv);
             }
         } else {
-            for (int k = 0; k < kn; ++k) {
-                const int s = s_src[k];
-                if (s < 0) continue;
-                const u64 v = x[s * cell_words + col];
+            for (int kb = 0; kb < kpad; kb += TAPB) {
+                u64 v[TAPB];
 #pragma unroll
-                for (int o = 0; o < OCT; ++o) {
-                    const ulonglong2 c = s_ws[k][o];
-                    const u64 t = s00[o] + mul_shoup_lazy(v, c.x, c.y, q);
-                    s00[o] = t >= two_q ? t - two_q : t;
+                for (int u = 0; u < TAPB; ++u) {
+                    const int s = s_src[kb + u];
+                    v[u] = s >= 0 ? __ldg(xc + s * cell_words) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < TAPB; ++u) {
+                    const int k = kb + u;
+#pragma unroll
+                    for (int o = 0; o < OCT; ++o) {
+                        const ulonglong2 c = s_ws[k][o];
+                        const u64 t = s00[o] + mul_shoup_lazy(v[u], c.x, c.y, q);
+                        s00[o] = t >= two_q ? t - two_q : t;
+                    }
                 }
             }
         }
@@ -167,12 +196,14 @@ __global__ void k_gather_cells(const u64* __restrict__ x, const int* __restrict_
 void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, const Launch& L) {
     const long long cell_words = 2LL * (level + 1) * R.n;
     const int tpb = std::min(TPB, R.n);
-    dim3 grid(static_cast<unsigned>((cell_words + tpb - 1) / tpb), static_cast<unsigned>(g.pixels),
-              static_cast<unsigned>((g.oc + OCT - 1) / OCT));
     if (!g.pixels || !g.oc) return;
+    const int oc_tiles = (g.oc + OCT - 1) / OCT;
+    const long long blocks = (cell_words + tpb - 1) / tpb * g.pixels * oc_tiles;
+    if (blocks > 0x7fffffffLL) throw std::runtime_error("gather_mac: grid too large");
+    const unsigned grid = static_cast<unsigned>(blocks);
     L.begin("k_gather_mac", double(g.pixels) * g.K * g.oc * cell_words,
             8.0 * cell_words * (double(g.pixels) * g.oc + g.pixels * g.K));
-    k_gather_mac<<<grid, tpb, 0, L.stream>>>(R, g, x, y, level);
+    k_gather_mac<<<grid, tpb, 0, L.stream>>>(R, g, x, y, level, oc_tiles);
     L.count();
     check_launch("gather_mac");
 }

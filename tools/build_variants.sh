@@ -3,11 +3,11 @@
 set -e
 cd "$(dirname "$0")/.."
 declare -A V
-V[k1]=""
-V[k2]="-DHECNN_KS_MAXT=512"
-V[k3]="-DHECNN_KS_MAXT=512 -DHECNN_KS_LOGE=4"
-V[k4]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT=512 -DHECNN_KS_MINB=2"
-V[n2]="-DHECNN_NTT_LOGE=4 -DHECNN_NTT_MINB=1 -DHECNN_KS_MAXT=512"
+V[va]=""
+V[vb]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT=512 -DHECNN_KS_MINB=2"
+V[vc]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT=256 -DHECNN_KS_MINB=2"
+V[vd]="-DHECNN_KS_LOGE=4"
+V[ve]="-DHECNN_KS_LOGB=12 -DHECNN_KS_LOGE=4 -DHECNN_KS_MAXT=256 -DHECNN_KS_MINB=2"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null

@@ -74,6 +74,19 @@ def main():
         xin.set_shape(spec.input, 4096)
         wall, prof, _ = timed(eng, lambda: hb.forward_encrypted(m, xin, eng))
         res["conv1_c4"] = {"ms": wall * 1e3, "kernels": prof}
+    if "conv5" in which:
+        # AlexNet conv2 shape (5x5, 96 -> 256) at its C5 level, on an 8x8 spatial tile
+        pl = hb.preset_params("large-n16384-d24")
+        el = hb.CkksEngine(pl).keygen(1)
+        spec = hb.ModelSpec(hb.Shape.spatial(8, 8, 96))
+        spec.layers = [hb.LayerSpec.conv2d(256, 5, 5)]
+        hb.glorot_weights(spec, 4)
+        m5 = el.model(spec)
+        lv = 20
+        xin = el.tensor_from_words(uniform_words(pl, 8 * 8 * 96, lv), lv, pl.scale)
+        xin.set_shape(spec.input, 8192)
+        wall, prof, _ = timed(el, lambda: hb.forward_encrypted(m5, xin, el), reps=1)
+        res["conv_alexnet2_l20"] = {"ms": wall * 1e3, "kernels": prof}
     if "large" in which:
         pl = hb.preset_params("large-n16384-d24")
         el = hb.CkksEngine(pl).keygen(1)
