@@ -936,7 +936,7 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
     if (it == M.linear.end()) {
         Model::LinearCache lc;
         lc.oc = static_cast<int>(oc);
-        lc.oc_pad = static_cast<int>((oc + 7) / 8 * 8);
+        lc.oc_pad = static_cast<int>((oc + 15) / 16 * 16);
         std::vector<ulonglong2> w(rows * lc.oc_pad * limbs, make_ulonglong2(0, 0));
         std::vector<uint2> ws(rows * lc.oc_pad * limbs, make_uint2(0, 0));
         for (std::size_t r = 0; r < rows; ++r)
@@ -957,7 +957,7 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
         }
         lc.wsplit = C.upload_vec(ws);
         lc.recomb = C.upload_vec(rc);
-        std::vector<int> src, wrow;
+        std::vector<int> src;  // tap k of every pixel uses weight row k (ky, kx, ic order)
         if (conv) {
             const std::size_t need_h = (out_shape.h - 1) * l.stride + l.kh, need_w = (out_shape.w - 1) * l.stride + l.kw;
             long long pad_top = 0, pad_left = 0;
@@ -977,19 +977,14 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
                                 bool ok = y >= 0 && xx >= 0 && y < static_cast<long long>(in.h) &&
                                           xx < static_cast<long long>(in.w);
                                 src.push_back(ok ? static_cast<int>((y * in.w + xx) * in.c + ic) : -1);
-                                wrow.push_back(static_cast<int>((ky * l.kw + kx) * in.c + ic));
                             }
         } else {
             lc.pixels = 1;
             lc.K = static_cast<int>(rows);
-            for (std::size_t k = 0; k < rows; ++k) {
-                src.push_back(static_cast<int>(k));
-                wrow.push_back(static_cast<int>(k));
-            }
+            for (std::size_t k = 0; k < rows; ++k) src.push_back(static_cast<int>(k));
         }
         lc.weights = C.upload_vec(w);
         lc.src = C.upload_vec(src);
-        lc.wrow = C.upload_vec(wrow);
         it = M.linear.emplace(key, std::move(lc)).first;
     }
     Model::LinearCache& lc = it->second;
@@ -1016,9 +1011,9 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
     Launch L = C.L();
     for (std::size_t p0 = 0; p0 < static_cast<std::size_t>(lc.pixels); p0 += pix_chunk) {
         const std::size_t m = std::min(pix_chunk, lc.pixels - p0);
-        GatherMac g{lc.src.as<int>() + p0 * lc.K, lc.wrow.as<int>() + p0 * lc.K, lc.weights.as<ulonglong2>(),
+        GatherMac g{lc.src.as<int>() + p0 * lc.K, lc.weights.as<ulonglong2>(),
                     bit->second.as<u64>(), lc.wsplit.as<uint2>(), lc.recomb.as<ulonglong2>(),
-                    static_cast<int>(m), lc.K, lc.oc, lc.oc_pad, lc.oc, static_cast<int>(rows)};
+                    static_cast<int>(m), lc.K, lc.oc, lc.oc_pad, lc.oc};
         gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), L);
         rescale(C.dev, pre.as<u64>(), out->cell(p0 * oc), static_cast<int>(level), 2 * m * oc, L);
     }

@@ -185,7 +185,7 @@ struct Model {
     std::vector<Shape> shapes;  // per-layer output shapes (shape_infer)
     // integer-weight caches, keyed by (layer, level) and (layer, level, scale)
     struct LinearCache {
-        DevBuf src, wrow, weights, wsplit, recomb;
+        DevBuf src, weights, wsplit, recomb;
         int pixels = 0, K = 0, oc = 0, oc_pad = 0;
     };
     std::map<std::pair<std::size_t, std::uint32_t>, LinearCache> linear;

@@ -126,14 +126,12 @@ double fp64_modmul_probe(const DevRing& R, int iters, u64* sink, const Launch& L
 // ---- linear layers (linear.cu)
 // Gather-MAC for conv/dense: see linear.cu for the table formats.
 struct GatherMac {
-    const int* src;            // [pixels][K] input cell index per tap (-1: invalid tap)
-    const int* wrow;           // [pixels][K] weight row per tap
-    const ulonglong2* weights; // [limbs][rows][oc_pad] (residue, shoup) at level, oc_pad % 8 == 0
+    const int* src;            // [pixels][K] input cell index per tap (-1: invalid tap); tap k uses weight row k
+    const ulonglong2* weights; // [limbs][K][oc_pad] (residue, shoup) at level, oc_pad % 16 == 0
     const u64* bias;           // [oc][level+1] residues (added to c0 coeff 0), or null
-    const uint2* wsplit;       // [limbs][rows][oc_pad] residue split (w mod 2^21, w >> 21) for q < 2^41
+    const uint2* wsplit;       // [limbs][K][oc_pad] residue split (w mod 2^21, w >> 21) for q < 2^42
     const ulonglong2* recomb;  // [limbs][2]: (2^21 mod q, shoup), (2^42 mod q, shoup)
     int pixels, K, oc, oc_pad, out_stride_pixel;  // output cell = pixel * out_stride_pixel + oc
-    int rows;                                     // weight rows (taps of one output channel)
 };
 void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, const Launch& L);
 // 2x2-style average pool: out cell p sums srcs[p][0..taps) then multiplies by w (shoup), level kept

@@ -21,146 +21,189 @@ namespace hecnn_b200 {
 namespace {
 
 constexpr int TPB = 256;
-constexpr int OCT = 8;
+#ifndef HECNN_GM_TPB
+#define HECNN_GM_TPB 256
+#endif
+#ifndef HECNN_GM_OCT
+#define HECNN_GM_OCT 8
+#endif
+#ifndef HECNN_GM_TAPB
+#define HECNN_GM_TAPB 4
+#endif
+#ifndef HECNN_GM_MINB
+#define HECNN_GM_MINB 2
+#endif
+constexpr int GM_TPB = HECNN_GM_TPB;
+constexpr int OCT = HECNN_GM_OCT;  // output channels per thread; weights are padded to 16
+static_assert(16 % OCT == 0, "OCT must divide the weight padding");
 
-constexpr int KCHUNK = 128;
-constexpr int TAPB = 4;  // input words in flight per thread
+constexpr int KCHUNK = 256;
+constexpr int TAPB = HECNN_GM_TAPB;  // input words in flight per thread
+#ifndef HECNN_GM_PG
+#define HECNN_GM_PG 8
+#endif
+constexpr int PG = HECNN_GM_PG;  // pixels per CTA when all K taps fit one staged chunk
 
 // One thread = one (component, limb, coefficient) column of OCT output
-// channels of one pixel. The pixel's taps (source cell, weight row) and the
-// limb's weights for the OCT channels are staged in shared memory per chunk
-// of KCHUNK taps, so the inner loop is: TAPB independent coalesced loads of
-// input words, then OCT multiply-accumulates each against broadcast shared
-// words. The grid is column-block major (blockIdx.x = (column block, pixel,
-// channel tile), channel tile fastest), so while one column block is in
-// flight every input cell's slice of it (cells x TPB words) stays in L2 and
+// channels, for a group of pixels. Tap k of every pixel uses weight row k, so
+// when K <= KCHUNK the CTA stages the limb's weights for its OCT channels and
+// the taps of all its pixels once, then runs the pixel loop out of shared
+// memory; larger K streams chunks of KCHUNK taps for one pixel. The inner loop
+// issues TAPB independent coalesced loads of input words, then OCT
+// multiply-accumulates each against broadcast shared words. The grid is
+// column-block major (column block slowest, channel tile fastest), so while
+// one column block is in flight every input cell's slice of it stays in L2 and
 // is reused by all pixels whose window covers it and by all channel tiles.
-__global__ void __launch_bounds__(TPB, 2) k_gather_mac(DevRing R, GatherMac g, const u64* __restrict__ x,
-                                                    u64* __restrict__ y, int level, int oc_tiles) {
-    __shared__ int s_src[KCHUNK];
-    __shared__ double2 s_w[KCHUNK][OCT];
-    __shared__ ulonglong2 s_ws[KCHUNK][OCT];
-    const int limbs = level + 1;
-    const long long poly_words = static_cast<long long>(limbs) * R.n;
-    const long long cell_words = 2 * poly_words;
-    const int tpb = blockDim.x;  // <= n, so a CTA's columns share one limb
-    const long long per_block = static_cast<long long>(g.pixels) * oc_tiles;
+struct GmTile {
+    long long cell_words, col;
+    const u64* xc;
+    int p_begin, p_end, oc0, i, limbs, comp, j, tpb;
+    bool resident, live;
+    u64 q;
+    double qd, qinv;
+};
+
+template <bool SPLIT>
+__device__ __forceinline__ void gm_body(const GatherMac& g, const GmTile& T, const ModConst& m, u64* __restrict__ y,
+                                        unsigned char* s_raw, int (*s_src)[KCHUNK]) {
+    auto s_w = reinterpret_cast<double2(*)[OCT]>(s_raw);
+    auto s_ws = reinterpret_cast<ulonglong2(*)[OCT]>(s_raw);
+    const u64 q = T.q, two_q = q << 1;
+    const double qd = T.qd, qinv = T.qinv;
+    const long long wbase = static_cast<long long>(T.i) * g.K;
+    for (int p = T.p_begin; p < T.p_end; ++p) {
+        // SPLIT: f00 = sum x0 w0, fm0 = sum x0 w1, fm1 = sum x1 w0, f11 = sum x1 w1
+        double f00[OCT], fm0[OCT], fm1[OCT], f11[OCT];
+        u64 s00[OCT];
+#pragma unroll
+        for (int o = 0; o < OCT; ++o) {
+            if (SPLIT) f00[o] = fm0[o] = fm1[o] = f11[o] = 0.0;
+            else s00[o] = 0;
+        }
+        for (int k0 = 0; k0 < g.K; k0 += KCHUNK) {
+            const int kn = min(KCHUNK, g.K - k0);
+            const int kpad = (kn + TAPB - 1) / TAPB * TAPB;  // taps kn..kpad: src -1, weight 0
+            if (!T.resident || p == T.p_begin) {
+                __syncthreads();
+                for (int t = threadIdx.x; t < kpad * OCT; t += T.tpb) {
+                    const int k = t / OCT, o = t % OCT;
+                    const bool ok = k < kn;
+                    const long long at = ok ? (wbase + k0 + k) * g.oc_pad + T.oc0 + o : 0;
+                    if (SPLIT) {
+                        const uint2 w = ok ? g.wsplit[at] : make_uint2(0, 0);
+                        s_w[k][o] = make_double2(static_cast<double>(w.x), static_cast<double>(w.y));
+                    } else {
+                        s_ws[k][o] = ok ? g.weights[at] : make_ulonglong2(0, 0);
+                    }
+                }
+                const int np = T.p_end - p;
+                for (int t = threadIdx.x; t < np * kpad; t += T.tpb) {
+                    const int pp = t / kpad, k = t - pp * kpad;
+                    s_src[pp][k] = k < kn ? g.src[static_cast<long long>(p + pp) * g.K + k0 + k] : -1;
+                }
+                __syncthreads();
+            }
+            if (!T.live) continue;
+            const int* ss = s_src[T.resident ? p - T.p_begin : 0];
+            // invalid taps (s < 0, zero padding) load nothing and contribute 0
+            for (int kb = 0; kb < kpad; kb += TAPB) {
+                u64 v[TAPB];
+#pragma unroll
+                for (int u = 0; u < TAPB; ++u) {
+                    const int s = ss[kb + u];
+                    v[u] = s >= 0 ? __ldg(T.xc + s * T.cell_words) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < TAPB; ++u) {
+                    const int k = kb + u;
+                    if (SPLIT) {
+                        const double v0 = ntt::to_fp(v[u] & 0x1FFFFFull), v1 = ntt::to_fp(v[u] >> 21);
+#pragma unroll
+                        for (int o = 0; o < OCT; ++o) {
+                            const double2 c = s_w[k][o];
+                            f00[o] = fma(v0, c.x, f00[o]);
+                            fm0[o] = fma(v0, c.y, fm0[o]);
+                            fm1[o] = fma(v1, c.x, fm1[o]);
+                            f11[o] = fma(v1, c.y, f11[o]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int o = 0; o < OCT; ++o) {
+                            const ulonglong2 c = s_ws[k][o];
+                            const u64 t = s00[o] + mul_shoup_lazy(v[u], c.x, c.y, q);
+                            s00[o] = t >= two_q ? t - two_q : t;
+                        }
+                    }
+                }
+            }
+            if (SPLIT) {
+#pragma unroll
+                for (int o = 0; o < OCT; ++o) {
+                    f00[o] = ntt::fcentre(f00[o], qd, qinv);
+                    fm0[o] = ntt::fcentre(fm0[o], qd, qinv);
+                    fm1[o] = ntt::fcentre(fm1[o], qd, qinv);
+                    f11[o] = ntt::fcentre(f11[o], qd, qinv);
+                }
+            }
+        }
+        if (!T.live) continue;
+        const ulonglong2 c21 = g.recomb[2 * T.i], c42 = g.recomb[2 * T.i + 1];
+#pragma unroll
+        for (int o = 0; o < OCT; ++o) {
+            const int oc = T.oc0 + o;
+            if (oc >= g.oc) break;
+            u64 v;
+            if (SPLIT) {
+                const double t = f00[o] + ntt::fmodmul(fm0[o] + fm1[o], static_cast<double>(c21.x), qd, qinv) +
+                                 ntt::fmodmul(f11[o], static_cast<double>(c42.x), qd, qinv);
+                v = ntt::fcanon(t, qd, qinv);
+            } else {
+                v = reduce_2q(s00[o], q);
+            }
+            if (g.bias && T.comp == 0 && T.j == 0) v = add_mod(v, g.bias[static_cast<long long>(oc) * T.limbs + T.i], q);
+            y[(static_cast<long long>(p) * g.out_stride_pixel + oc) * T.cell_words + T.col] = v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(GM_TPB, HECNN_GM_MINB) k_gather_mac(DevRing R, GatherMac g, const u64* __restrict__ x,
+                                                                     u64* __restrict__ y, int level, int oc_tiles,
+                                                                     int groups, int pg) {
+    // staged weights: split doubles (FP64 limbs) or (residue, shoup) (q0); one per CTA
+    __shared__ __align__(16) unsigned char s_raw[KCHUNK * OCT * 16];
+    __shared__ int s_src[PG][KCHUNK];
+    GmTile T;
+    T.limbs = level + 1;
+    const long long poly_words = static_cast<long long>(T.limbs) * R.n;
+    T.cell_words = 2 * poly_words;
+    T.tpb = blockDim.x;  // <= n, so a CTA's columns share one limb
+    const long long per_block = static_cast<long long>(groups) * oc_tiles;
     const long long bid = blockIdx.x;
     const long long cb = bid / per_block;
-    const int pz = static_cast<int>(bid - cb * per_block);
-    const int pixel = pz / oc_tiles;
-    const int oc0 = (pz - pixel * oc_tiles) * OCT;
-    const long long col0 = cb * tpb;
-    const long long col = col0 + threadIdx.x;
-    const bool live = col < cell_words;
-    const int comp = static_cast<int>(col / poly_words);
-    const int i = static_cast<int>(((live ? col : col0) / R.n) % limbs);  // uniform when n >= TPB
-    const int j = static_cast<int>(col % R.n);
-    const ModConst m = R.mod[i];
-    const u64 q = m.q, two_q = q << 1;
-    const int* src = g.src + static_cast<long long>(pixel) * g.K;
-    const int* wrow = g.wrow + static_cast<long long>(pixel) * g.K;
-    const long long wbase = static_cast<long long>(i) * g.rows;
-    const u64* xc = x + (live ? col : 0);
+    const int rest = static_cast<int>(bid - cb * per_block);
+    const int grp = rest / oc_tiles;
+    T.oc0 = (rest - grp * oc_tiles) * OCT;
+    T.p_begin = grp * pg;
+    T.p_end = min(T.p_begin + pg, g.pixels);
+    T.resident = g.K <= KCHUNK;  // host sets pg = 1 otherwise
+    const long long col0 = cb * T.tpb;
+    T.col = col0 + threadIdx.x;
+    T.live = T.col < T.cell_words;
+    T.comp = static_cast<int>(T.col / poly_words);
+    T.i = static_cast<int>(((T.live ? T.col : col0) / R.n) % T.limbs);  // uniform when n >= TPB
+    T.j = static_cast<int>(T.col % R.n);
+    const ModConst m = R.mod[T.i];
+    T.q = m.q;
+    T.qd = static_cast<double>(T.q);
+    T.qinv = R.inv_q[T.i];
+    T.xc = x + (T.live ? T.col : 0);
     // q < 2^42: x, w split at bit 21 into exact doubles; every partial product
-    // is < 2^42 and a chunk of KCHUNK taps sums below 2^51, so the FP64 pipe
-    // accumulates exactly; accumulators are centred mod q after each chunk.
-    const bool split = ntt::fp_limb(q);
-    const double qd = static_cast<double>(q), qinv = R.inv_q[i];
-
-    u64 s00[OCT];
-    double f00[OCT], fmid[OCT], f11[OCT];
-#pragma unroll
-    for (int o = 0; o < OCT; ++o) {
-        s00[o] = 0;
-        f00[o] = fmid[o] = f11[o] = 0.0;
-    }
-
-    for (int k0 = 0; k0 < g.K; k0 += KCHUNK) {
-        const int kn = min(KCHUNK, g.K - k0);
-        const int kpad = (kn + TAPB - 1) / TAPB * TAPB;  // taps kn..kpad: src -1, weight 0
-        __syncthreads();
-        for (int t = threadIdx.x; t < kpad * OCT; t += tpb) {
-            const int k = t / OCT, o = t % OCT;
-            const bool ok = k < kn;
-            const long long at = ok ? (wbase + wrow[k0 + k]) * g.oc_pad + oc0 + o : 0;
-            if (split) {
-                const uint2 w = ok ? g.wsplit[at] : make_uint2(0, 0);
-                s_w[k][o] = make_double2(static_cast<double>(w.x), static_cast<double>(w.y));
-            } else {
-                s_ws[k][o] = ok ? g.weights[at] : make_ulonglong2(0, 0);
-            }
-            if (o == 0) s_src[k] = ok ? src[k0 + k] : -1;
-        }
-        __syncthreads();
-        if (!live) continue;
-        // invalid taps (s < 0, zero padding) load nothing and contribute 0
-        if (split) {
-            for (int kb = 0; kb < kpad; kb += TAPB) {
-                u64 v[TAPB];
-#pragma unroll
-                for (int u = 0; u < TAPB; ++u) {
-                    const int s = s_src[kb + u];
-                    v[u] = s >= 0 ? __ldg(xc + s * cell_words) : 0;
-                }
-#pragma unroll
-                for (int u = 0; u < TAPB; ++u) {
-                    const int k = kb + u;
-                    const double v0 = ntt::to_fp(v[u] & 0x1FFFFFull), v1 = ntt::to_fp(v[u] >> 21);
-#pragma unroll
-                    for (int o = 0; o < OCT; ++o) {
-                        const double2 c = s_w[k][o];
-                        f00[o] = fma(v0, c.x, f00[o]);
-                        fmid[o] = fma(v0, c.y, fmid[o]);
-                        fmid[o] = fma(v1, c.x, fmid[o]);
-                        f11[o] = fma(v1, c.y, f11[o]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int o = 0; o < OCT; ++o) {
-                f00[o] = ntt::fcentre(f00[o], qd, qinv);
-                fmid[o] = ntt::fcentre(fmid[o], qd, qinv);
-                f11[o] = ntt::fcentre(f11[o], qd, qinv);
-            }
-        } else {
-            for (int kb = 0; kb < kpad; kb += TAPB) {
-                u64 v[TAPB];
-#pragma unroll
-                for (int u = 0; u < TAPB; ++u) {
-                    const int s = s_src[kb + u];
-                    v[u] = s >= 0 ? __ldg(xc + s * cell_words) : 0;
-                }
-#pragma unroll
-                for (int u = 0; u < TAPB; ++u) {
-                    const int k = kb + u;
-#pragma unroll
-                    for (int o = 0; o < OCT; ++o) {
-                        const ulonglong2 c = s_ws[k][o];
-                        const u64 t = s00[o] + mul_shoup_lazy(v[u], c.x, c.y, q);
-                        s00[o] = t >= two_q ? t - two_q : t;
-                    }
-                }
-            }
-        }
-    }
-    if (!live) return;
-    const ulonglong2 c21 = g.recomb[2 * i], c42 = g.recomb[2 * i + 1];
-#pragma unroll
-    for (int o = 0; o < OCT; ++o) {
-        const int oc = oc0 + o;
-        if (oc >= g.oc) break;
-        u64 v;
-        if (split) {
-            const double t = f00[o] + ntt::fmodmul(fmid[o], static_cast<double>(c21.x), qd, qinv) +
-                             ntt::fmodmul(f11[o], static_cast<double>(c42.x), qd, qinv);
-            v = ntt::fcanon(t, qd, qinv);
-        } else {
-            v = reduce_2q(s00[o], q);
-        }
-        if (g.bias && comp == 0 && j == 0) v = add_mod(v, g.bias[static_cast<long long>(oc) * limbs + i], q);
-        y[(static_cast<long long>(pixel) * g.out_stride_pixel + oc) * cell_words + col] = v;
-    }
+    // is < 2^42 and each accumulator sums at most KCHUNK of them (< 2^50), so
+    // the FP64 pipe accumulates exactly; accumulators are centred mod q after
+    // each chunk. The middle term uses two accumulators so no two dependent
+    // FMAs are issued back to back. The 60-bit q0 limb uses lazy Shoup.
+    if (ntt::fp_limb(T.q)) gm_body<true>(g, T, m, y, s_raw, s_src);
+    else gm_body<false>(g, T, m, y, s_raw, s_src);
 }
 
 // avg_pool2d_encrypted (layers.hpp:213-239): sum of the window, times
@@ -195,15 +238,17 @@ __global__ void k_gather_cells(const u64* __restrict__ x, const int* __restrict_
 
 void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, const Launch& L) {
     const long long cell_words = 2LL * (level + 1) * R.n;
-    const int tpb = std::min(TPB, R.n);
+    const int tpb = std::min(GM_TPB, R.n);
     if (!g.pixels || !g.oc) return;
     const int oc_tiles = (g.oc + OCT - 1) / OCT;
-    const long long blocks = (cell_words + tpb - 1) / tpb * g.pixels * oc_tiles;
+    const int pg = g.K <= KCHUNK ? PG : 1;
+    const int groups = (g.pixels + pg - 1) / pg;
+    const long long blocks = (cell_words + tpb - 1) / tpb * groups * oc_tiles;
     if (blocks > 0x7fffffffLL) throw std::runtime_error("gather_mac: grid too large");
     const unsigned grid = static_cast<unsigned>(blocks);
     L.begin("k_gather_mac", double(g.pixels) * g.K * g.oc * cell_words,
             8.0 * cell_words * (double(g.pixels) * g.oc + g.pixels * g.K));
-    k_gather_mac<<<grid, tpb, 0, L.stream>>>(R, g, x, y, level, oc_tiles);
+    k_gather_mac<<<grid, tpb, 0, L.stream>>>(R, g, x, y, level, oc_tiles, groups, pg);
     L.count();
     check_launch("gather_mac");
 }
