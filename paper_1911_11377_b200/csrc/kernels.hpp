@@ -31,6 +31,7 @@ struct DevRing {
     const double* fwd_f = nullptr;           // [limbs][n]
     const double* inv_f = nullptr;           // [limbs][n]
     const double* n_inv_f = nullptr;         // [limbs]
+    unsigned long long int_limbs = 0;        // bit i: q_i >= 2^42 (integer-pipe path), for i < 64
 };
 
 // Optional per-kernel timing: CUDA events recorded on the launching stream

@@ -148,47 +148,94 @@ __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const u
 }
 
 // Per digit t: lift -> forward NTT (shared rounds) -> in the last butterfly
-// round each thread multiplies its outputs by (b_t, a_t) and accumulates into
-// registers; accumulator positions are the thread's last-round positions,
-// identical for every t. A = IntArith (u64 Shoup, evk + evk_sh) or FpArith
-// (exact FP64, evk_f = e as doubles). The block's twiddles are staged once in
-// shared memory as a block-local table TL[2^s + m] = tw[2^(s+C) + b 2^s + m]
-// and reused by all D digit transforms (round code indexes it with b = c = 0).
+// round each thread multiplies its outputs by (b_t, a_t) and accumulates;
+// accumulator positions are the thread's last-round positions, identical for
+// every t. A = IntArith (u64 Shoup, evk + evk_sh) or FpArith (exact FP64,
+// evk_f = e as doubles). The block's twiddles are staged once in shared memory
+// as a block-local table TL[2^s + m] = tw[2^(s+C) + b 2^s + m] and reused by
+// all D digit transforms (round code indexes it with b = c = 0).
+// FP64 path (all limbs but the 60-bit q0): the c1 accumulator lives in the
+// shared-memory space the integer path needs for its 16-byte twiddles
+// (thread-private swizzled slots, no barriers), and the registers this frees
+// hold the next digit's first-round inputs, loaded while the current digit
+// is transformed.
 template <int LOGN, int LOGB, int LOGE, int T, class A, class KeyAt>
 __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typename A::TW* tw, const u32* digits,
                                         KeyAt key, u64* acc01, int level, int D, long long ct, int i, int b, u64 q) {
     using V = typename A::V;
     using TW = typename A::TW;
+    constexpr bool FP = std::is_same<V, double>::value;
     extern __shared__ u64 smem[];
     constexpr int B = 1 << LOGB, C = LOGN - LOGB;
     constexpr int SL = ntt::last_round_start(LOGB, LOGE);
     constexpr int RL = LOGB - SL, EL = 1 << RL, UL = B >> RL, PL = (UL + T - 1) / T;
     constexpr int GL = B >> SL, STRL = GL >> RL;
+    // first round (S0 = 0): unit u owns positions u + k * STR0, k < E0
+    constexpr int R0 = ntt::round_size(LOGB, LOGE, 0), E0 = 1 << R0, U0 = B >> R0, P0 = (U0 + T - 1) / T;
+    constexpr int STR0 = U0;
+    constexpr bool PREFETCH = FP && C == 0;
     const long long n = 1LL << LOGN;
     const long long blk_off = static_cast<long long>(b) << LOGB;
     const ulonglong2* itw = R.fwd + (static_cast<long long>(i) << LOGN);  // integer twiddles for the column stages
 
     TW* stw = reinterpret_cast<TW*>(smem + B);
+    double* sacc = reinterpret_cast<double*>(smem + 2 * B);  // FP path: c1 accumulators
     for (int j = threadIdx.x + 1; j < B; j += T) {
         const int s = 31 - __clz(j), m = j - (1 << s);
         stw[j] = tw[(1 << (s + C)) + (b << s) + m];
     }
+    if constexpr (FP) {
+        for (int j = threadIdx.x; j < B; j += T) sacc[j] = 0.0;
+    }
     __syncthreads();  // table complete before the first round reads it
 
-    V a0[PL * EL], a1[PL * EL];
+    V a0[PL * EL], a1[FP ? 1 : PL * EL];
 #pragma unroll
-    for (int k = 0; k < PL * EL; ++k) a0[k] = a1[k] = V(0);
+    for (int k = 0; k < PL * EL; ++k) a0[k] = V(0);
+#pragma unroll
+    for (int k = 0; k < (FP ? 1 : PL * EL); ++k) a1[k] = V(0);
+
+    u32 pf[PREFETCH ? P0 * E0 : 1];
+    auto prefetch = [&](int t) {
+        if constexpr (PREFETCH) {
+            const u32* dig = digits + (ct * D + t) * n;
+#pragma unroll
+            for (int uu = 0; uu < P0; ++uu) {
+                const int u = threadIdx.x + uu * T;
+#pragma unroll
+                for (int k = 0; k < E0; ++k)
+                    pf[uu * E0 + k] = (U0 % T != 0 && u >= U0) ? 0u : __ldg(dig + u + k * STR0);
+            }
+        }
+    };
+    prefetch(0);
 
     for (int t = 0; t < D; ++t) {
         const u32* dig = digits + (ct * D + t) * n;
-        ntt::fwd_block<LOGB, LOGE, T>(
-            reinterpret_cast<V*>(smem), ar, stw, 0, 0,
-            [=](int r) {
+        u32 cur[PREFETCH ? P0 * E0 : 1];
+        if constexpr (PREFETCH) {
+#pragma unroll
+            for (int k = 0; k < P0 * E0; ++k) cur[k] = pf[k];
+            if (t + 1 < D) prefetch(t + 1);  // lands while digit t is transformed
+        }
+        auto first = [&](int r, int uu, int k) -> V {
+            if constexpr (PREFETCH) {
+                (void)r;
+                return ntt::to_fp(lift_digit(cur[uu * E0 + k], q));
+            } else {
                 const u64 v = column_value<LOGN, C>(dig, itw, q, r, b);
-                if constexpr (std::is_same<V, double>::value) return ntt::to_fp(v);
+                if constexpr (FP) return ntt::to_fp(v);
                 else return v;
-            },
-            [&](int idx, V v, int uu, int k) { key(t, blk_off + idx, v, a0[uu * EL + k], a1[uu * EL + k]); });
+            }
+        };
+        ntt::fwd_block<LOGB, LOGE, T>(reinterpret_cast<V*>(smem), ar, stw, 0, 0, first,
+                                      [&](int idx, V v, int uu, int k) {
+                                          if constexpr (FP) {
+                                              key(t, blk_off + idx, v, a0[uu * EL + k], sacc[ntt::swz(idx)]);
+                                          } else {
+                                              key(t, blk_off + idx, v, a0[uu * EL + k], a1[uu * EL + k]);
+                                          }
+                                      });
         __syncthreads();  // the next digit's first round overwrites shared memory
     }
     const int limbs = level + 1;
@@ -203,9 +250,9 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         for (int k = 0; k < EL; ++k) {
             const int idx = base + k * STRL;
             u64 r0, r1;
-            if constexpr (std::is_same<V, double>::value) {
+            if constexpr (FP) {
                 r0 = ntt::fcanon(a0[uu * EL + k], ar.q, ar.qinv);
-                r1 = ntt::fcanon(a1[uu * EL + k], ar.q, ar.qinv);
+                r1 = ntt::fcanon(sacc[ntt::swz(idx)], ar.q, ar.qinv);
             } else {
                 r0 = reduce_2q(a0[uu * EL + k], q);
                 r1 = reduce_2q(a1[uu * EL + k], q);
@@ -216,23 +263,25 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     }
 }
 
-// blockIdx.x = (ct * limbs + i) * nblocks + b
-template <int LOGN, int LOGB, int LOGE, int T, int MINB>
+// blockIdx.x = (ct * nsel + i - limb0) * nblocks + b over limbs [limb0, limb0 + nsel). FPK: this instantiation serves
+// the FP64 limbs (q < 2^42) and skips the others, or the reverse, so each
+// path gets its own register allocation; the host launches both.
+template <int LOGN, int LOGB, int LOGE, int T, int MINB, bool FPK>
 __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
                                                  const u64* __restrict__ evk_sh, const double* __restrict__ evk_f,
-                                                 u64* __restrict__ acc01, int level, int D) {
+                                                 u64* __restrict__ acc01, int level, int D, int limb0, int nsel) {
     constexpr int C = LOGN - LOGB;
-    const int limbs = level + 1;
     const long long cta = blockIdx.x;
     const int b = static_cast<int>(cta & ((1 << C) - 1));
-    const long long row = cta >> C;  // ct * limbs + i
-    const long long ct = row / limbs;
-    const int i = static_cast<int>(row % limbs);
+    const long long row = cta >> C;  // ct * nsel + (i - limb0)
+    const long long ct = row / nsel;
+    const int i = limb0 + static_cast<int>(row % nsel);
     const u64 q = R.mod[i].q;
     const long long n = 1LL << LOGN;
     const long long key_stride = static_cast<long long>(R.limbs) * n;  // one evk polynomial
     const long long ioff = static_cast<long long>(i) * n;
-    if (ntt::fp_limb(q)) {
+    if (ntt::fp_limb(q) != FPK) return;
+    if constexpr (FPK) {
         const ntt::FpArith ar{static_cast<double>(q), R.inv_q[i]};
         auto key = [=](int t, long long pos, double v, double& s0, double& s1) {
             const double kb = evk_f[(2LL * t) * key_stride + ioff + pos];
@@ -282,19 +331,37 @@ template <int LOGN>
 void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
                    u64* acc01, int level, int D, std::size_t count, const Launch& L) {
     using P = KsPlan<LOGN>;
-    auto kern = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB>;
-    const int smem = P::B * (8 + 16);  // data + staged twiddles (u64 Shoup pairs on the integer path)
-    static bool init = (smem > 48 * 1024 ? (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true) : true);
+    auto kfp = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true>;
+    auto kint = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false>;
+    // data + staged twiddles (u64 Shoup pairs on the integer path; double
+    // twiddles + c1 accumulators on the FP64 path)
+    const int smem = P::B * (8 + 16);
+    static bool init = (smem > 48 * 1024 ? (cudaFuncSetAttribute(kfp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                                           cudaFuncSetAttribute(kint, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true)
+                                        : true);
     (void)init;
-    const std::size_t ctas = count * static_cast<std::size_t>(level + 1) << (LOGN - P::LOGB);
-    {
-        // per (ct, limb, digit): one N-point NTT + 2N MACs; bytes: evk once + digits + acc r/w
-        const double n = double(1 << LOGN), cl = double(count) * (level + 1);
-        L.begin("k_keyswitch", cl * D * (n / 2 * LOGN + 2 * n),
-                2.0 * D * (level + 1) * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
-    }
-    kern<<<static_cast<unsigned>(ctas), P::T, smem, L.stream>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D);
-    L.count();
+    const int limbs = level + 1;
+    const unsigned long long lmask = limbs >= 64 ? ~0ull : (1ull << limbs) - 1;
+    const unsigned long long int_mask = R.int_limbs & lmask;
+    // exact limb ranges when only q0 is an integer limb (the presets); otherwise
+    // both kernels cover every limb and skip the other kind's rows
+    int fp0 = 0, nfp = limbs, int0 = 0, nint = limbs;
+    if (int_mask == 0) nint = 0;
+    else if (int_mask == lmask) nfp = 0;
+    else if (int_mask == 1) { fp0 = 1; nfp = limbs - 1; nint = 1; }
+    const double n = double(1 << LOGN);
+    // per (ct, limb, digit): one N-point NTT + 2N MACs; bytes: evk once + digits + acc r/w
+    const int n_int = __builtin_popcountll(int_mask);
+    auto run = [&](auto kern, const char* name, int l0, int nsel, int work_limbs) {
+        if (!nsel) return;
+        const std::size_t ctas = count * static_cast<std::size_t>(nsel) << (LOGN - P::LOGB);
+        const double sel = work_limbs, cl = double(count) * sel;
+        L.begin(name, cl * D * (n / 2 * LOGN + 2 * n), 2.0 * D * sel * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
+        kern<<<static_cast<unsigned>(ctas), P::T, smem, L.stream>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel);
+        L.count();
+    };
+    run(kfp, "k_keyswitch", fp0, nfp, limbs - n_int);
+    run(kint, "k_keyswitch_q0", int0, nint, n_int);
 }
 
 }  // namespace

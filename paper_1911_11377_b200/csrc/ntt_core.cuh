@@ -21,6 +21,8 @@
 //               runs it 2.7x faster than integer Shoup (tools/modmul_probe.cu).
 // Both produce the same residues; the caller's epilogue makes them canonical.
 #pragma once
+#include <type_traits>
+
 #include "kernels.hpp"
 
 namespace hecnn_b200 {
@@ -147,7 +149,11 @@ __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __r
         const int base = grp * G + col;
         V x[E];
 #pragma unroll
-        for (int k = 0; k < E; ++k) x[k] = load(base + k * STRIDE);
+        for (int k = 0; k < E; ++k) {
+            // loads that can use the (unit, element) slot, e.g. prefetched registers
+            if constexpr (std::is_invocable_v<Load, int, int, int>) x[k] = load(base + k * STRIDE, uu, k);
+            else x[k] = load(base + k * STRIDE);
+        }
 #pragma unroll
         for (int rho = 0; rho < R; ++rho) {
             const int half = E >> (rho + 1);
