@@ -14,11 +14,11 @@
 
 namespace hecnn_b200 {
 
-namespace {
-
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
+
+namespace {
 
 // HECNN_TRACE=1 prints host wall time of the engine's phases (diagnostics).
 struct Trace {
@@ -284,6 +284,9 @@ Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, doubl
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
     own_stream = true;
+    cuda_check(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming), "cudaEventCreate");
 
     std::vector<ModConst> mods;
     for (const auto& m : ring.mods) mods.push_back(ModConst{m.q, 2 * m.q, m.ratio_lo, m.ratio_hi});
@@ -338,7 +341,11 @@ Context::~Context() {
     evk_f.reset();
     tables.clear();
     cudaStreamSynchronize(stream);
+    cudaStreamSynchronize(aux);
     if (own_stream) cudaStreamDestroy(stream);
+    cudaStreamDestroy(aux);
+    cudaEventDestroy(fork_ev);
+    cudaEventDestroy(join_ev);
 }
 
 void Context::upload(void* dst, const void* src, std::size_t bytes) {

@@ -88,9 +88,12 @@ struct Context {
     Profiler prof;
     Arena arena;
 
+    cudaStream_t aux = nullptr;  // side stream (key switch: integer-limb kernel beside the FP64 one)
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+
     Context(std::size_t n, const std::vector<u64>& primes, double scale, double sigma, bool degenerate, int device);
     ~Context();
-    Launch L() { return Launch{stream, &launches, &prof}; }
+    Launch L() { return Launch{stream, &launches, &prof, aux, fork_ev, join_ev}; }
     std::size_t n() const { return ring.n; }
     std::size_t top() const { return ring.limbs - 1; }
     void upload(void* dst, const void* src, std::size_t bytes);

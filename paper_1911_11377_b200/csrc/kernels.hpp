@@ -66,6 +66,10 @@ struct Launch {
     cudaStream_t stream = nullptr;
     unsigned long long* counter = nullptr;
     Profiler* prof = nullptr;
+    // side stream for independent work inside one operation (fork/join with
+    // the events below); null: everything runs on `stream`
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     void begin(const char* name, double ops = 0, double bytes = 0) const {
         if (prof && prof->enabled) prof->begin(name, stream, ops, bytes);
     }
@@ -76,6 +80,7 @@ struct Launch {
 };
 
 void check_launch(const char* what);
+void cuda_check(cudaError_t e, const char* what);  // throws std::runtime_error on failure
 
 // ---- NTT (ntt.cu). polys: [count][level+1][n], limb index = poly % (level+1)
 void ntt_forward(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L);

@@ -349,19 +349,31 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
     if (int_mask == 0) nint = 0;
     else if (int_mask == lmask) nfp = 0;
     else if (int_mask == 1) { fp0 = 1; nfp = limbs - 1; nint = 1; }
-    const double n = double(1 << LOGN);
+    const double n = double(1 << LOGN), cl = double(count) * limbs;
     // per (ct, limb, digit): one N-point NTT + 2N MACs; bytes: evk once + digits + acc r/w
-    const int n_int = __builtin_popcountll(int_mask);
-    auto run = [&](auto kern, const char* name, int l0, int nsel, int work_limbs) {
-        if (!nsel) return;
+    L.begin("k_keyswitch", cl * D * (n / 2 * LOGN + 2 * n),
+            2.0 * D * limbs * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
+    auto launch = [&](auto kern, cudaStream_t st, int l0, int nsel) {
         const std::size_t ctas = count * static_cast<std::size_t>(nsel) << (LOGN - P::LOGB);
-        const double sel = work_limbs, cl = double(count) * sel;
-        L.begin(name, cl * D * (n / 2 * LOGN + 2 * n), 2.0 * D * sel * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
-        kern<<<static_cast<unsigned>(ctas), P::T, smem, L.stream>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel);
-        L.count();
+        kern<<<static_cast<unsigned>(ctas), P::T, smem, st>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel);
     };
-    run(kfp, "k_keyswitch", fp0, nfp, limbs - n_int);
-    run(kint, "k_keyswitch_q0", int0, nint, n_int);
+    // The integer-limb kernel (IMAD pipes) runs on the side stream beside the
+    // FP64 kernel, filling the SMs the FP64 kernel's last wave leaves idle.
+    const bool split = nfp && nint && L.aux;
+    unsigned long long launched = 0;
+    if (split) {
+        cuda_check(cudaEventRecord(L.fork_ev, L.stream), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(L.aux, L.fork_ev, 0), "cudaStreamWaitEvent");
+        launch(kint, L.aux, int0, nint);
+        launch(kfp, L.stream, fp0, nfp);
+        cuda_check(cudaEventRecord(L.join_ev, L.aux), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(L.stream, L.join_ev, 0), "cudaStreamWaitEvent");
+        launched = 2;
+    } else {
+        if (nfp) launch(kfp, L.stream, fp0, nfp), ++launched;
+        if (nint) launch(kint, L.stream, int0, nint), ++launched;
+    }
+    L.count(launched);
 }
 
 }  // namespace
