@@ -1,0 +1,288 @@
+// Plaintext-weight x ciphertext layers on the integer tensor cores (K8 in
+// SURVEY.md §2.3; conv2d_encrypted layers.hpp:174-211, dense_encrypted
+// :269-293), for limbs with q < 2^40.
+//
+// Per (component, limb, coefficient) column the layer is an exact integer
+// GEMM with a gather: y[pixel][oc] = sum_k W[k][oc] x[src(pixel,k)] mod q.
+// Both factors are residues below 2^40, so they split into five unsigned
+// bytes each (x = sum_a x_a 2^8a, W = sum_b W_b 2^8b) and
+//   sum_k W x = sum_s 2^8s D_s,  D_s = sum_{a+b=s} sum_k W_b x_a   (s = 0..8)
+// where every D_s is an exact int32 sum of u8 x u8 products while K <= 6144
+// (at most five byte pairs per s: 5 * 255^2 * 6144 < 2^31). The D_s are
+// mma.sync.m16n8k32 u8.u8.s32 tensor-core products (25 per 32-tap step: the
+// weight byte planes are the A operand, stored in global memory already in
+// fragment order; the ciphertext byte planes are the B operand, transposed
+// out of 64-bit words with byte permutes in registers). The epilogue reduces
+// sum_s D_s (2^8s mod q) with the exact FP64 modmul of ntt_core.cuh; longer
+// K folds the int32 sums into FP64 residues every 6144 taps. Modular sums
+// are order independent, so the words equal the reference's sequential
+// mul_scalar_mac accumulation (ckks.hpp:448-465).
+//
+// Tiling: a warp owns 8 consecutive columns of one (component, limb) row and
+// MT x 16 output channels; a CTA is 4 warps = 32 columns of one pixel. The
+// grid is column-block major (pixels fastest), so a column block of every
+// input cell stays L2-resident while all pixels consume it.
+
+#include <stdexcept>
+
+#include "ntt_core.cuh"
+
+namespace hecnn_b200 {
+
+namespace {
+
+constexpr int WARPS = 4;
+constexpr int KSTEP = 32;
+constexpr int FOLD_STEPS = 192;  // 6144 taps per exact int32 accumulation chunk
+
+__device__ __forceinline__ void imma(int (&c)[4], const uint4& a, unsigned b0, unsigned b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void imma_s8(int (&c)[4], const uint4& a, unsigned b0, unsigned b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+// 4x4 byte transpose of four 32-bit words: p[a] = byte a of each word, word u in byte u.
+__device__ __forceinline__ void transpose4(unsigned l0, unsigned l1, unsigned l2, unsigned l3, unsigned* p) {
+    const unsigned x01 = __byte_perm(l0, l1, 0x5140), x01h = __byte_perm(l0, l1, 0x7362);
+    const unsigned x23 = __byte_perm(l2, l3, 0x5140), x23h = __byte_perm(l2, l3, 0x7362);
+    p[0] = __byte_perm(x01, x23, 0x5410);
+    p[1] = __byte_perm(x01, x23, 0x7632);
+    p[2] = __byte_perm(x01h, x23h, 0x5410);
+    p[3] = __byte_perm(x01h, x23h, 0x7632);
+}
+
+// Byte planes of four words (taps k..k+3 of one column), the B-fragment
+// order along K: NA = 5 for residues below 2^40, 8 for full words.
+template <int NA>
+__device__ __forceinline__ void byte_planes(const u64 (&w)[4], unsigned (&p)[NA]) {
+    transpose4(static_cast<unsigned>(w[0]), static_cast<unsigned>(w[1]), static_cast<unsigned>(w[2]),
+               static_cast<unsigned>(w[3]), p);
+    const unsigned h0 = static_cast<unsigned>(w[0] >> 32), h1 = static_cast<unsigned>(w[1] >> 32);
+    const unsigned h2 = static_cast<unsigned>(w[2] >> 32), h3 = static_cast<unsigned>(w[3] >> 32);
+    if constexpr (NA == 8) {
+        transpose4(h0, h1, h2, h3, p + 4);
+    } else {
+        static_assert(NA == 5, "5 or 8 byte planes");
+        p[4] = __byte_perm(__byte_perm(h0, h1, 0x0040), __byte_perm(h2, h3, 0x0040), 0x5410);
+    }
+}
+
+template <int MT>
+__global__ void __launch_bounds__(WARPS * 32) k_conv_imma(DevRing R, ImmaMac g, const u64* __restrict__ x,
+                                                         u64* __restrict__ y, int level, int limb0, int nl) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int limbs = level + 1;
+    const long long poly_words = static_cast<long long>(limbs) * R.n;
+    const long long cell_words = 2 * poly_words;
+    const int nj = R.n / (WARPS * 8);  // column blocks per (component, limb) row
+    const long long bid = blockIdx.x;
+    const long long cb = bid / g.pixels;
+    const int p = static_cast<int>(bid - cb * g.pixels);
+    const int jb = static_cast<int>(cb % nj);
+    const int row = static_cast<int>(cb / nj);  // comp * nl + li
+    const int comp = row / nl, i = limb0 + row % nl;
+    const int j0 = jb * (WARPS * 8) + warp * 8;
+    const long long col_base = comp * poly_words + static_cast<long long>(i) * R.n + j0;
+    const u64* xc = x + col_base + gq;  // this lane's B-operand column
+    const double qd = static_cast<double>(R.mod[i].q), qinv = R.inv_q[i];
+    const u64 q = R.mod[i].q;
+    const double* cs = g.shift + i * 9;  // 2^8s mod q, read at fold time
+    const int* src = g.src + static_cast<long long>(p) * g.kpad;
+    const uint4* wf = g.wfrag + static_cast<long long>(i) * g.oc_tiles * g.ksteps * 5 * 32 + lane;
+
+    for (int ot = 0; ot < g.oc_tiles; ot += MT) {
+        double facc[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) facc[mt][c] = 0.0;
+        for (int ks0 = 0; ks0 < g.ksteps; ks0 += FOLD_STEPS) {
+            const int ks1 = min(g.ksteps, ks0 + FOLD_STEPS);
+            int acc[9][MT][4];
+#pragma unroll
+            for (int s = 0; s < 9; ++s)
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[s][mt][c] = 0;
+            for (int ks = ks0; ks < ks1; ++ks) {
+                // B operand: taps ks*32 + 4t + {0..3} (reg 0) and +16 (reg 1) of column j0 + g
+                const int4 sa = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 4 * tq));
+                const int4 sb = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 16 + 4 * tq));
+                u64 wa[4], wb[4];
+                wa[0] = sa.x >= 0 ? __ldg(xc + sa.x * cell_words) : 0;
+                wa[1] = sa.y >= 0 ? __ldg(xc + sa.y * cell_words) : 0;
+                wa[2] = sa.z >= 0 ? __ldg(xc + sa.z * cell_words) : 0;
+                wa[3] = sa.w >= 0 ? __ldg(xc + sa.w * cell_words) : 0;
+                wb[0] = sb.x >= 0 ? __ldg(xc + sb.x * cell_words) : 0;
+                wb[1] = sb.y >= 0 ? __ldg(xc + sb.y * cell_words) : 0;
+                wb[2] = sb.z >= 0 ? __ldg(xc + sb.z * cell_words) : 0;
+                wb[3] = sb.w >= 0 ? __ldg(xc + sb.w * cell_words) : 0;
+                unsigned pa[5], pb[5];
+                byte_planes<5>(wa, pa);
+                byte_planes<5>(wb, pb);
+#pragma unroll
+                for (int b = 0; b < 5; ++b) {
+                    uint4 af[MT];
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+                        af[mt] = __ldg(wf + ((static_cast<long long>(ot + mt) * g.ksteps + ks) * 5 + b) * 32);
+#pragma unroll
+                    for (int a = 0; a < 5; ++a)
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) imma(acc[a + b][mt], af[mt], pa[a], pb[a]);
+                }
+            }
+            // fold: sum_s D_s (2^8s mod q), exact FP64 (|D_s| < 2^31, sums < 2^45)
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    double v = facc[mt][c];
+#pragma unroll
+                    for (int s = 0; s < 9; ++s) v += ntt::fmodmul(static_cast<double>(acc[s][mt][c]), __ldg(cs + s), qd, qinv);
+                    facc[mt][c] = ntt::fcentre(v, qd, qinv);
+                }
+        }
+        // C fragment: c0, c1 -> row g, cols 2t, 2t+1; c2, c3 -> row g + 8
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int oc = (ot + mt) * 16 + gq + (c >= 2 ? 8 : 0);
+                const int j = j0 + 2 * tq + (c & 1);
+                if (oc >= g.oc) continue;
+                u64 v = ntt::fcanon(facc[mt][c], qd, qinv);
+                if (g.bias && comp == 0 && j == 0) v = add_mod(v, g.bias[static_cast<long long>(oc) * limbs + i], q);
+                y[(static_cast<long long>(p) * g.out_stride_pixel + oc) * cell_words + col_base - j0 + j] = v;
+            }
+    }
+}
+
+// Limbs with q >= 2^40 (the 60-bit q0): the weights enter as the six
+// balanced signed base-256 digits of the integer W = round(w * Delta) itself
+// (identical for every limb, |W| < 2^47), the ciphertext words as eight
+// unsigned bytes; 48 s8 x u8 products per tap in 13 shift classes, each an
+// exact int32 sum (|D_s| <= 6 * 128 * 255 * 6144 < 2^31). The epilogue adds
+// D_s (2^8s mod q) with 64-bit Shoup multiplies.
+__global__ void __launch_bounds__(WARPS * 32) k_conv_imma_wide(DevRing R, ImmaMac g, const u64* __restrict__ x,
+                                                              u64* __restrict__ y, int level, int limb0, int nl) {
+    constexpr int NA = 8, NB = 6, NS = NA + NB - 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int limbs = level + 1;
+    const long long poly_words = static_cast<long long>(limbs) * R.n;
+    const long long cell_words = 2 * poly_words;
+    const int nj = R.n / (WARPS * 8);
+    const long long bid = blockIdx.x;
+    const long long cb = bid / g.pixels;
+    const int p = static_cast<int>(bid - cb * g.pixels);
+    const int jb = static_cast<int>(cb % nj);
+    const int row = static_cast<int>(cb / nj);
+    const int comp = row / nl, i = limb0 + row % nl;
+    const int j0 = jb * (WARPS * 8) + warp * 8;
+    const long long col_base = comp * poly_words + static_cast<long long>(i) * R.n + j0;
+    const u64* xc = x + col_base + gq;
+    const u64 q = R.mod[i].q;
+    const ulonglong2* cs = g.shift_wide + i * 16;  // (2^8s mod q, shoup)
+    const int* src = g.src + static_cast<long long>(p) * g.kpad;
+    const uint4* wf = g.wfrag_wide + lane;
+
+    for (int ot = 0; ot < g.oc_tiles; ++ot) {
+        u64 facc[4] = {0, 0, 0, 0};
+        for (int ks0 = 0; ks0 < g.ksteps; ks0 += FOLD_STEPS) {
+            const int ks1 = min(g.ksteps, ks0 + FOLD_STEPS);
+            int acc[NS][4];
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[s][c] = 0;
+            for (int ks = ks0; ks < ks1; ++ks) {
+                const int4 sa = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 4 * tq));
+                const int4 sb = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 16 + 4 * tq));
+                u64 wa[4], wb[4];
+                wa[0] = sa.x >= 0 ? __ldg(xc + sa.x * cell_words) : 0;
+                wa[1] = sa.y >= 0 ? __ldg(xc + sa.y * cell_words) : 0;
+                wa[2] = sa.z >= 0 ? __ldg(xc + sa.z * cell_words) : 0;
+                wa[3] = sa.w >= 0 ? __ldg(xc + sa.w * cell_words) : 0;
+                wb[0] = sb.x >= 0 ? __ldg(xc + sb.x * cell_words) : 0;
+                wb[1] = sb.y >= 0 ? __ldg(xc + sb.y * cell_words) : 0;
+                wb[2] = sb.z >= 0 ? __ldg(xc + sb.z * cell_words) : 0;
+                wb[3] = sb.w >= 0 ? __ldg(xc + sb.w * cell_words) : 0;
+                unsigned pa[NA], pb[NA];
+                byte_planes<NA>(wa, pa);
+                byte_planes<NA>(wb, pb);
+#pragma unroll
+                for (int b = 0; b < NB; ++b) {
+                    const uint4 af = __ldg(wf + ((static_cast<long long>(ot) * g.ksteps + ks) * NB + b) * 32);
+#pragma unroll
+                    for (int a = 0; a < NA; ++a) imma_s8(acc[a + b], af, pa[a], pb[a]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                u64 v = facc[c];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    const int d = acc[s][c];
+                    const u64 r = d >= 0 ? static_cast<u64>(d) : q - static_cast<u64>(-static_cast<long long>(d));
+                    const ulonglong2 k = __ldg(cs + s);
+                    v = add_mod(v, mul_shoup(r, k.x, k.y, q), q);
+                }
+                facc[c] = v;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int oc = ot * 16 + gq + (c >= 2 ? 8 : 0);
+            const int j = j0 + 2 * tq + (c & 1);
+            if (oc >= g.oc) continue;
+            u64 v = facc[c];
+            if (g.bias && comp == 0 && j == 0) v = add_mod(v, g.bias[static_cast<long long>(oc) * limbs + i], q);
+            y[(static_cast<long long>(p) * g.out_stride_pixel + oc) * cell_words + col_base - j0 + j] = v;
+        }
+    }
+}
+
+}  // namespace
+
+bool imma_mac_supported(const DevRing& R, std::size_t K) {
+    return R.n >= WARPS * 8 && K > 0 && K <= (1u << 20);
+}
+
+void imma_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level, int limb0, int limb1, bool wide,
+              const Launch& L) {
+    const int nl = limb1 - limb0;
+    if (!g.pixels || !g.oc || nl <= 0) return;
+    if (R.n < WARPS * 8) throw std::invalid_argument("imma_mac: ring degree below 32");
+    const long long rows = 2LL * nl, nj = R.n / (WARPS * 8);
+    const long long blocks = rows * nj * g.pixels;
+    if (blocks > 0x7fffffffLL) throw std::runtime_error("imma_mac: grid too large");
+    const double cols = double(rows) * R.n;
+    if (wide) {
+        L.begin("k_conv_imma_wide", double(g.pixels) * g.K * g.oc * cols,
+                8.0 * cols * (double(g.pixels) * g.oc + double(g.pixels) * g.K));
+        k_conv_imma_wide<<<static_cast<unsigned>(blocks), WARPS * 32, 0, L.stream>>>(R, g, x, y, level, limb0, nl);
+        L.count();
+        check_launch("imma_mac_wide");
+        return;
+    }
+    L.begin("k_conv_imma", double(g.pixels) * g.K * g.oc * cols, 8.0 * cols * (double(g.pixels) * g.oc + double(g.pixels) * g.K));
+    if (g.oc_tiles >= 2)
+        k_conv_imma<2><<<static_cast<unsigned>(blocks), WARPS * 32, 0, L.stream>>>(R, g, x, y, level, limb0, nl);
+    else
+        k_conv_imma<1><<<static_cast<unsigned>(blocks), WARPS * 32, 0, L.stream>>>(R, g, x, y, level, limb0, nl);
+    L.count();
+    check_launch("imma_mac");
+}
+
+}  // namespace hecnn_b200

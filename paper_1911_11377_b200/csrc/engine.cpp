@@ -926,6 +926,132 @@ std::size_t Model::depth_cost() const {
 
 namespace {
 
+// Limbs whose residues fit five bytes run the linear layers on the integer
+// tensor cores (conv_imma.cu); HECNN_NO_IMMA=1 keeps every limb on the
+// FP64 / integer gather-MAC (linear.cu) for A/B comparisons.
+bool imma_limb(const Context& C, std::size_t i) { return C.ring.primes[i] < (1ull << 40); }
+
+bool imma_enabled(const Context& C, std::size_t K) {
+    const char* e = std::getenv("HECNN_NO_IMMA");  // read per layer build (cached per model and level)
+    const bool off = e && *e && *e != '0';
+    return !off && imma_mac_supported(C.dev, K);
+}
+
+// Calls f(l0, l1, tc) for maximal runs of limbs [l0, l1) of equal kind.
+template <class F>
+void for_limb_runs(const Context& C, std::size_t limbs, F f) {
+    std::size_t l0 = 0;
+    while (l0 < limbs) {
+        const bool tc = imma_limb(C, l0);
+        std::size_t l1 = l0 + 1;
+        while (l1 < limbs && imma_limb(C, l1) == tc) ++l1;
+        f(l0, l1, tc);
+        l0 = l1;
+    }
+}
+
+// A fragments of mma.m16n8k32 (row-major 16 x 32): lane (g, t) holds
+// reg0 = row g, k 4t..4t+3; reg1 = row g+8, same k; reg2/reg3 = the same rows
+// at k + 16; byte u of a register is k + u. Row = output channel in the tile.
+void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulonglong2>& w, const std::vector<int>& src,
+                      std::size_t rows, std::size_t limbs) {
+    const std::size_t K = rows, oc = static_cast<std::size_t>(lc.oc), oc_pad = static_cast<std::size_t>(lc.oc_pad);
+    const std::size_t ksteps = (K + 31) / 32, kpad = ksteps * 32;
+    std::size_t tiles = (oc + 15) / 16;
+    if (tiles >= 2) tiles = (tiles + 1) / 2 * 2;  // the kernel pairs tiles
+    std::vector<std::uint32_t> frag(limbs * tiles * ksteps * 5 * 32 * 4, 0u);
+    for (std::size_t i = 0; i < limbs; ++i) {
+        if (!imma_limb(C, i)) continue;
+        for (std::size_t t = 0; t < tiles; ++t)
+            for (std::size_t ks = 0; ks < ksteps; ++ks)
+                for (std::size_t lane = 0; lane < 32; ++lane) {
+                    const std::size_t g = lane >> 2, tq = lane & 3;
+                    for (int r = 0; r < 4; ++r) {
+                        const std::size_t o = t * 16 + g + ((r & 1) ? 8 : 0);
+                        const std::size_t k0 = ks * 32 + 4 * tq + ((r & 2) ? 16 : 0);
+                        std::uint64_t wv[4] = {0, 0, 0, 0};
+                        for (int u = 0; u < 4; ++u)
+                            if (o < oc && k0 + u < K) wv[u] = w[(i * rows + k0 + u) * oc_pad + o].x;
+                        for (int b = 0; b < 5; ++b) {
+                            std::uint32_t reg = 0;
+                            for (int u = 0; u < 4; ++u) reg |= static_cast<std::uint32_t>((wv[u] >> (8 * b)) & 0xFF) << (8 * u);
+                            frag[((((i * tiles + t) * ksteps + ks) * 5 + b) * 32 + lane) * 4 + r] = reg;
+                        }
+                    }
+                }
+    }
+    // signed weight integers W (|W| < 2^47) recovered from the widest limb and
+    // checked against every limb's residue; their balanced base-256 digits
+    // feed the wide-limb kernel
+    std::size_t wl = 0;
+    for (std::size_t i = 1; i < limbs; ++i)
+        if (C.ring.primes[i] > C.ring.primes[wl]) wl = i;
+    const std::int64_t wmax = 127LL * ((1LL << 48) - 1) / 255;  // 6 balanced digits
+    bool wide_ok = true;
+    std::vector<std::int64_t> W(K * oc, 0);
+    for (std::size_t k = 0; k < K && wide_ok; ++k)
+        for (std::size_t o = 0; o < oc && wide_ok; ++o) {
+            const u64 qw = C.ring.primes[wl], r = w[(wl * rows + k) * oc_pad + o].x;
+            const std::int64_t v = r > qw / 2 ? -static_cast<std::int64_t>(qw - r) : static_cast<std::int64_t>(r);
+            if (v > wmax || v < -wmax) wide_ok = false;
+            for (std::size_t i = 0; i < limbs && wide_ok; ++i) {
+                const u64 qi = C.ring.primes[i];
+                const u64 ri = v >= 0 ? static_cast<u64>(v) % qi : (qi - static_cast<u64>(-v) % qi) % qi;
+                if (ri != w[(i * rows + k) * oc_pad + o].x) wide_ok = false;
+            }
+            W[k * oc + o] = v;
+        }
+    if (wide_ok) {
+        std::vector<std::uint32_t> fw(tiles * ksteps * 6 * 32 * 4, 0u);
+        for (std::size_t t = 0; t < tiles; ++t)
+            for (std::size_t ks = 0; ks < ksteps; ++ks)
+                for (std::size_t lane = 0; lane < 32; ++lane) {
+                    const std::size_t g = lane >> 2, tq = lane & 3;
+                    for (int r = 0; r < 4; ++r) {
+                        const std::size_t o = t * 16 + g + ((r & 1) ? 8 : 0);
+                        const std::size_t k0 = ks * 32 + 4 * tq + ((r & 2) ? 16 : 0);
+                        std::int8_t dig[4][6] = {};
+                        for (int u = 0; u < 4; ++u) {
+                            if (o >= oc || k0 + u >= K) continue;
+                            std::int64_t v = W[(k0 + u) * oc + o];
+                            for (int b = 0; b < 6; ++b) {
+                                const std::int8_t d = static_cast<std::int8_t>(v & 0xFF);  // balanced digit
+                                dig[u][b] = d;
+                                v = (v - d) / 256;
+                            }
+                        }
+                        for (int b = 0; b < 6; ++b) {
+                            std::uint32_t reg = 0;
+                            for (int u = 0; u < 4; ++u) reg |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(dig[u][b])) << (8 * u);
+                            fw[(((t * ksteps + ks) * 6 + b) * 32 + lane) * 4 + r] = reg;
+                        }
+                    }
+                }
+        std::vector<ulonglong2> shw(limbs * 16, make_ulonglong2(0, 0));
+        for (std::size_t i = 0; i < limbs; ++i)
+            for (int s = 0; s < 13; ++s) {
+                const u64 c = C.ring.mods[i].pow(2, 8 * s);
+                shw[i * 16 + s] = make_ulonglong2(c, shoup_of(c, C.ring.primes[i]));
+            }
+        lc.wfrag_wide = C.upload_vec(fw);
+        lc.shift_wide = C.upload_vec(shw);
+    }
+    lc.wide_ok = wide_ok;
+    std::vector<double> sh(limbs * 9);
+    for (std::size_t i = 0; i < limbs; ++i)
+        for (int s = 0; s < 9; ++s) sh[i * 9 + s] = static_cast<double>(C.ring.mods[i].pow(2, 8 * s));
+    const std::size_t pixels = static_cast<std::size_t>(lc.pixels);
+    std::vector<int> sp(pixels * kpad, -1);
+    for (std::size_t p = 0; p < pixels; ++p)
+        for (std::size_t k = 0; k < K; ++k) sp[p * kpad + k] = src[p * K + k];
+    lc.wfrag = C.upload_vec(frag);
+    lc.shift = C.upload_vec(sh);
+    lc.src_pad = C.upload_vec(sp);
+    lc.kpad = static_cast<int>(kpad);
+    lc.ksteps = static_cast<int>(ksteps);
+    lc.oc_tiles = static_cast<int>(tiles);
+}
+
 // conv2d / dense as a gather-MAC (layers.hpp:174-211, 269-293)
 TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, const Shape& out_shape) {
     Trace tr("linear_layer");
@@ -995,6 +1121,7 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
         }
         lc.weights = C.upload_vec(w);
         lc.src = C.upload_vec(src);
+        if (imma_enabled(C, rows)) build_imma_cache(C, lc, w, src, rows, limbs);
         it = M.linear.emplace(key, std::move(lc)).first;
     }
     Model::LinearCache& lc = it->second;
@@ -1024,7 +1151,20 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
         GatherMac g{lc.src.as<int>() + p0 * lc.K, lc.weights.as<ulonglong2>(),
                     bit->second.as<u64>(), lc.wsplit.as<uint2>(), lc.recomb.as<ulonglong2>(),
                     static_cast<int>(m), lc.K, lc.oc, lc.oc_pad, lc.oc};
-        gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), L);
+        if (lc.ksteps) {
+            ImmaMac im{lc.src_pad.as<int>() + p0 * lc.kpad, lc.wfrag.as<uint4>(), bit->second.as<u64>(),
+                       lc.shift.as<double>(), static_cast<int>(m), lc.K, lc.kpad, lc.ksteps, lc.oc, lc.oc_tiles, lc.oc,
+                       lc.wfrag_wide.as<uint4>(), lc.shift_wide.as<ulonglong2>()};
+            for_limb_runs(C, limbs, [&](std::size_t l0, std::size_t l1, bool tc) {
+                if (tc || lc.wide_ok)
+                    imma_mac(C.dev, im, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
+                             static_cast<int>(l1), !tc, L);
+                else gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
+                                static_cast<int>(l1), L);
+            });
+        } else {
+            gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), 0, static_cast<int>(limbs), L);
+        }
         rescale(C.dev, pre.as<u64>(), out->cell(p0 * oc), static_cast<int>(level), 2 * m * oc, L);
     }
     return out;

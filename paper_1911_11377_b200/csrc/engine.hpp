@@ -190,6 +190,11 @@ struct Model {
     struct LinearCache {
         DevBuf src, weights, wsplit, recomb;
         int pixels = 0, K = 0, oc = 0, oc_pad = 0;
+        // integer tensor-core path (limbs with q < 2^40): fragment-ordered weight
+        // byte planes, 2^8s mod q table, taps padded to whole 32-tap steps
+        DevBuf wfrag, shift, src_pad, wfrag_wide, shift_wide;
+        int kpad = 0, ksteps = 0, oc_tiles = 0;
+        bool wide_ok = false;  // limbs with q >= 2^40 also on the tensor cores (signed weight digits)
     };
     std::map<std::pair<std::size_t, std::uint32_t>, LinearCache> linear;
     std::map<std::tuple<std::size_t, std::uint32_t, double>, DevBuf> bias;

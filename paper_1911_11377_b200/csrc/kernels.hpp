@@ -139,7 +139,24 @@ struct GatherMac {
     const ulonglong2* recomb;  // [limbs][2]: (2^21 mod q, shoup), (2^42 mod q, shoup)
     int pixels, K, oc, oc_pad, out_stride_pixel;  // output cell = pixel * out_stride_pixel + oc
 };
-void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, const Launch& L);
+// limbs [limb0, limb1) only (both components)
+void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, int limb0, int limb1,
+                const Launch& L);
+// The same layer on the integer tensor cores for limbs with q < 2^40 (conv_imma.cu).
+struct ImmaMac {
+    const int* src;          // [pixels][kpad] input cell per tap, -1 for invalid / padding taps
+    const uint4* wfrag;      // [limbs][oc_tiles][ksteps][5 byte planes][32 lanes] m16n8k32 A fragments
+    const u64* bias;         // [oc][level+1] residues (added to c0 coeff 0), or null
+    const double* shift;     // [limbs][9]: 2^(8s) mod q as exact doubles
+    int pixels, K, kpad, ksteps, oc, oc_tiles, out_stride_pixel;  // kpad = 32 * ksteps; oc_tiles even if >= 2
+    // limbs with q >= 2^40: signed base-256 digits of the weight integers (one
+    // copy for all limbs) [oc_tiles][ksteps][6][32 lanes], and (2^8s mod q, shoup)
+    const uint4* wfrag_wide;
+    const ulonglong2* shift_wide;  // [limbs][16]
+};
+bool imma_mac_supported(const DevRing& R, std::size_t K);
+void imma_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level, int limb0, int limb1, bool wide,
+              const Launch& L);
 // 2x2-style average pool: out cell p sums srcs[p][0..taps) then multiplies by w (shoup), level kept
 void pool_sum_scale(const DevRing& R, const u64* x, const int* srcs, int taps, const ulonglong2* w, u64* y,
                     int level, std::size_t out_cells, const Launch& L);

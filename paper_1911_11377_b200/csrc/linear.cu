@@ -168,7 +168,7 @@ __device__ __forceinline__ void gm_body(const GatherMac& g, const GmTile& T, con
 
 __global__ void __launch_bounds__(GM_TPB, HECNN_GM_MINB) k_gather_mac(DevRing R, GatherMac g, const u64* __restrict__ x,
                                                                      u64* __restrict__ y, int level, int oc_tiles,
-                                                                     int groups, int pg) {
+                                                                     int groups, int pg, int limb0, int nl) {
     // staged weights: split doubles (FP64 limbs) or (residue, shoup) (q0); one per CTA
     __shared__ __align__(16) unsigned char s_raw[KCHUNK * OCT * 16];
     __shared__ int s_src[PG][KCHUNK];
@@ -186,7 +186,10 @@ __global__ void __launch_bounds__(GM_TPB, HECNN_GM_MINB) k_gather_mac(DevRing R,
     T.p_begin = grp * pg;
     T.p_end = min(T.p_begin + pg, g.pixels);
     T.resident = g.K <= KCHUNK;  // host sets pg = 1 otherwise
-    const long long col0 = cb * T.tpb;
+    // cb -> (component, limb in [limb0, limb0 + nl), block of tpb coefficients)
+    const int nb = R.n / T.tpb;
+    const int rowc = static_cast<int>(cb / nb);
+    const long long col0 = (rowc / nl) * poly_words + static_cast<long long>(limb0 + rowc % nl) * R.n + (cb % nb) * T.tpb;
     T.col = col0 + threadIdx.x;
     T.live = T.col < T.cell_words;
     T.comp = static_cast<int>(T.col / poly_words);
@@ -236,10 +239,12 @@ __global__ void k_gather_cells(const u64* __restrict__ x, const int* __restrict_
 
 }  // namespace
 
-void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, const Launch& L) {
-    const long long cell_words = 2LL * (level + 1) * R.n;
+void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int level, int limb0, int limb1,
+                const Launch& L) {
+    const int nl = limb1 - limb0;
+    const long long cell_words = 2LL * nl * R.n;  // columns this launch covers
     const int tpb = std::min(GM_TPB, R.n);
-    if (!g.pixels || !g.oc) return;
+    if (!g.pixels || !g.oc || nl <= 0) return;
     const int oc_tiles = (g.oc + OCT - 1) / OCT;
     const int pg = g.K <= KCHUNK ? PG : 1;
     const int groups = (g.pixels + pg - 1) / pg;
@@ -248,7 +253,7 @@ void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int 
     const unsigned grid = static_cast<unsigned>(blocks);
     L.begin("k_gather_mac", double(g.pixels) * g.K * g.oc * cell_words,
             8.0 * cell_words * (double(g.pixels) * g.oc + g.pixels * g.K));
-    k_gather_mac<<<grid, tpb, 0, L.stream>>>(R, g, x, y, level, oc_tiles, groups, pg);
+    k_gather_mac<<<grid, tpb, 0, L.stream>>>(R, g, x, y, level, oc_tiles, groups, pg, limb0, nl);
     L.count();
     check_launch("gather_mac");
 }
