@@ -49,6 +49,48 @@ __device__ __forceinline__ void imma_s8(int (&c)[4], const uint4& a, unsigned b0
         : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
+// Gathered input words go through a STAGES-deep cp.async ring in shared
+// memory, laid out [stage][word][thread] (conflict-free); every thread
+// consumes only the words it copied itself, so cp.async.wait_group alone
+// orders the pipeline (no CTA barrier).
+constexpr int STAGES = 4;
+
+struct XRing {
+    u64* s;  // [STAGES][8][WARPS * 32]
+    __device__ __forceinline__ u64* at(int stage, int u) const {
+        return s + (stage * 8 + u) * (WARPS * 32) + threadIdx.x;
+    }
+};
+
+__device__ __forceinline__ void cp_async8(u64* dst, const u64* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Issue the copies of step ks (taps ks*32 + 4t + {0..3}, +16) into `stage`.
+__device__ __forceinline__ void gather_step(const XRing& ring, int stage, const int* src, int ks, int tq,
+                                            const u64* xc, long long cell_words) {
+    const int4 sa = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 4 * tq));
+    const int4 sb = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 16 + 4 * tq));
+    const int t[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        if (t[u] >= 0) cp_async8(ring.at(stage, u), xc + t[u] * cell_words);
+        else *ring.at(stage, u) = 0;
+    }
+}
+
+__device__ __forceinline__ void read_step(const XRing& ring, int stage, u64 (&wa)[4], u64 (&wb)[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        wa[u] = *ring.at(stage, u);
+        wb[u] = *ring.at(stage, 4 + u);
+    }
+}
+
 // 4x4 byte transpose of four 32-bit words: p[a] = byte a of each word, word u in byte u.
 __device__ __forceinline__ void transpose4(unsigned l0, unsigned l1, unsigned l2, unsigned l3, unsigned* p) {
     const unsigned x01 = __byte_perm(l0, l1, 0x5140), x01h = __byte_perm(l0, l1, 0x7362);
@@ -75,9 +117,12 @@ __device__ __forceinline__ void byte_planes(const u64 (&w)[4], unsigned (&p)[NA]
     }
 }
 
-template <int MT>
+// SHORT: every accumulation chunk has <= 48 steps (three shift classes per
+// exact double in the fold); otherwise classes are folded in pairs.
+template <int MT, bool SHORT>
 __global__ void __launch_bounds__(WARPS * 32) k_conv_imma(DevRing R, ImmaMac g, const u64* __restrict__ x,
-                                                         u64* __restrict__ y, int level, int limb0, int nl) {
+                                                         u64* __restrict__ y, int level, int limb0, int nl,
+                                                         int groups, int pg) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gq = lane >> 2, tq = lane & 3;
     const int limbs = level + 1;
@@ -85,8 +130,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma(DevRing R, ImmaMac g, 
     const long long cell_words = 2 * poly_words;
     const int nj = R.n / (WARPS * 8);  // column blocks per (component, limb) row
     const long long bid = blockIdx.x;
-    const long long cb = bid / g.pixels;
-    const int p = static_cast<int>(bid - cb * g.pixels);
+    const long long cb = bid / groups;  // pixel groups fastest
+    const int p_begin = static_cast<int>(bid - cb * groups) * pg;
+    const int p_end = SHORT ? min(p_begin + pg, g.pixels) : p_begin + 1;  // host: pg == 1 unless SHORT
     const int jb = static_cast<int>(cb % nj);
     const int row = static_cast<int>(cb / nj);  // comp * nl + li
     const int comp = row / nl, i = limb0 + row % nl;
@@ -96,9 +142,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma(DevRing R, ImmaMac g, 
     const double qd = static_cast<double>(R.mod[i].q), qinv = R.inv_q[i];
     const u64 q = R.mod[i].q;
     const double* cs = g.shift + i * 9;  // 2^8s mod q, read at fold time
-    const int* src = g.src + static_cast<long long>(p) * g.kpad;
     const uint4* wf = g.wfrag + static_cast<long long>(i) * g.oc_tiles * g.ksteps * 5 * 32 + lane;
+    __shared__ u64 s_ring[STAGES * 8 * WARPS * 32];
+    const XRing ring{s_ring};
 
+    for (int p = p_begin; p < p_end; ++p) {
+    const int* src = g.src + static_cast<long long>(p) * g.kpad;
     for (int ot = 0; ot < g.oc_tiles; ot += MT) {
         double facc[MT][4];
 #pragma unroll
@@ -114,19 +163,19 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma(DevRing R, ImmaMac g, 
                 for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) acc[s][mt][c] = 0;
+            // prologue: steps ks0 .. ks0 + STAGES - 2 in flight
+#pragma unroll
+            for (int d = 0; d < STAGES - 1; ++d) {
+                if (ks0 + d < ks1) gather_step(ring, (ks0 + d) % STAGES, src, ks0 + d, tq, xc, cell_words);
+                cp_async_commit();
+            }
             for (int ks = ks0; ks < ks1; ++ks) {
                 // B operand: taps ks*32 + 4t + {0..3} (reg 0) and +16 (reg 1) of column j0 + g
-                const int4 sa = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 4 * tq));
-                const int4 sb = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 16 + 4 * tq));
+                if (ks + STAGES - 1 < ks1) gather_step(ring, (ks + STAGES - 1) % STAGES, src, ks + STAGES - 1, tq, xc, cell_words);
+                cp_async_commit();
+                cp_async_wait<STAGES - 1>();
                 u64 wa[4], wb[4];
-                wa[0] = sa.x >= 0 ? __ldg(xc + sa.x * cell_words) : 0;
-                wa[1] = sa.y >= 0 ? __ldg(xc + sa.y * cell_words) : 0;
-                wa[2] = sa.z >= 0 ? __ldg(xc + sa.z * cell_words) : 0;
-                wa[3] = sa.w >= 0 ? __ldg(xc + sa.w * cell_words) : 0;
-                wb[0] = sb.x >= 0 ? __ldg(xc + sb.x * cell_words) : 0;
-                wb[1] = sb.y >= 0 ? __ldg(xc + sb.y * cell_words) : 0;
-                wb[2] = sb.z >= 0 ? __ldg(xc + sb.z * cell_words) : 0;
-                wb[3] = sb.w >= 0 ? __ldg(xc + sb.w * cell_words) : 0;
+                read_step(ring, ks % STAGES, wa, wb);
                 unsigned pa[5], pb[5];
                 byte_planes<5>(wa, pa);
                 byte_planes<5>(wb, pb);
@@ -148,8 +197,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma(DevRing R, ImmaMac g, 
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     double v = facc[mt][c];
+                    auto D = [&](int s) { return static_cast<double>(acc[s][mt][c]); };
+                    if constexpr (SHORT) {
+                        // D_s < 5 * 255^2 * 1536 < 2^29: three classes per exact double (< 2^45)
+                        v += ntt::fmodmul(D(0) + 256.0 * D(1) + 65536.0 * D(2), __ldg(cs + 0), qd, qinv);
+                        v += ntt::fmodmul(D(3) + 256.0 * D(4) + 65536.0 * D(5), __ldg(cs + 3), qd, qinv);
+                        v += ntt::fmodmul(D(6) + 256.0 * D(7) + 65536.0 * D(8), __ldg(cs + 6), qd, qinv);
+                    } else {
 #pragma unroll
-                    for (int s = 0; s < 9; ++s) v += ntt::fmodmul(static_cast<double>(acc[s][mt][c]), __ldg(cs + s), qd, qinv);
+                        for (int s = 0; s < 9; ++s) v += ntt::fmodmul(D(s), __ldg(cs + s), qd, qinv);
+                    }
                     facc[mt][c] = ntt::fcentre(v, qd, qinv);
                 }
         }
@@ -166,6 +223,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma(DevRing R, ImmaMac g, 
                 y[(static_cast<long long>(p) * g.out_stride_pixel + oc) * cell_words + col_base - j0 + j] = v;
             }
     }
+    }  // pixel loop
 }
 
 // Limbs with q >= 2^40 (the 60-bit q0): the weights enter as the six
@@ -175,7 +233,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma(DevRing R, ImmaMac g, 
 // exact int32 sum (|D_s| <= 6 * 128 * 255 * 6144 < 2^31). The epilogue adds
 // D_s (2^8s mod q) with 64-bit Shoup multiplies.
 __global__ void __launch_bounds__(WARPS * 32) k_conv_imma_wide(DevRing R, ImmaMac g, const u64* __restrict__ x,
-                                                              u64* __restrict__ y, int level, int limb0, int nl) {
+                                                              u64* __restrict__ y, int level, int limb0, int nl,
+                                                              int groups, int pg) {
     constexpr int NA = 8, NB = 6, NS = NA + NB - 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gq = lane >> 2, tq = lane & 3;
@@ -184,8 +243,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma_wide(DevRing R, ImmaMa
     const long long cell_words = 2 * poly_words;
     const int nj = R.n / (WARPS * 8);
     const long long bid = blockIdx.x;
-    const long long cb = bid / g.pixels;
-    const int p = static_cast<int>(bid - cb * g.pixels);
+    const long long cb = bid / groups;  // pixel groups fastest
+    const int p_begin = static_cast<int>(bid - cb * groups) * pg, p_end = min(p_begin + pg, g.pixels);
     const int jb = static_cast<int>(cb % nj);
     const int row = static_cast<int>(cb / nj);
     const int comp = row / nl, i = limb0 + row % nl;
@@ -194,9 +253,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma_wide(DevRing R, ImmaMa
     const u64* xc = x + col_base + gq;
     const u64 q = R.mod[i].q;
     const ulonglong2* cs = g.shift_wide + i * 16;  // (2^8s mod q, shoup)
-    const int* src = g.src + static_cast<long long>(p) * g.kpad;
     const uint4* wf = g.wfrag_wide + lane;
+    __shared__ u64 s_ring[STAGES * 8 * WARPS * 32];
+    const XRing ring{s_ring};
 
+    for (int p = p_begin; p < p_end; ++p) {
+    const int* src = g.src + static_cast<long long>(p) * g.kpad;
     for (int ot = 0; ot < g.oc_tiles; ++ot) {
         u64 facc[4] = {0, 0, 0, 0};
         for (int ks0 = 0; ks0 < g.ksteps; ks0 += FOLD_STEPS) {
@@ -206,18 +268,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma_wide(DevRing R, ImmaMa
             for (int s = 0; s < NS; ++s)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) acc[s][c] = 0;
+#pragma unroll
+            for (int d = 0; d < STAGES - 1; ++d) {
+                if (ks0 + d < ks1) gather_step(ring, (ks0 + d) % STAGES, src, ks0 + d, tq, xc, cell_words);
+                cp_async_commit();
+            }
             for (int ks = ks0; ks < ks1; ++ks) {
-                const int4 sa = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 4 * tq));
-                const int4 sb = __ldg(reinterpret_cast<const int4*>(src + ks * KSTEP + 16 + 4 * tq));
+                if (ks + STAGES - 1 < ks1) gather_step(ring, (ks + STAGES - 1) % STAGES, src, ks + STAGES - 1, tq, xc, cell_words);
+                cp_async_commit();
+                cp_async_wait<STAGES - 1>();
                 u64 wa[4], wb[4];
-                wa[0] = sa.x >= 0 ? __ldg(xc + sa.x * cell_words) : 0;
-                wa[1] = sa.y >= 0 ? __ldg(xc + sa.y * cell_words) : 0;
-                wa[2] = sa.z >= 0 ? __ldg(xc + sa.z * cell_words) : 0;
-                wa[3] = sa.w >= 0 ? __ldg(xc + sa.w * cell_words) : 0;
-                wb[0] = sb.x >= 0 ? __ldg(xc + sb.x * cell_words) : 0;
-                wb[1] = sb.y >= 0 ? __ldg(xc + sb.y * cell_words) : 0;
-                wb[2] = sb.z >= 0 ? __ldg(xc + sb.z * cell_words) : 0;
-                wb[3] = sb.w >= 0 ? __ldg(xc + sb.w * cell_words) : 0;
+                read_step(ring, ks % STAGES, wa, wb);
                 unsigned pa[NA], pb[NA];
                 byte_planes<NA>(wa, pa);
                 byte_planes<NA>(wb, pb);
@@ -231,10 +292,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma_wide(DevRing R, ImmaMa
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 u64 v = facc[c];
+                // classes in pairs: |D_s + 2^8 D_s+1| < 2^31 * 257 < 2^40 <= q, so one
+                // conditional add of q makes the pair canonical
 #pragma unroll
-                for (int s = 0; s < NS; ++s) {
-                    const int d = acc[s][c];
-                    const u64 r = d >= 0 ? static_cast<u64>(d) : q - static_cast<u64>(-static_cast<long long>(d));
+                for (int s = 0; s < NS; s += 2) {
+                    long long t = acc[s][c];
+                    if (s + 1 < NS) t += static_cast<long long>(acc[s + 1][c]) * 256;
+                    const u64 r = t >= 0 ? static_cast<u64>(t) : q - static_cast<u64>(-t);
                     const ulonglong2 k = __ldg(cs + s);
                     v = add_mod(v, mul_shoup(r, k.x, k.y, q), q);
                 }
@@ -251,6 +315,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma_wide(DevRing R, ImmaMa
             y[(static_cast<long long>(p) * g.out_stride_pixel + oc) * cell_words + col_base - j0 + j] = v;
         }
     }
+    }  // pixel loop
 }
 
 }  // namespace
@@ -265,22 +330,29 @@ void imma_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int leve
     if (!g.pixels || !g.oc || nl <= 0) return;
     if (R.n < WARPS * 8) throw std::invalid_argument("imma_mac: ring degree below 32");
     const long long rows = 2LL * nl, nj = R.n / (WARPS * 8);
-    const long long blocks = rows * nj * g.pixels;
+    const int pg = g.ksteps <= 4 ? 8 : 1;  // short K: a CTA runs a group of pixels
+    const int groups = (g.pixels + pg - 1) / pg;
+    const long long blocks = rows * nj * groups;
     if (blocks > 0x7fffffffLL) throw std::runtime_error("imma_mac: grid too large");
     const double cols = double(rows) * R.n;
     if (wide) {
         L.begin("k_conv_imma_wide", double(g.pixels) * g.K * g.oc * cols,
                 8.0 * cols * (double(g.pixels) * g.oc + double(g.pixels) * g.K));
-        k_conv_imma_wide<<<static_cast<unsigned>(blocks), WARPS * 32, 0, L.stream>>>(R, g, x, y, level, limb0, nl);
+        k_conv_imma_wide<<<static_cast<unsigned>(blocks), WARPS * 32, 0, L.stream>>>(R, g, x, y, level, limb0, nl, groups, pg);
         L.count();
         check_launch("imma_mac_wide");
         return;
     }
     L.begin("k_conv_imma", double(g.pixels) * g.K * g.oc * cols, 8.0 * cols * (double(g.pixels) * g.oc + double(g.pixels) * g.K));
-    if (g.oc_tiles >= 2)
-        k_conv_imma<2><<<static_cast<unsigned>(blocks), WARPS * 32, 0, L.stream>>>(R, g, x, y, level, limb0, nl);
-    else
-        k_conv_imma<1><<<static_cast<unsigned>(blocks), WARPS * 32, 0, L.stream>>>(R, g, x, y, level, limb0, nl);
+    const bool short_k = g.ksteps <= 48;
+    const dim3 grid(static_cast<unsigned>(blocks)), block(WARPS * 32);
+    if (g.oc_tiles >= 2) {
+        if (short_k) k_conv_imma<2, true><<<grid, block, 0, L.stream>>>(R, g, x, y, level, limb0, nl, groups, pg);
+        else k_conv_imma<2, false><<<grid, block, 0, L.stream>>>(R, g, x, y, level, limb0, nl, groups, pg);
+    } else {
+        if (short_k) k_conv_imma<1, true><<<grid, block, 0, L.stream>>>(R, g, x, y, level, limb0, nl, groups, pg);
+        else k_conv_imma<1, false><<<grid, block, 0, L.stream>>>(R, g, x, y, level, limb0, nl, groups, pg);
+    }
     L.count();
     check_launch("imma_mac");
 }
