@@ -169,6 +169,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def measured_traffic(kernel):
+    """DRAM bytes per launch for `kernel` from the committed ncu capture
+    (profiles/r01_traffic.json), or None when that kernel was not captured."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")) as f:
+            t = json.load(f).get(kernel)
+        return t["dram_bytes_per_launch"] if t else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -407,7 +418,7 @@ def run_ours(args):
             "peak": int_peak / 1e9 if int_bound else pk["hbm_gbs"],
             "unit": "Gmodmul/s" if int_bound else "GB/s",
             "frac": (achieved_ops / int_peak) if int_bound else achieved_gbs / pk["hbm_gbs"],
-            "traffic": None,
+            "traffic": measured_traffic(name),
             "ops_per_launch": ops_per_launch, "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
             "share_of_step": st["ms"] / 1e3 / dev_s,
             "peak_source": "int: live probe of chained exact FP64 modmuls (hecnn_fp64_modmul_peak, the faster "
