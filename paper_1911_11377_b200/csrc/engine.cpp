@@ -548,19 +548,15 @@ static TensorPtr relin_product(Context& C, const Tensor& x, const Tensor* y) {
     const int lv = static_cast<int>(l);
     for (std::size_t c0 = 0; c0 < x.cells; c0 += chunk) {
         const std::size_t m = std::min(chunk, x.cells - c0);
-        cuda_check(cudaMemcpyAsync(d01.get(), x.cell(c0), m * cw * 8, cudaMemcpyDeviceToDevice, C.stream), "copy x");
-        ntt_forward(C.dev, d01.as<u64>(), lv, 2 * m, L);
-        if (sq) {
-            tensor_square(C.dev, d01.as<u64>(), d01.as<u64>(), d2.as<u64>(), lv, m, L);
-        } else {
-            cuda_check(cudaMemcpyAsync(fy.get(), y->cell(c0), m * cw * 8, cudaMemcpyDeviceToDevice, C.stream), "copy y");
-            ntt_forward(C.dev, fy.as<u64>(), lv, 2 * m, L);
-            tensor_mul(C.dev, d01.as<u64>(), fy.as<u64>(), d01.as<u64>(), d2.as<u64>(), lv, m, L);
-        }
-        ntt_inverse(C.dev, d2.as<u64>(), lv, m, L);
+        // tensor product fused away: d2 = x1 y1 is formed in the INTT's first
+        // round, (d0, d1) in the key-switch epilogue (both from NTT(x), NTT(y))
+        ntt_forward_to(C.dev, x.cell(c0), d01.as<u64>(), lv, 2 * m, L);
+        if (!sq) ntt_forward_to(C.dev, y->cell(c0), fy.as<u64>(), lv, 2 * m, L);
+        const u64* fyp = sq ? d01.as<u64>() : fy.as<u64>();
+        ntt_inverse_product(C.dev, d01.as<u64>(), fyp, d2.as<u64>(), lv, m, L);
         crt_digits(C.dev, d2.as<u64>(), dig.as<u32>(), lv, static_cast<int>(D), m, L);
         keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), C.evk_f.as<double>(),
-                      d01.as<u64>(), lv, static_cast<int>(D), m, L);
+                      d01.as<u64>(), lv, static_cast<int>(D), m, L, sq ? 1 : 2, sq ? nullptr : fy.as<u64>());
         ntt_inverse(C.dev, d01.as<u64>(), lv, 2 * m, L);
         rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L);
     }
@@ -601,14 +597,13 @@ TensorPtr ct_mul_const(Context& C, const Tensor& x, double c, double scale) {
     check_scale_headroom(C, x.scale, scale, x.level);
     std::vector<ulonglong2> consts = with_shoup(C.ring, res);
     DevBuf dc = C.upload_vec(consts);
-    DevBuf tmp(&C, x.cells * x.cell_words() * 8);
     Launch L = C.L();
-    scalar_mul(C.dev, x.data(), dc.as<ulonglong2>(), tmp.as<u64>(), static_cast<int>(x.level), 2 * x.cells, L);
     const double raw_scale = x.scale * scale;
     TensorPtr out = make_tensor(C, x.cells, x.level - 1, raw_scale / static_cast<double>(C.ring.primes[x.level]));
     out->shape = x.shape;
     out->batch = x.batch;
-    rescale(C.dev, tmp.as<u64>(), out->data(), static_cast<int>(x.level), 2 * x.cells, L);
+    // the product x * c is consumed inside the rescale kernel, never stored
+    rescale(C.dev, x.data(), out->data(), static_cast<int>(x.level), 2 * x.cells, L, dc.as<ulonglong2>());
     return out;
 }
 
@@ -673,12 +668,35 @@ static TensorPtr eval_activation_cells(Context& C, const Activation& act, const 
     }
     std::uint32_t out_level = terms.back()->level;
     for (auto& t : terms) out_level = std::min(out_level, t->level);
-    TensorPtr acc = ct_mod_switch(C, *terms[0], out_level);
-    for (std::size_t i = 1; i < terms.size(); ++i) {
-        TensorPtr t = ct_mod_switch(C, *terms[i], out_level);
-        acc = ct_add(C, *acc, *t, false);
+    TensorPtr acc;
+    if (terms.size() <= static_cast<std::size_t>(kMaxTerms)) {
+        // mod_switch + add chain + add_const as one pass over the terms, with the
+        // reference's checks in its order (ckks.hpp:288-311)
+        SumTerms st{};
+        st.count = static_cast<int>(terms.size());
+        for (std::size_t i = 0; i < terms.size(); ++i) {
+            if (i) require_scale_match(terms[0]->scale, terms[i]->scale, "add");
+            st.ptr[i] = terms[i]->data();
+            st.limbs[i] = static_cast<int>(terms[i]->level + 1);
+        }
+        DevBuf dc;
+        if (act.coefficients[0] != 0.0) {
+            const double c = act.coefficients[0];
+            C.enc->check_encode(1, std::abs(c), terms[0]->scale, out_level);
+            dc = C.upload_vec(C.enc->residues_of_rounded(
+                roundl(static_cast<long double>(c) * static_cast<long double>(terms[0]->scale)), out_level));
+            st.c0 = dc.as<u64>();
+        }
+        acc = make_tensor(C, x.cells, out_level, terms[0]->scale);
+        sum_terms(C.dev, st, acc->data(), static_cast<int>(out_level), x.cells, C.L());
+    } else {
+        acc = ct_mod_switch(C, *terms[0], out_level);
+        for (std::size_t i = 1; i < terms.size(); ++i) {
+            TensorPtr t = ct_mod_switch(C, *terms[i], out_level);
+            acc = ct_add(C, *acc, *t, false);
+        }
+        if (act.coefficients[0] != 0.0) acc = ct_add_const(C, *acc, act.coefficients[0]);
     }
-    if (act.coefficients[0] != 0.0) acc = ct_add_const(C, *acc, act.coefficients[0]);
     acc->shape = x.shape;
     acc->batch = x.batch;
     return acc;

@@ -84,14 +84,31 @@ void cuda_check(cudaError_t e, const char* what);  // throws std::runtime_error 
 
 // ---- NTT (ntt.cu). polys: [count][level+1][n], limb index = poly % (level+1)
 void ntt_forward(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L);
+// out of place (src may equal dst)
+void ntt_forward_to(const DevRing& R, const u64* src, u64* dst, int level, std::size_t count, const Launch& L);
 void ntt_inverse(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L);
+// d2 = INTT(x1 * y1): x, y forward-transformed ciphertexts [count][2][level+1][n] (y may equal
+// x), the product formed in the first butterfly round; d2 [count][level+1][n] coefficients
+void ntt_inverse_product(const DevRing& R, const u64* x, const u64* y, u64* d2, int level, std::size_t count,
+                         const Launch& L);
 
 // ---- elementwise ring ops (ring_ops.cu), [count][level+1][n]
 enum class EwOp { Add, Sub, Neg, Mul, Mac };
 void poly_elementwise(const DevRing& R, EwOp op, const u64* a, const u64* b, u64* out, int level,
                       std::size_t count, const Launch& L);
 // rescale_poly on [count][level+1][n] -> [count][level][n] (ring.hpp:419-442)
-void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L);
+// scale_by: optional per-limb (c, shoup) multiplied into the input first (mul_plain + rescale)
+void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L,
+             const ulonglong2* scale_by = nullptr);
+// out = sum of the terms at level+1 limbs (+ c0 on coefficient 0 of component 0); count ciphertexts
+constexpr int kMaxTerms = 8;
+struct SumTerms {
+    const u64* ptr[kMaxTerms];
+    int limbs[kMaxTerms];
+    int count;
+    const u64* c0;  // [level+1] residues or null
+};
+void sum_terms(const DevRing& R, const SumTerms& t, u64* out, int level, std::size_t count, const Launch& L);
 // copy limbs 0..to_level of [count][level+1][n] into [count][to_level+1][n]
 void drop_limbs(const DevRing& R, const u64* in, u64* out, int level, int to_level, std::size_t count,
                 const Launch& L);
@@ -120,8 +137,11 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
 // acc01[ct] (NTT domain, [count][2][level+1][n]) += sum_t NTT(digit_t) * evk_t
 //   evk: [Dtop][2][limbs][n] values, evk_sh: Shoup companions
 //   evk_f: FP64-path copy (used for limbs with q < 2^42)
+//   mode 0: acc01 holds (d0, d1); mode 1: acc01 holds NTT(x) and d0 = x0^2, d1 = 2 x0 x1 are
+//   formed in the epilogue; mode 2: likewise d0 = x0 y0, d1 = x0 y1 + x1 y0 with fy = NTT(y)
 void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
-                   u64* acc01, int level, int D, std::size_t count, const Launch& L);
+                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode = 0,
+                   const u64* fy = nullptr);
 
 // Integer-pipe peak probe: chained Shoup modmuls (the NTT butterfly's
 // multiply), `iters` per thread over the whole GPU; returns modmuls issued.

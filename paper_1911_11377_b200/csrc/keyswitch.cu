@@ -161,7 +161,8 @@ __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const u
 // is transformed.
 template <int LOGN, int LOGB, int LOGE, int T, class A, class KeyAt>
 __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typename A::TW* tw, const u32* digits,
-                                        KeyAt key, u64* acc01, int level, int D, long long ct, int i, int b, u64 q) {
+                                        KeyAt key, u64* acc01, int level, int D, long long ct, int i, int b, u64 q,
+                                        int mode, const u64* fy) {
     using V = typename A::V;
     using TW = typename A::TW;
     constexpr bool FP = std::is_same<V, double>::value;
@@ -241,6 +242,15 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     const int limbs = level + 1;
     u64* o0 = acc01 + ((ct * 2) * limbs + i) * n + blk_off;
     u64* o1 = o0 + static_cast<long long>(limbs) * n;
+    const u64* y0 = fy ? fy + ((ct * 2) * limbs + i) * n + blk_off : nullptr;
+    const u64* y1 = fy ? y0 + static_cast<long long>(limbs) * n : nullptr;
+    const ModConst mc = R.mod[i];
+    // the tensor product's (d0, d1) from the forward-transformed operands
+    // (ckks.hpp:320-327), formed at the positions this thread writes
+    auto mulq = [&](u64 a, u64 c) -> u64 {
+        if constexpr (FP) return ntt::fcanon(ntt::fmodmul(ntt::to_fp(a), ntt::to_fp(c), ar.q, ar.qinv), ar.q, ar.qinv);
+        else return mul_mod(a, c, mc);
+    };
 #pragma unroll
     for (int uu = 0; uu < PL; ++uu) {
         const int u = threadIdx.x + uu * T;
@@ -257,8 +267,24 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                 r0 = reduce_2q(a0[uu * EL + k], q);
                 r1 = reduce_2q(a1[uu * EL + k], q);
             }
-            o0[idx] = add_mod(o0[idx], r0, q);
-            o1[idx] = add_mod(o1[idx], r1, q);
+            u64 b0, b1;
+            if (mode == 0) {  // acc01 already holds (d0, d1)
+                b0 = o0[idx];
+                b1 = o1[idx];
+            } else {  // acc01 holds NTT(x); mode 1: d = x^2, mode 2: d = x * y
+                const u64 x0 = o0[idx], x1 = o1[idx];
+                if (mode == 1) {
+                    b0 = mulq(x0, x0);
+                    const u64 c = mulq(x0, x1);
+                    b1 = add_mod(c, c, q);
+                } else {
+                    const u64 v0 = y0[idx], v1 = y1[idx];
+                    b0 = mulq(x0, v0);
+                    b1 = add_mod(mulq(x0, v1), mulq(x1, v0), q);
+                }
+            }
+            o0[idx] = add_mod(b0, r0, q);
+            o1[idx] = add_mod(b1, r1, q);
         }
     }
 }
@@ -269,7 +295,8 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
 template <int LOGN, int LOGB, int LOGE, int T, int MINB, bool FPK>
 __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
                                                  const u64* __restrict__ evk_sh, const double* __restrict__ evk_f,
-                                                 u64* __restrict__ acc01, int level, int D, int limb0, int nsel) {
+                                                 u64* __restrict__ acc01, int level, int D, int limb0, int nsel,
+                                                 int mode, const u64* __restrict__ fy) {
     constexpr int C = LOGN - LOGB;
     const long long cta = blockIdx.x;
     const int b = static_cast<int>(cta & ((1 << C) - 1));
@@ -289,7 +316,7 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
             s0 += ntt::fmodmul(v, kb, ar.q, ar.qinv);  // |s| < D q < 2^48: exact sums
             s1 += ntt::fmodmul(v, ka, ar.q, ar.qinv);
         };
-        ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd_f + ioff, digits, key, acc01, level, D, ct, i, b, q);
+        ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd_f + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
     } else {
         const ntt::IntArith ar{q, q << 1};
         const u64 two_q = q << 1;
@@ -300,7 +327,7 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
             s0 = x0 >= two_q ? x0 - two_q : x0;
             s1 = x1 >= two_q ? x1 - two_q : x1;
         };
-        ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd + ioff, digits, key, acc01, level, D, ct, i, b, q);
+        ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
     }
 }
 
@@ -329,7 +356,7 @@ struct KsPlan {
 
 template <int LOGN>
 void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
-                   u64* acc01, int level, int D, std::size_t count, const Launch& L) {
+                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy) {
     using P = KsPlan<LOGN>;
     auto kfp = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true>;
     auto kint = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false>;
@@ -355,7 +382,7 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
             2.0 * D * limbs * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
     auto launch = [&](auto kern, cudaStream_t st, int l0, int nsel) {
         const std::size_t ctas = count * static_cast<std::size_t>(nsel) << (LOGN - P::LOGB);
-        kern<<<static_cast<unsigned>(ctas), P::T, smem, st>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel);
+        kern<<<static_cast<unsigned>(ctas), P::T, smem, st>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel, mode, fy);
     };
     // The integer-limb kernel (IMAD pipes) runs on the side stream beside the
     // FP64 kernel, filling the SMs the FP64 kernel's last wave leaves idle.
@@ -398,10 +425,11 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
 }
 
 void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
-                   u64* acc01, int level, int D, std::size_t count, const Launch& L) {
+                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy) {
     if (!count) return;
+    if (mode == 2 && !fy) throw std::invalid_argument("keyswitch_mac: product mode needs the second operand");
 #define HECNN_KS_CASE(LG) \
-    case LG: run_keyswitch<LG>(R, digits, evk, evk_sh, evk_f, acc01, level, D, count, L); break;
+    case LG: run_keyswitch<LG>(R, digits, evk, evk_sh, evk_f, acc01, level, D, count, L, mode, fy); break;
     switch (R.logn) {
         HECNN_KS_CASE(3) HECNN_KS_CASE(4) HECNN_KS_CASE(5) HECNN_KS_CASE(6) HECNN_KS_CASE(7) HECNN_KS_CASE(8)
         HECNN_KS_CASE(9) HECNN_KS_CASE(10) HECNN_KS_CASE(11) HECNN_KS_CASE(12) HECNN_KS_CASE(13)

@@ -35,7 +35,7 @@ using ntt::gs_butterfly;
 // The first forward round reads HBM and the last round writes HBM directly
 // (canonical values); the inverse likewise, with n^-1 folded into the store.
 template <int LOGN, int LOGB, int LOGE, int THREADS, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB) k_ntt_fwd_block(DevRing R, u64* __restrict__ data, int limbs) {
+__global__ void __launch_bounds__(THREADS, MINB) k_ntt_fwd_block(DevRing R, const u64* src, u64* dst, int limbs) {
     extern __shared__ u64 smem[];
     constexpr int C = LOGN - LOGB;
     const long long cta = blockIdx.x;
@@ -43,17 +43,21 @@ __global__ void __launch_bounds__(THREADS, MINB) k_ntt_fwd_block(DevRing R, u64*
     const int b = static_cast<int>(cta & ((1 << C) - 1));
     const int limb = static_cast<int>(poly % limbs);
     const u64 q = R.mod[limb].q;
-    u64* g = data + (poly << LOGN) + (static_cast<long long>(b) << LOGB);
+    // src may equal dst: every element is read in the first round and written
+    // in the last, with barriers in between
+    const long long off = (poly << LOGN) + (static_cast<long long>(b) << LOGB);
+    const u64* gi = src + off;
+    u64* g = dst + off;
     const long long toff = static_cast<long long>(limb) << LOGN;
     if (ntt::fp_limb(q)) {
         const ntt::FpArith ar{static_cast<double>(q), R.inv_q[limb]};
         ntt::fwd_block<LOGB, LOGE, THREADS>(
-            reinterpret_cast<double*>(smem), ar, R.fwd_f + toff, b, C, [=](int i) { return ntt::to_fp(g[i]); },
+            reinterpret_cast<double*>(smem), ar, R.fwd_f + toff, b, C, [=](int i) { return ntt::to_fp(gi[i]); },
             [=](int i, double v, int, int) { g[i] = ntt::fcanon(v, ar.q, ar.qinv); });
     } else {
         const ntt::IntArith ar{q, q << 1};
         ntt::fwd_block<LOGB, LOGE, THREADS>(
-            smem, ar, R.fwd + toff, b, C, [=](int i) { return g[i]; },
+            smem, ar, R.fwd + toff, b, C, [=](int i) { return gi[i]; },
             [=](int i, u64 v, int, int) { g[i] = reduce_4q(v, q); });
     }
 }
@@ -90,10 +94,55 @@ __global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_block(DevRing R, u64*
     }
 }
 
+// d2 = INTT(x1 * y1) (CkksEngine::mul tensor step ckks.hpp:320-327 then
+// the relinearisation's to_coeff, :611): blockIdx.x = (poly * nblocks + b)
+// over the output polys [count][limbs]; the operands are the component-1
+// rows of the forward-transformed ciphertexts.
+template <int LOGN, int LOGB, int LOGE, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_prod(DevRing R, const u64* __restrict__ x,
+                                                                const u64* __restrict__ y, u64* __restrict__ out,
+                                                                int limbs) {
+    extern __shared__ u64 smem[];
+    constexpr int C = LOGN - LOGB;
+    const long long cta = blockIdx.x;
+    const long long poly = cta >> C;
+    const int b = static_cast<int>(cta & ((1 << C) - 1));
+    const int limb = static_cast<int>(poly % limbs);
+    const long long ct = poly / limbs;
+    const u64 q = R.mod[limb].q;
+    const long long boff = static_cast<long long>(b) << LOGB;
+    const long long in_off = (((ct * 2 + 1) * limbs + limb) << LOGN) + boff;
+    const u64* xa = x + in_off;
+    const u64* ya = y + in_off;
+    u64* g = out + (poly << LOGN) + boff;
+    const long long toff = static_cast<long long>(limb) << LOGN;
+    if (ntt::fp_limb(q)) {
+        const ntt::FpArith ar{static_cast<double>(q), R.inv_q[limb]};
+        const double ni = R.n_inv_f[limb];
+        ntt::inv_block<LOGB, LOGE, THREADS>(
+            reinterpret_cast<double*>(smem), ar, R.inv_f + toff, b, C,
+            [=](int i) { return ntt::fmodmul(ntt::to_fp(xa[i]), ntt::to_fp(ya[i]), ar.q, ar.qinv); },
+            [=](int i, double v, int, int) {
+                if constexpr (C == 0) v = ntt::fmodmul(v, ni, ar.q, ar.qinv);
+                g[i] = ntt::fcanon(v, ar.q, ar.qinv);
+            });
+    } else {
+        const ntt::IntArith ar{q, q << 1};
+        const ulonglong2 ni = R.n_inv[limb];
+        const ModConst m = R.mod[limb];
+        ntt::inv_block<LOGB, LOGE, THREADS>(
+            smem, ar, R.inv + toff, b, C, [=](int i) { return mul_mod(xa[i], ya[i], m); },
+            [=](int i, u64 v, int, int) {
+                if constexpr (C == 0) g[i] = reduce_2q(mul_shoup_lazy(v, ni.x, ni.y, q), q);
+                else g[i] = v;
+            });
+    }
+}
+
 // Column passes for N > 2^LOGB: the C stages that couple the 2^C blocks.
 // Thread = one column (poly, col), elements col + k * (N >> C).
 template <int LOGN, int C>
-__global__ void __launch_bounds__(256) k_ntt_fwd_cols(DevRing R, u64* __restrict__ data, int limbs, long long total) {
+__global__ void __launch_bounds__(256) k_ntt_fwd_cols(DevRing R, const u64* src, u64* data, int limbs, long long total) {
     constexpr int E = 1 << C, STRIDE = 1 << (LOGN - C);
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= total) return;
@@ -102,10 +151,11 @@ __global__ void __launch_bounds__(256) k_ntt_fwd_cols(DevRing R, u64* __restrict
     const int limb = static_cast<int>(poly % limbs);
     const u64 q = R.mod[limb].q, two_q = q << 1;
     const ulonglong2* tw = R.fwd + (static_cast<long long>(limb) << LOGN);
+    const u64* gi = src + (poly << LOGN) + col;
     u64* g = data + (poly << LOGN) + col;
     u64 x[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = g[static_cast<long long>(k) * STRIDE];
+    for (int k = 0; k < E; ++k) x[k] = gi[static_cast<long long>(k) * STRIDE];
 #pragma unroll
     for (int rho = 0; rho < C; ++rho) {
         const int half = E >> (rho + 1);
@@ -175,20 +225,21 @@ struct NttPlan {
 };
 
 template <int LOGN>
-void run_forward(const DevRing& R, u64* data, int limbs, std::size_t polys, const Launch& L) {
+void run_forward(const DevRing& R, const u64* src, u64* data, int limbs, std::size_t polys, const Launch& L) {
     using P = NttPlan<LOGN>;
     if constexpr (P::C > 0) {
         long long total = static_cast<long long>(polys) << (LOGN - P::C);
         L.begin("k_ntt_fwd_cols", double(polys) * (1 << (LOGN - 1)) * P::C, 16.0 * polys * (1 << LOGN));
-        k_ntt_fwd_cols<LOGN, P::C><<<static_cast<unsigned>((total + 255) / 256), 256, 0, L.stream>>>(R, data, limbs, total);
+        k_ntt_fwd_cols<LOGN, P::C><<<static_cast<unsigned>((total + 255) / 256), 256, 0, L.stream>>>(R, src, data, limbs, total);
         L.count();
+        src = data;  // the block pass continues in place
     }
     auto kern = k_ntt_fwd_block<LOGN, P::LOGB, P::LOGE, P::THREADS, P::MINB>;
     const int smem = (1 << P::LOGB) * 8;
     static bool init = (set_smem(kern, smem), true);
     (void)init;
     L.begin("k_ntt_fwd_block", double(polys) * (1 << (LOGN - 1)) * P::LOGB, 16.0 * polys * (1 << LOGN));
-    kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, data, limbs);
+    kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, src, data, limbs);
     L.count();
 }
 
@@ -210,14 +261,33 @@ void run_inverse(const DevRing& R, u64* data, int limbs, std::size_t polys, cons
     }
 }
 
+template <int LOGN>
+void run_inverse_product(const DevRing& R, const u64* x, const u64* y, u64* d2, int limbs, std::size_t polys,
+                         const Launch& L) {
+    using P = NttPlan<LOGN>;
+    auto kern = k_ntt_inv_prod<LOGN, P::LOGB, P::LOGE, P::THREADS, P::MINB>;
+    const int smem = (1 << P::LOGB) * 8;
+    static bool init = (set_smem(kern, smem), true);
+    (void)init;
+    L.begin("k_ntt_inv_block", double(polys) * ((1 << (LOGN - 1)) * P::LOGB + (1 << LOGN)), 24.0 * polys * (1 << LOGN));
+    kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, x, y, d2, limbs);
+    L.count();
+    if constexpr (P::C > 0) {
+        long long total = static_cast<long long>(polys) << (LOGN - P::C);
+        L.begin("k_ntt_inv_cols", double(polys) * (1 << (LOGN - 1)) * P::C, 16.0 * polys * (1 << LOGN));
+        k_ntt_inv_cols<LOGN, P::C><<<static_cast<unsigned>((total + 255) / 256), 256, 0, L.stream>>>(R, d2, limbs, total);
+        L.count();
+    }
+}
+
 template <bool FWD>
-void dispatch(const DevRing& R, u64* data, int level, std::size_t count, const Launch& L) {
+void dispatch(const DevRing& R, const u64* src, u64* data, int level, std::size_t count, const Launch& L) {
     const int limbs = level + 1;
     const std::size_t polys = count * static_cast<std::size_t>(limbs);
     if (polys == 0) return;
 #define HECNN_NTT_CASE(LG)                                             \
     case LG:                                                          \
-        if (FWD) run_forward<LG>(R, data, limbs, polys, L);           \
+        if (FWD) run_forward<LG>(R, src, data, limbs, polys, L);      \
         else run_inverse<LG>(R, data, limbs, polys, L);               \
         break;
     switch (R.logn) {
@@ -244,11 +314,32 @@ void dispatch(const DevRing& R, u64* data, int level, std::size_t count, const L
 }  // namespace
 
 void ntt_forward(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L) {
-    dispatch<true>(R, polys, level, count, L);
+    dispatch<true>(R, polys, polys, level, count, L);
+}
+
+void ntt_forward_to(const DevRing& R, const u64* src, u64* dst, int level, std::size_t count, const Launch& L) {
+    dispatch<true>(R, src, dst, level, count, L);
 }
 
 void ntt_inverse(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L) {
-    dispatch<false>(R, polys, level, count, L);
+    dispatch<false>(R, polys, polys, level, count, L);
+}
+
+void ntt_inverse_product(const DevRing& R, const u64* x, const u64* y, u64* d2, int level, std::size_t count,
+                         const Launch& L) {
+    const int limbs = level + 1;
+    const std::size_t polys = count * static_cast<std::size_t>(limbs);
+    if (!polys) return;
+#define HECNN_NTT_CASE(LG) \
+    case LG: run_inverse_product<LG>(R, x, y, d2, limbs, polys, L); break;
+    switch (R.logn) {
+        HECNN_NTT_CASE(3) HECNN_NTT_CASE(4) HECNN_NTT_CASE(5) HECNN_NTT_CASE(6) HECNN_NTT_CASE(7)
+        HECNN_NTT_CASE(8) HECNN_NTT_CASE(9) HECNN_NTT_CASE(10) HECNN_NTT_CASE(11) HECNN_NTT_CASE(12)
+        HECNN_NTT_CASE(13) HECNN_NTT_CASE(14) HECNN_NTT_CASE(15) HECNN_NTT_CASE(16)
+        default: throw std::invalid_argument("ntt: ring degree outside 2^3..2^16 is not supported on the device");
+    }
+#undef HECNN_NTT_CASE
+    check_launch("ntt_inverse_product");
 }
 
 }  // namespace hecnn_b200

@@ -46,22 +46,48 @@ __global__ void k_elementwise(DevRing R, int op, const u64* __restrict__ a, cons
 // rescale_poly (ring.hpp:419-442): out_i = (a_i - centre(a_l)) * p_l^{-1} mod q_i,
 // centre(v) = v if v <= floor(p_l/2) else v - p_l. One thread per (poly, j)
 // walks the l output limbs; a_l is read once.
-__global__ void k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level) {
+// SCALED: the input is first multiplied by a per-limb constant c_i (Shoup),
+// i.e. rescale(mul_plain(x, c)) (ckks.hpp:395-398 then :419-442) without
+// materialising the product.
+template <bool SCALED>
+__global__ void k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level,
+                          const ulonglong2* __restrict__ c) {
     const int j = blockIdx.y * TPB + threadIdx.x;
     if (j >= R.n) return;
     const long long poly = blockIdx.x;
     const u64* src = in + poly * (level + 1) * R.n;
     u64* dst = out + poly * level * R.n;
     const u64 p = R.mod[level].q;
-    const u64 v = src[static_cast<long long>(level) * R.n + j];
+    u64 v = src[static_cast<long long>(level) * R.n + j];
+    if constexpr (SCALED) v = mul_shoup(v, c[level].x, c[level].y, p);
     const bool upper = v > (p >> 1);
     for (int i = 0; i < level; ++i) {
         const ModConst m = R.mod[i];
         u64 centred = v < m.q ? v : reduce128(v, 0, m);
         if (upper) centred = sub_mod(centred, R.p_mod[level * R.limbs + i], m.q);
         const ulonglong2 inv = R.inv_dropped[level * R.limbs + i];
-        dst[static_cast<long long>(i) * R.n + j] = mul_shoup(sub_mod(src[static_cast<long long>(i) * R.n + j], centred, m.q), inv.x, inv.y, m.q);
+        u64 a = src[static_cast<long long>(i) * R.n + j];
+        if constexpr (SCALED) a = mul_shoup(a, c[i].x, c[i].y, m.q);
+        dst[static_cast<long long>(i) * R.n + j] = mul_shoup(sub_mod(a, centred, m.q), inv.x, inv.y, m.q);
     }
+}
+
+// Sum of up to kMaxTerms ciphertext tensors read at `limbs` limbs (each term
+// may carry more: mod_switch, ckks.hpp:288-303, is a prefix), plus a constant
+// on coefficient 0 of c0 (add_plain of encode_const, ckks.hpp:305-311).
+__global__ void k_sum_terms(DevRing R, SumTerms t, u64* __restrict__ out, int limbs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;  // (ct * 2 + comp) * limbs + i
+    const long long pc = row / limbs;
+    const int i = static_cast<int>(row % limbs);
+    const u64 q = R.mod[i].q;
+    u64 acc = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxTerms; ++k)  // constant indices: the parameter arrays stay in constant space
+        if (k < t.count) acc = add_mod(acc, __ldg(t.ptr[k] + (pc * t.limbs[k] + i) * R.n + j), q);
+    if (t.c0 && j == 0 && (pc & 1) == 0) acc = add_mod(acc, t.c0[i], q);
+    out[row * R.n + j] = acc;
 }
 
 __global__ void k_drop_limbs(const u64* __restrict__ in, u64* __restrict__ out, int n, int limbs_in, int limbs_out) {
@@ -317,12 +343,23 @@ void poly_elementwise(const DevRing& R, EwOp op, const u64* a, const u64* b, u64
     check_launch("poly_elementwise");
 }
 
-void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L) {
+void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L,
+             const ulonglong2* scale_by) {
     if (!count) return;
-    L.begin("k_rescale", double(count) * level * R.n, 8.0 * count * R.n * (2 * level + 1));
-    k_rescale<<<rows_grid(count, R.n), TPB, 0, L.stream>>>(R, in, out, level);
+    L.begin("k_rescale", double(count) * level * R.n * (scale_by ? 2 : 1), 8.0 * count * R.n * (2 * level + 1));
+    if (scale_by) k_rescale<true><<<rows_grid(count, R.n), TPB, 0, L.stream>>>(R, in, out, level, scale_by);
+    else k_rescale<false><<<rows_grid(count, R.n), TPB, 0, L.stream>>>(R, in, out, level, nullptr);
     L.count();
     check_launch("rescale");
+}
+
+void sum_terms(const DevRing& R, const SumTerms& t, u64* out, int level, std::size_t count, const Launch& L) {
+    const std::size_t rows = count * 2 * (level + 1);
+    if (!rows) return;
+    L.begin("k_sum_terms", 0, 8.0 * rows * R.n * (t.count + 1));
+    k_sum_terms<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, t, out, level + 1);
+    L.count();
+    check_launch("sum_terms");
 }
 
 void drop_limbs(const DevRing& R, const u64* in, u64* out, int level, int to_level, std::size_t count,
