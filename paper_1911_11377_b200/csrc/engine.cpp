@@ -557,8 +557,10 @@ static TensorPtr relin_product(Context& C, const Tensor& x, const Tensor* y) {
         crt_digits(C.dev, d2.as<u64>(), dig.as<u32>(), lv, static_cast<int>(D), m, L);
         keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), C.evk_f.as<double>(),
                       d01.as<u64>(), lv, static_cast<int>(D), m, L, sq ? 1 : 2, sq ? nullptr : fy.as<u64>());
-        ntt_inverse(C.dev, d01.as<u64>(), lv, 2 * m, L);
-        rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L);
+        if (!ntt_inverse_rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L)) {
+            ntt_inverse(C.dev, d01.as<u64>(), lv, 2 * m, L);
+            rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L);
+        }
     }
     return out;
 }

@@ -87,6 +87,9 @@ void ntt_forward(const DevRing& R, u64* polys, int level, std::size_t count, con
 // out of place (src may equal dst)
 void ntt_forward_to(const DevRing& R, const u64* src, u64* dst, int level, std::size_t count, const Launch& L);
 void ntt_inverse(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L);
+// out = rescale(INTT(d)) for `groups` polys of level+1 limbs (d is overwritten); false (nothing
+// launched) when the ring needs a column pass (N > 2^14): call ntt_inverse + rescale instead
+bool ntt_inverse_rescale(const DevRing& R, u64* d, u64* out, int level, std::size_t groups, const Launch& L);
 // d2 = INTT(x1 * y1): x, y forward-transformed ciphertexts [count][2][level+1][n] (y may equal
 // x), the product formed in the first butterfly round; d2 [count][level+1][n] coefficients
 void ntt_inverse_product(const DevRing& R, const u64* x, const u64* y, u64* d2, int level, std::size_t count,

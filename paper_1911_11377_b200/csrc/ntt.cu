@@ -94,6 +94,52 @@ __global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_block(DevRing R, u64*
     }
 }
 
+// Inverse NTT of limbs [limb0, limb0 + nsel) of every poly group
+// (groups = ciphertext components, `limbs` limbs each), single block pass
+// (N <= 2^LOGB). RESCALE: the last round stores rescale_poly's output
+// (ring.hpp:419-442) for limb i < L = limbs - 1 straight into `out`
+// ([groups][limbs - 1][n]), reading the top limb's coefficients, which a
+// previous launch (RESCALE = false, limb0 = L) transformed in place.
+template <int LOGN, int LOGE, int THREADS, int MINB, bool RESCALE>
+__global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_sel(DevRing R, u64* __restrict__ data, u64* __restrict__ out,
+                                                               int limbs, int limb0, int nsel) {
+    extern __shared__ u64 smem[];
+    const long long cta = blockIdx.x;
+    const long long grp = cta / nsel;
+    const int limb = limb0 + static_cast<int>(cta % nsel);
+    const u64 q = R.mod[limb].q;
+    u64* g = data + ((grp * limbs + limb) << LOGN);
+    const long long toff = static_cast<long long>(limb) << LOGN;
+    const int L = limbs - 1;
+    const u64* top = data + ((grp * limbs + L) << LOGN);
+    u64* o = out + ((grp * L + limb) << LOGN);
+    auto store = [=](int i, u64 c) {
+        if constexpr (RESCALE) {
+            const ModConst m = R.mod[limb];
+            const u64 vt = top[i];
+            u64 centred = vt < m.q ? vt : reduce128(vt, 0, m);
+            if (vt > (R.mod[L].q >> 1)) centred = sub_mod(centred, R.p_mod[L * R.limbs + limb], m.q);
+            const ulonglong2 inv = R.inv_dropped[L * R.limbs + limb];
+            o[i] = mul_shoup(sub_mod(c, centred, m.q), inv.x, inv.y, m.q);
+        } else {
+            g[i] = c;
+        }
+    };
+    if (ntt::fp_limb(q)) {
+        const ntt::FpArith ar{static_cast<double>(q), R.inv_q[limb]};
+        const double ni = R.n_inv_f[limb];
+        ntt::inv_block<LOGN, LOGE, THREADS>(
+            reinterpret_cast<double*>(smem), ar, R.inv_f + toff, 0, 0, [=](int i) { return ntt::to_fp(g[i]); },
+            [=](int i, double v, int, int) { store(i, ntt::fcanon(ntt::fmodmul(v, ni, ar.q, ar.qinv), ar.q, ar.qinv)); });
+    } else {
+        const ntt::IntArith ar{q, q << 1};
+        const ulonglong2 ni = R.n_inv[limb];
+        ntt::inv_block<LOGN, LOGE, THREADS>(
+            smem, ar, R.inv + toff, 0, 0, [=](int i) { return g[i]; },
+            [=](int i, u64 v, int, int) { store(i, reduce_2q(mul_shoup_lazy(v, ni.x, ni.y, q), q)); });
+    }
+}
+
 // d2 = INTT(x1 * y1) (CkksEngine::mul tensor step ckks.hpp:320-327 then
 // the relinearisation's to_coeff, :611): blockIdx.x = (poly * nblocks + b)
 // over the output polys [count][limbs]; the operands are the component-1
@@ -221,7 +267,8 @@ struct NttPlan {
     static constexpr int LOGE = LOGB >= 8 ? HECNN_NTT_LOGE : 3;
     static constexpr int UNITS = (1 << LOGB) >> LOGE;
     static constexpr int THREADS = UNITS >= HECNN_NTT_MAXT ? HECNN_NTT_MAXT : (UNITS >= 32 ? UNITS : 32);
-    static constexpr int MINB = THREADS >= 256 ? HECNN_NTT_MINB : 1;
+    // two CTAs per SM only when two blocks' shared memory fits (2^14 words: one per SM)
+    static constexpr int MINB = THREADS >= 256 && (2 << LOGB) * 8 <= 227 * 1024 ? HECNN_NTT_MINB : 1;
 };
 
 template <int LOGN>
@@ -323,6 +370,47 @@ void ntt_forward_to(const DevRing& R, const u64* src, u64* dst, int level, std::
 
 void ntt_inverse(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L) {
     dispatch<false>(R, polys, polys, level, count, L);
+}
+
+namespace {
+template <int LOGN>
+bool run_inverse_rescale(const DevRing& R, u64* d, u64* out, int limbs, std::size_t groups, const Launch& L) {
+    using P = NttPlan<LOGN>;
+    if constexpr (P::C > 0) {
+        return false;
+    } else {
+        auto ktop = k_ntt_inv_sel<LOGN, P::LOGE, P::THREADS, P::MINB, false>;
+        auto kres = k_ntt_inv_sel<LOGN, P::LOGE, P::THREADS, P::MINB, true>;
+        const int smem = (1 << LOGN) * 8;
+        static bool init = (set_smem(ktop, smem), set_smem(kres, smem), true);
+        (void)init;
+        const double bfly = double(1 << (LOGN - 1)) * LOGN, nn = double(1 << LOGN);
+        L.begin("k_ntt_inv_block", double(groups) * bfly, 16.0 * groups * nn);
+        ktop<<<static_cast<unsigned>(groups), P::THREADS, smem, L.stream>>>(R, d, out, limbs, limbs - 1, 1);
+        L.count();
+        const std::size_t polys = groups * static_cast<std::size_t>(limbs - 1);
+        L.begin("k_ntt_inv_rescale", double(polys) * (bfly + 2 * nn), 8.0 * nn * (2.0 * polys + groups));
+        kres<<<static_cast<unsigned>(polys), P::THREADS, smem, L.stream>>>(R, d, out, limbs, 0, limbs - 1);
+        L.count();
+        return true;
+    }
+}
+}  // namespace
+
+bool ntt_inverse_rescale(const DevRing& R, u64* d, u64* out, int level, std::size_t groups, const Launch& L) {
+    if (level < 1 || !groups) return false;
+    bool done = false;
+#define HECNN_NTT_CASE(LG) \
+    case LG: done = run_inverse_rescale<LG>(R, d, out, level + 1, groups, L); break;
+    switch (R.logn) {
+        HECNN_NTT_CASE(3) HECNN_NTT_CASE(4) HECNN_NTT_CASE(5) HECNN_NTT_CASE(6) HECNN_NTT_CASE(7)
+        HECNN_NTT_CASE(8) HECNN_NTT_CASE(9) HECNN_NTT_CASE(10) HECNN_NTT_CASE(11) HECNN_NTT_CASE(12)
+        HECNN_NTT_CASE(13) HECNN_NTT_CASE(14) HECNN_NTT_CASE(15) HECNN_NTT_CASE(16)
+        default: return false;
+    }
+#undef HECNN_NTT_CASE
+    check_launch("ntt_inverse_rescale");
+    return done;
 }
 
 void ntt_inverse_product(const DevRing& R, const u64* x, const u64* y, u64* d2, int level, std::size_t count,
