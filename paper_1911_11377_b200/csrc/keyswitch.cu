@@ -147,6 +147,40 @@ __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const u
     }
 }
 
+// The same column stages on the FP64 pipe (limbs with q < 2^42): values stay
+// below (C + 1) q < 2^45 in magnitude, so fmodmul stays exact without
+// corrections; the block's first round continues from these doubles.
+template <int LOGN, int C>
+__device__ __forceinline__ double column_value_fp(const u32* __restrict__ dig, const double* __restrict__ tw, u64 q,
+                                                  double qd, double qinv, int r, int b) {
+    constexpr int E = 1 << C, B = 1 << (LOGN - C);
+    double x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) x[k] = ntt::to_fp(lift_digit(dig[r + k * B], q));
+#pragma unroll
+    for (int rho = 0; rho < C; ++rho) {
+        const int half = E >> (rho + 1);
+#pragma unroll
+        for (int blk = 0; blk < (1 << rho); ++blk) {
+            const double w = tw[(1 << rho) + blk];
+#pragma unroll
+            for (int kk = 0; kk < half; ++kk) {
+                double& a = x[blk * 2 * half + kk];
+                double& c = x[blk * 2 * half + kk + half];
+                const double v = ntt::fmodmul(c, w, qd, qinv);
+                const double u = a;
+                a = u + v;
+                c = u - v;
+            }
+        }
+    }
+    double v = x[0];
+#pragma unroll
+    for (int k = 1; k < E; ++k)
+        if (k == b) v = x[k];
+    return v;
+}
+
 // Per digit t: lift -> forward NTT (shared rounds) -> in the last butterfly
 // round each thread multiplies its outputs by (b_t, a_t) and accumulates;
 // accumulator positions are the thread's last-round positions, identical for
@@ -223,10 +257,10 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
             if constexpr (PREFETCH) {
                 (void)r;
                 return ntt::to_fp(lift_digit(cur[uu * E0 + k], q));
+            } else if constexpr (FP) {
+                return column_value_fp<LOGN, C>(dig, R.fwd_f + (static_cast<long long>(i) << LOGN), q, ar.q, ar.qinv, r, b);
             } else {
-                const u64 v = column_value<LOGN, C>(dig, itw, q, r, b);
-                if constexpr (FP) return ntt::to_fp(v);
-                else return v;
+                return column_value<LOGN, C>(dig, itw, q, r, b);
             }
         };
         ntt::fwd_block<LOGB, LOGE, T>(reinterpret_cast<V*>(smem), ar, stw, 0, 0, first,
