@@ -3,12 +3,9 @@
 set -e
 cd "$(dirname "$0")/.."
 declare -A V
-V[ha]=""
-V[hb]="-DHECNN_GM_TAPB=2"
-V[hc]="-DHECNN_GM_TAPB=2 -DHECNN_GM_MINB=1"
-V[hd]="-DHECNN_GM_OCT=4 -DHECNN_GM_MINB=3"
-V[he]="-DHECNN_GM_TAPB=2 -DHECNN_GM_TPB=128 -DHECNN_GM_MINB=4"
-V[hf]="-DHECNN_GM_OCT=4 -DHECNN_GM_TAPB=8 -DHECNN_GM_MINB=3"
+V[ka]=""
+V[kb]="-DHECNN_KS_MAXT=1024"
+V[kc]="-DHECNN_KS_MAXT=1024 -DHECNN_KS_LOGE=4"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
