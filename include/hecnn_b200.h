@@ -146,6 +146,12 @@ int hecnn_tensor_shape(const hecnn_tensor* t, int* flat, size_t* h, size_t* w, s
 int hecnn_tensor_data(const hecnn_tensor* t, uint64_t** dptr);
 int hecnn_tensor_upload(hecnn_context* ctx, hecnn_tensor* t, const uint64_t* host);
 int hecnn_tensor_download(hecnn_context* ctx, const hecnn_tensor* t, uint64_t* host);
+/* Asynchronous variants for pipelined serving: the copy is enqueued on `stream`
+ * (a cudaStream_t; NULL = the context's stream) and the call returns at once.
+ * `host` must be pinned and stay valid until the stream reaches the copy; the
+ * caller orders the copy against the context's work with CUDA events. */
+int hecnn_tensor_upload_async(hecnn_context* ctx, hecnn_tensor* t, const uint64_t* host, void* stream);
+int hecnn_tensor_download_async(hecnn_context* ctx, const hecnn_tensor* t, uint64_t* host, void* stream);
 /* device-to-device copy of the words (e.g. into an NCCL buffer) */
 int hecnn_tensor_copy_to_device(hecnn_context* ctx, const hecnn_tensor* t, void* dst);
 

@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = (
     "hecnn_poly_add", "hecnn_poly_sub", "hecnn_poly_neg", "hecnn_poly_pointwise_mul", "hecnn_poly_pointwise_mac",
     "hecnn_rescale_poly", "hecnn_key_switch", "hecnn_tensor_create", "hecnn_tensor_destroy", "hecnn_tensor_info",
     "hecnn_tensor_set_shape", "hecnn_tensor_shape", "hecnn_tensor_data", "hecnn_tensor_upload",
-    "hecnn_tensor_download", "hecnn_encrypt_tensor", "hecnn_encrypt_raw", "hecnn_decrypt_raw",
+    "hecnn_tensor_download", "hecnn_tensor_upload_async", "hecnn_tensor_download_async", "hecnn_encrypt_tensor", "hecnn_encrypt_raw", "hecnn_decrypt_raw",
     "hecnn_decrypt_tensor", "hecnn_ct_add", "hecnn_ct_sub", "hecnn_ct_mul", "hecnn_ct_square", "hecnn_ct_rescale",
     "hecnn_ct_mod_switch", "hecnn_ct_mul_const", "hecnn_ct_add_const", "hecnn_eval_activation",
     "hecnn_model_create", "hecnn_model_destroy", "hecnn_model_depth_cost", "hecnn_forward_encrypted",
@@ -106,6 +106,8 @@ _SIGNATURES = {
     "hecnn_tensor_data": [_V, ctypes.POINTER(_PU64)],
     "hecnn_tensor_upload": [_V, _V, _PU64],
     "hecnn_tensor_download": [_V, _V, _PU64],
+    "hecnn_tensor_upload_async": [_V, _V, _PU64, _V],
+    "hecnn_tensor_download_async": [_V, _V, _PU64, _V],
     "hecnn_tensor_copy_to_device": [_V, _V, _V],
     "hecnn_encrypt_tensor": [_V, _PD, _SZ, _SZ, _U64, _PV],
     "hecnn_encrypt_raw": [_V, _PU64, _PI64, _PI64, _PI64, _SZ, _D, _PV],
@@ -682,6 +684,16 @@ class CkksEngine:
 
     def download_into(self, t: "EncryptedTensor", host_ptr: int):
         _check(lib().hecnn_tensor_download(self.ctx, t.handle, ctypes.cast(host_ptr, _u64p)))
+
+    def upload_async(self, t: "EncryptedTensor", host_ptr: int, stream: int = 0):
+        """Enqueue the H2D on `stream` (cudaStream_t as int; 0 = the context's stream) and
+        return; host_ptr must be pinned and outlive the copy."""
+        _check(lib().hecnn_tensor_upload_async(self.ctx, t.handle, ctypes.cast(host_ptr, _u64p),
+                                               ctypes.c_void_p(stream or None)))
+
+    def download_async(self, t: "EncryptedTensor", host_ptr: int, stream: int = 0):
+        _check(lib().hecnn_tensor_download_async(self.ctx, t.handle, ctypes.cast(host_ptr, _u64p),
+                                                 ctypes.c_void_p(stream or None)))
 
     def empty_tensor(self, cells: int, level: int, scale: float) -> "EncryptedTensor":
         h = ctypes.c_void_p()

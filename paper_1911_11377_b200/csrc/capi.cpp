@@ -417,6 +417,24 @@ int hecnn_tensor_download(hecnn_context* ctx, const hecnn_tensor* t, uint64_t* h
     return guard([&] { C(ctx).download(host, T(t).data(), T(t).cells * T(t).cell_words() * 8); });
 }
 
+int hecnn_tensor_upload_async(hecnn_context* ctx, hecnn_tensor* t, const uint64_t* host, void* stream) {
+    return guard([&] {
+        if (!host) throw std::invalid_argument("tensor_upload_async: null host buffer");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : C(ctx).stream;
+        cuda_check(cudaMemcpyAsync(t->t->data(), host, t->t->cells * t->t->cell_words() * 8, cudaMemcpyHostToDevice, st),
+                   "cudaMemcpyAsync H2D");
+    });
+}
+
+int hecnn_tensor_download_async(hecnn_context* ctx, const hecnn_tensor* t, uint64_t* host, void* stream) {
+    return guard([&] {
+        if (!host) throw std::invalid_argument("tensor_download_async: null host buffer");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : C(ctx).stream;
+        cuda_check(cudaMemcpyAsync(host, T(t).data(), T(t).cells * T(t).cell_words() * 8, cudaMemcpyDeviceToHost, st),
+                   "cudaMemcpyAsync D2H");
+    });
+}
+
 int hecnn_encrypt_tensor(hecnn_context* ctx, const double* data, size_t batch, size_t positions, uint64_t seed,
                          hecnn_tensor** out) {
     return guard([&] { *out = wrap(ctx, encrypt_tensor(C(ctx), data, batch, positions, seed)); });

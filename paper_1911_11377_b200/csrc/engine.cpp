@@ -350,9 +350,14 @@ Context::~Context() {
 
 void Context::upload(void* dst, const void* src, std::size_t bytes) {
     cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream), "cudaMemcpyAsync H2D");
-    // pageable source: the copy has been staged when the call returns, but keep the
-    // host buffer's lifetime rule simple for callers by synchronizing here
-    cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    // A pageable source has been staged when cudaMemcpyAsync returns, so the
+    // caller may reuse it and the stream keeps running (the engine's small
+    // constant tables). A pinned source is read by the DMA later: wait, so the
+    // caller's buffer-lifetime rule stays "valid for the duration of the call".
+    cudaPointerAttributes a{};
+    const bool pinned = cudaPointerGetAttributes(&a, src) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // clear a possible "invalid value" from the query
+    if (pinned) cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
 }
 
 void Context::download(void* dst, const void* src, std::size_t bytes) {
