@@ -595,15 +595,20 @@ TensorPtr ct_mod_switch(Context& C, const Tensor& x, std::uint32_t to_level) {
     return out;
 }
 
-// mul_plain(x, encode_const(c, scale, x.level)) (ckks.hpp:395-398, 372-382, 588-597)
-TensorPtr ct_mul_const(Context& C, const Tensor& x, double c, double scale) {
+// encode_const + mul_plain's checks (ckks.hpp:372-382, 395-398), then the constant's
+// residues with Shoup companions on the device
+static DevBuf mul_const_table(Context& C, const Tensor& x, double c, double scale) {
     C.enc->check_encode(1, std::abs(c), scale, x.level);
     std::vector<u64> res =
         C.enc->residues_of_rounded(roundl(static_cast<long double>(c) * static_cast<long double>(scale)), x.level);
     if (x.level == 0) throw std::invalid_argument("mul_plain: at last level, no room to rescale");
     check_scale_headroom(C, x.scale, scale, x.level);
-    std::vector<ulonglong2> consts = with_shoup(C.ring, res);
-    DevBuf dc = C.upload_vec(consts);
+    return C.upload_vec(with_shoup(C.ring, res));
+}
+
+// mul_plain(x, encode_const(c, scale, x.level)) (ckks.hpp:395-398, 372-382, 588-597)
+TensorPtr ct_mul_const(Context& C, const Tensor& x, double c, double scale) {
+    DevBuf dc = mul_const_table(C, x, c, scale);
     Launch L = C.L();
     const double raw_scale = x.scale * scale;
     TensorPtr out = make_tensor(C, x.cells, x.level - 1, raw_scale / static_cast<double>(C.ring.primes[x.level]));
@@ -668,10 +673,48 @@ static TensorPtr eval_activation_cells(Context& C, const Activation& act, const 
     };
     const double target = C.scale;
     std::vector<TensorPtr> terms;
-    for (std::size_t k = 1; k <= d; ++k) {
+    for (std::size_t k = 1; k < d; ++k) {
         const Tensor& p = power(k);
         double u = target * static_cast<double>(C.ring.primes[p.level]) / p.scale;
         terms.push_back(ct_mul_const(C, p, act.coefficients[k], u));
+    }
+    {
+        // The last term (the highest power, lowest level) is rescaled with the
+        // other terms and the constant added on the way out when its level is
+        // the output level; checks keep the reference's order.
+        const Tensor& p = power(d);
+        const double u = target * static_cast<double>(C.ring.primes[p.level]) / p.scale;
+        const std::uint32_t lvl = p.level - (p.level ? 1 : 0);
+        bool fuse = p.level > 0 && terms.size() + 1 <= static_cast<std::size_t>(kMaxTerms);
+        for (auto& t : terms) fuse = fuse && t->level >= lvl;
+        if (fuse) {
+            DevBuf dc = mul_const_table(C, p, act.coefficients[d], u);
+            const double sc = p.scale * u / static_cast<double>(C.ring.primes[p.level]);
+            const double s0 = terms.empty() ? sc : terms[0]->scale;
+            for (std::size_t i = 1; i < terms.size(); ++i) require_scale_match(s0, terms[i]->scale, "add");
+            if (!terms.empty()) require_scale_match(s0, sc, "add");
+            SumTerms st{};
+            st.count = static_cast<int>(terms.size());
+            for (std::size_t i = 0; i < terms.size(); ++i) {
+                st.ptr[i] = terms[i]->data();
+                st.limbs[i] = static_cast<int>(terms[i]->level + 1);
+            }
+            DevBuf d0;
+            if (act.coefficients[0] != 0.0) {
+                const double c = act.coefficients[0];
+                C.enc->check_encode(1, std::abs(c), s0, lvl);
+                d0 = C.upload_vec(
+                    C.enc->residues_of_rounded(roundl(static_cast<long double>(c) * static_cast<long double>(s0)), lvl));
+                st.c0 = d0.as<u64>();
+            }
+            TensorPtr acc = make_tensor(C, x.cells, lvl, s0);
+            rescale(C.dev, p.data(), acc->data(), static_cast<int>(p.level), 2 * x.cells, C.L(), dc.as<ulonglong2>(),
+                    &st);
+            acc->shape = x.shape;
+            acc->batch = x.batch;
+            return acc;
+        }
+        terms.push_back(ct_mul_const(C, p, act.coefficients[d], u));
     }
     std::uint32_t out_level = terms.back()->level;
     for (auto& t : terms) out_level = std::min(out_level, t->level);

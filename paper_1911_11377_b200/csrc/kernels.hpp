@@ -100,9 +100,6 @@ enum class EwOp { Add, Sub, Neg, Mul, Mac };
 void poly_elementwise(const DevRing& R, EwOp op, const u64* a, const u64* b, u64* out, int level,
                       std::size_t count, const Launch& L);
 // rescale_poly on [count][level+1][n] -> [count][level][n] (ring.hpp:419-442)
-// scale_by: optional per-limb (c, shoup) multiplied into the input first (mul_plain + rescale)
-void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L,
-             const ulonglong2* scale_by = nullptr);
 // out = sum of the terms at level+1 limbs (+ c0 on coefficient 0 of component 0); count ciphertexts
 constexpr int kMaxTerms = 8;
 struct SumTerms {
@@ -111,6 +108,11 @@ struct SumTerms {
     int count;
     const u64* c0;  // [level+1] residues or null
 };
+// scale_by: optional per-limb (c, shoup) multiplied into the input first (mul_plain + rescale);
+// add: optional terms (ciphertext tensors of >= level limbs, read as their first `level` limbs,
+// i.e. mod-switched) and constant added to the result (count = polys = 2 x ciphertexts)
+void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L,
+             const ulonglong2* scale_by = nullptr, const SumTerms* add = nullptr);
 void sum_terms(const DevRing& R, const SumTerms& t, u64* out, int level, std::size_t count, const Launch& L);
 // copy limbs 0..to_level of [count][level+1][n] into [count][to_level+1][n]
 void drop_limbs(const DevRing& R, const u64* in, u64* out, int level, int to_level, std::size_t count,

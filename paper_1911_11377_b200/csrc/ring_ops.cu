@@ -49,9 +49,11 @@ __global__ void k_elementwise(DevRing R, int op, const u64* __restrict__ a, cons
 // SCALED: the input is first multiplied by a per-limb constant c_i (Shoup),
 // i.e. rescale(mul_plain(x, c)) (ckks.hpp:395-398 then :419-442) without
 // materialising the product.
-template <bool SCALED>
+// ADD: the activation's other terms (and its constant) are added on the way
+// out (mod_switch + add + add_plain, ckks.hpp:288-311, fused).
+template <bool SCALED, bool ADD>
 __global__ void k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level,
-                          const ulonglong2* __restrict__ c) {
+                          const ulonglong2* __restrict__ c, SumTerms t) {
     const int j = blockIdx.y * TPB + threadIdx.x;
     if (j >= R.n) return;
     const long long poly = blockIdx.x;
@@ -68,7 +70,14 @@ __global__ void k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict
         const ulonglong2 inv = R.inv_dropped[level * R.limbs + i];
         u64 a = src[static_cast<long long>(i) * R.n + j];
         if constexpr (SCALED) a = mul_shoup(a, c[i].x, c[i].y, m.q);
-        dst[static_cast<long long>(i) * R.n + j] = mul_shoup(sub_mod(a, centred, m.q), inv.x, inv.y, m.q);
+        u64 r = mul_shoup(sub_mod(a, centred, m.q), inv.x, inv.y, m.q);
+        if constexpr (ADD) {
+#pragma unroll
+            for (int k = 0; k < kMaxTerms; ++k)
+                if (k < t.count) r = add_mod(r, __ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j), m.q);
+            if (t.c0 && j == 0 && (poly & 1) == 0) r = add_mod(r, t.c0[i], m.q);
+        }
+        dst[static_cast<long long>(i) * R.n + j] = r;
     }
 }
 
@@ -344,11 +353,16 @@ void poly_elementwise(const DevRing& R, EwOp op, const u64* a, const u64* b, u64
 }
 
 void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L,
-             const ulonglong2* scale_by) {
+             const ulonglong2* scale_by, const SumTerms* add) {
     if (!count) return;
-    L.begin("k_rescale", double(count) * level * R.n * (scale_by ? 2 : 1), 8.0 * count * R.n * (2 * level + 1));
-    if (scale_by) k_rescale<true><<<rows_grid(count, R.n), TPB, 0, L.stream>>>(R, in, out, level, scale_by);
-    else k_rescale<false><<<rows_grid(count, R.n), TPB, 0, L.stream>>>(R, in, out, level, nullptr);
+    const SumTerms none{};
+    const double extra = add ? add->count : 0;
+    L.begin("k_rescale", double(count) * level * R.n * (scale_by ? 2 : 1),
+            8.0 * count * R.n * (2 * level + 1 + extra * level));
+    const dim3 grid = rows_grid(count, R.n);
+    if (add) k_rescale<true, true><<<grid, TPB, 0, L.stream>>>(R, in, out, level, scale_by, *add);
+    else if (scale_by) k_rescale<true, false><<<grid, TPB, 0, L.stream>>>(R, in, out, level, scale_by, none);
+    else k_rescale<false, false><<<grid, TPB, 0, L.stream>>>(R, in, out, level, nullptr, none);
     L.count();
     check_launch("rescale");
 }
