@@ -718,35 +718,13 @@ static TensorPtr eval_activation_cells(Context& C, const Activation& act, const 
     }
     std::uint32_t out_level = terms.back()->level;
     for (auto& t : terms) out_level = std::min(out_level, t->level);
-    TensorPtr acc;
-    if (terms.size() <= static_cast<std::size_t>(kMaxTerms)) {
-        // mod_switch + add chain + add_const as one pass over the terms, with the
-        // reference's checks in its order (ckks.hpp:288-311)
-        SumTerms st{};
-        st.count = static_cast<int>(terms.size());
-        for (std::size_t i = 0; i < terms.size(); ++i) {
-            if (i) require_scale_match(terms[0]->scale, terms[i]->scale, "add");
-            st.ptr[i] = terms[i]->data();
-            st.limbs[i] = static_cast<int>(terms[i]->level + 1);
-        }
-        DevBuf dc;
-        if (act.coefficients[0] != 0.0) {
-            const double c = act.coefficients[0];
-            C.enc->check_encode(1, std::abs(c), terms[0]->scale, out_level);
-            dc = C.upload_vec(C.enc->residues_of_rounded(
-                roundl(static_cast<long double>(c) * static_cast<long double>(terms[0]->scale)), out_level));
-            st.c0 = dc.as<u64>();
-        }
-        acc = make_tensor(C, x.cells, out_level, terms[0]->scale);
-        sum_terms(C.dev, st, acc->data(), static_cast<int>(out_level), x.cells, C.L());
-    } else {
-        acc = ct_mod_switch(C, *terms[0], out_level);
-        for (std::size_t i = 1; i < terms.size(); ++i) {
-            TensorPtr t = ct_mod_switch(C, *terms[i], out_level);
-            acc = ct_add(C, *acc, *t, false);
-        }
-        if (act.coefficients[0] != 0.0) acc = ct_add_const(C, *acc, act.coefficients[0]);
+    // (more than kMaxTerms terms: the reference's chain of mod_switch / add / add_const)
+    TensorPtr acc = ct_mod_switch(C, *terms[0], out_level);
+    for (std::size_t i = 1; i < terms.size(); ++i) {
+        TensorPtr t = ct_mod_switch(C, *terms[i], out_level);
+        acc = ct_add(C, *acc, *t, false);
     }
+    if (act.coefficients[0] != 0.0) acc = ct_add_const(C, *acc, act.coefficients[0]);
     acc->shape = x.shape;
     acc->batch = x.batch;
     return acc;

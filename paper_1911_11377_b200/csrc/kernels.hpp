@@ -100,7 +100,8 @@ enum class EwOp { Add, Sub, Neg, Mul, Mac };
 void poly_elementwise(const DevRing& R, EwOp op, const u64* a, const u64* b, u64* out, int level,
                       std::size_t count, const Launch& L);
 // rescale_poly on [count][level+1][n] -> [count][level][n] (ring.hpp:419-442)
-// out = sum of the terms at level+1 limbs (+ c0 on coefficient 0 of component 0); count ciphertexts
+// Terms added by rescale's fused epilogue: ciphertext tensors read at their first
+// `level` limbs (+ c0 on coefficient 0 of component 0)
 constexpr int kMaxTerms = 8;
 struct SumTerms {
     const u64* ptr[kMaxTerms];
@@ -113,7 +114,6 @@ struct SumTerms {
 // i.e. mod-switched) and constant added to the result (count = polys = 2 x ciphertexts)
 void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t count, const Launch& L,
              const ulonglong2* scale_by = nullptr, const SumTerms* add = nullptr);
-void sum_terms(const DevRing& R, const SumTerms& t, u64* out, int level, std::size_t count, const Launch& L);
 // copy limbs 0..to_level of [count][level+1][n] into [count][to_level+1][n]
 void drop_limbs(const DevRing& R, const u64* in, u64* out, int level, int to_level, std::size_t count,
                 const Launch& L);

@@ -81,24 +81,6 @@ __global__ void k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict
     }
 }
 
-// Sum of up to kMaxTerms ciphertext tensors read at `limbs` limbs (each term
-// may carry more: mod_switch, ckks.hpp:288-303, is a prefix), plus a constant
-// on coefficient 0 of c0 (add_plain of encode_const, ckks.hpp:305-311).
-__global__ void k_sum_terms(DevRing R, SumTerms t, u64* __restrict__ out, int limbs) {
-    const int j = blockIdx.y * TPB + threadIdx.x;
-    if (j >= R.n) return;
-    const long long row = blockIdx.x;  // (ct * 2 + comp) * limbs + i
-    const long long pc = row / limbs;
-    const int i = static_cast<int>(row % limbs);
-    const u64 q = R.mod[i].q;
-    u64 acc = 0;
-#pragma unroll
-    for (int k = 0; k < kMaxTerms; ++k)  // constant indices: the parameter arrays stay in constant space
-        if (k < t.count) acc = add_mod(acc, __ldg(t.ptr[k] + (pc * t.limbs[k] + i) * R.n + j), q);
-    if (t.c0 && j == 0 && (pc & 1) == 0) acc = add_mod(acc, t.c0[i], q);
-    out[row * R.n + j] = acc;
-}
-
 __global__ void k_drop_limbs(const u64* __restrict__ in, u64* __restrict__ out, int n, int limbs_in, int limbs_out) {
     const int j = blockIdx.y * TPB + threadIdx.x;
     if (j >= n) return;
@@ -365,15 +347,6 @@ void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t c
     else k_rescale<false, false><<<grid, TPB, 0, L.stream>>>(R, in, out, level, nullptr, none);
     L.count();
     check_launch("rescale");
-}
-
-void sum_terms(const DevRing& R, const SumTerms& t, u64* out, int level, std::size_t count, const Launch& L) {
-    const std::size_t rows = count * 2 * (level + 1);
-    if (!rows) return;
-    L.begin("k_sum_terms", 0, 8.0 * rows * R.n * (t.count + 1));
-    k_sum_terms<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, t, out, level + 1);
-    L.count();
-    check_launch("sum_terms");
 }
 
 void drop_limbs(const DevRing& R, const u64* in, u64* out, int level, int to_level, std::size_t count,

@@ -205,7 +205,9 @@ def test_rescale_mul_const_add_const(ref):
 
 
 @pytest.mark.parametrize("coeffs", [[0.0, 0.5, 0.000469841857369822], [0.0, 0.0, 1.0], [0.1, -0.3, 0.2, 0.05],
-                                    [0.25, 1.0, 0.5, -0.1, 0.02]])
+                                    [0.25, 1.0, 0.5, -0.1, 0.02],
+                                    # degree 9: more terms than the fused rescale-and-add epilogue takes
+                                    [0.05, 0.5, 0.1, 0.0, -0.02, 0.0, 0.003, 0.0, -0.0004, 0.00002]])
 def test_eval_activation_word_identical(ref, coeffs):
     p = hb.preset_params("nn-n4096-d8")
     eng, r = engines(ref, p, seed=6)
