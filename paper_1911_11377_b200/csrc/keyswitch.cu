@@ -377,6 +377,9 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
 #ifndef HECNN_KS_MINB
 #define HECNN_KS_MINB 1
 #endif
+#ifndef HECNN_KS_MAXT_COL
+#define HECNN_KS_MAXT_COL 1024
+#endif
 
 template <int LOGN>
 struct KsPlan {
@@ -386,7 +389,7 @@ struct KsPlan {
     static constexpr int UNITS = B >> LOGE;
     // N > 2^13 (column stages recomputed per block): 1024 threads, 8 words
     // each, measured 6% faster at N = 2^14 than 512 x 16; 512 at N <= 2^13
-    static constexpr int MAXT = LOGN > LOGB ? 1024 : HECNN_KS_MAXT;
+    static constexpr int MAXT = LOGN > LOGB ? HECNN_KS_MAXT_COL : HECNN_KS_MAXT;
     static constexpr int T = UNITS >= MAXT ? MAXT : (UNITS >= 32 ? UNITS : (B < 32 ? B : 32));
     static constexpr int MINB = T >= 256 ? HECNN_KS_MINB : 1;
 };
