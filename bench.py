@@ -451,8 +451,9 @@ def run_ours(args):
                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
         del x, y, xe, ye
         eng.trim()  # hand C4's cached arena back before the larger C2/C5 runs
-        mb = microbench(hb, local) if not args.no_micro else None
-        c5 = c5_extrapolated(hb, local, stream=stream.cuda_stream) if not args.no_c5 else None
+        # single-GPU reference figures: at N > 1 the other ranks would idle at the final barrier
+        mb = microbench(hb, local) if world == 1 and not args.no_micro else None
+        c5 = c5_extrapolated(hb, local, stream=stream.cuda_stream) if world == 1 and not args.no_c5 else None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle import ref
