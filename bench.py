@@ -88,6 +88,23 @@ def layer_work(hb, spec):
     return out
 
 
+def crop_extrapolation_check(hb, eng, full_ms, crop=8):
+    """Validates the C5 crop method on C4, where the full set also runs: the
+    C4 stack on a crop x crop x 3 input, each layer's CUDA-event time scaled
+    by the same layer_work ratios, against the measured full 32x32 step."""
+    spec = c4_spec(hb, crop)
+    model = eng.model(spec)
+    x = eng.encrypt_tensor(np.random.default_rng(3).uniform(0, 1, size=(eng.params.n // 2, spec.input.positions())),
+                           seed=11, shape=spec.input)
+    hb.forward_encrypted(model, x, eng, seed=13)
+    secs = []
+    hb.forward_encrypted(model, x, eng, seed=13, layer_seconds=secs)
+    wc, wf = layer_work(hb, spec), layer_work(hb, c4_spec(hb, 32))
+    est = sum(s * (a / b if b else 1.0) for s, a, b in zip(secs, wf, wc))
+    return {"crop": f"{crop}x{crop}x3", "extrapolated_ms": est * 1e3, "measured_ms": full_ms,
+            "ratio": est * 1e3 / full_ms}
+
+
 def c5_extrapolated(hb, device, crop=8, stream=None):
     """C5 (AlexNet-like COWC, alexnet32_preset layers, large-n16384-d24, 8192
     images per set): the full stack runs on the GPU on a crop x crop x 3 input
@@ -450,10 +467,13 @@ def run_ours(args):
                        "gb_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0}
                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
         del x, y, xe, ye
+        xcheck = crop_extrapolation_check(hb, eng, dev_s / args.steps * 1e3) if world == 1 and not args.no_c5 else None
         eng.trim()  # hand C4's cached arena back before the larger C2/C5 runs
         # single-GPU reference figures: at N > 1 the other ranks would idle at the final barrier
         mb = microbench(hb, local) if world == 1 and not args.no_micro else None
         c5 = c5_extrapolated(hb, local, stream=stream.cuda_stream) if world == 1 and not args.no_c5 else None
+        if c5 is not None:
+            c5["method_check_on_c4"] = xcheck
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle import ref

@@ -184,15 +184,18 @@ __device__ __forceinline__ double column_value_fp(const u32* __restrict__ dig, c
 // Per digit t: lift -> forward NTT (shared rounds) -> in the last butterfly
 // round each thread multiplies its outputs by (b_t, a_t) and accumulates;
 // accumulator positions are the thread's last-round positions, identical for
-// every t. A = IntArith (u64 Shoup, evk + evk_sh) or FpArith (exact FP64,
-// evk_f = e as doubles). The block's twiddles are staged once in shared memory
-// as a block-local table TL[2^s + m] = tw[2^(s+C) + b 2^s + m] and reused by
-// all D digit transforms (round code indexes it with b = c = 0).
+// every t. The last round's units are EL consecutive words (its stride is 1),
+// so the MAC runs once per unit with 16-byte evk loads (KeyAt::unit) instead
+// of one 8-byte load per word. A = IntArith (u64 Shoup, evk + evk_sh) or
+// FpArith (exact FP64, evk_f = e as doubles). The block's twiddles are staged
+// once in shared memory as a block-local table TL[2^s + m] =
+// tw[2^(s+C) + b 2^s + m] and reused by all D digit transforms (round code
+// indexes it with b = c = 0).
 // FP64 path (all limbs but the 60-bit q0): the c1 accumulator lives in the
-// shared-memory space the integer path needs for its 16-byte twiddles
-// (thread-private swizzled slots, no barriers), and the registers this frees
-// hold the next digit's first-round inputs, loaded while the current digit
-// is transformed.
+// shared-memory space the integer path needs for its 16-byte twiddles, in a
+// thread-private [slot][thread] layout (no barriers, no bank conflicts), and
+// the registers this frees hold the next digit's first-round inputs, loaded
+// while the current digit is transformed.
 template <int LOGN, int LOGB, int LOGE, int T, class A, class KeyAt>
 __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typename A::TW* tw, const u32* digits,
                                         KeyAt key, u64* acc01, int level, int D, long long ct, int i, int b, u64 q,
@@ -204,7 +207,10 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     constexpr int B = 1 << LOGB, C = LOGN - LOGB;
     constexpr int SL = ntt::last_round_start(LOGB, LOGE);
     constexpr int RL = LOGB - SL, EL = 1 << RL, UL = B >> RL, PL = (UL + T - 1) / T;
-    constexpr int GL = B >> SL, STRL = GL >> RL;
+    static_assert(EL % 2 == 0, "last round units must hold an even number of words");
+    // c1 accumulator slots: thread-private [slot][thread] when every thread
+    // owns PL whole units (fits the B-word region), else at swizzled positions
+    constexpr bool PRIV = UL % T == 0;
     // first round (S0 = 0): unit u owns positions u + k * STR0, k < E0
     constexpr int R0 = ntt::round_size(LOGB, LOGE, 0), E0 = 1 << R0, U0 = B >> R0, P0 = (U0 + T - 1) / T;
     constexpr int STR0 = U0;
@@ -215,6 +221,10 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
 
     TW* stw = reinterpret_cast<TW*>(smem + B);
     double* sacc = reinterpret_cast<double*>(smem + 2 * B);  // FP path: c1 accumulators
+    auto slot = [&](int idx, int uu, int k) -> int {
+        if constexpr (PRIV) { (void)idx; return (uu * EL + k) * T + threadIdx.x; }
+        else { (void)uu; (void)k; return ntt::swz(idx); }
+    };
     for (int j = threadIdx.x + 1; j < B; j += T) {
         const int s = 31 - __clz(j), m = j - (1 << s);
         stw[j] = tw[(1 << (s + C)) + (b << s) + m];
@@ -263,12 +273,19 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                 return column_value<LOGN, C>(dig, itw, q, r, b);
             }
         };
+        V stash[EL];
         ntt::fwd_block<LOGB, LOGE, T>(reinterpret_cast<V*>(smem), ar, stw, 0, 0, first,
                                       [&](int idx, V v, int uu, int k) {
-                                          if constexpr (FP) {
-                                              key(t, blk_off + idx, v, a0[uu * EL + k], sacc[ntt::swz(idx)]);
-                                          } else {
-                                              key(t, blk_off + idx, v, a0[uu * EL + k], a1[uu * EL + k]);
+                                          stash[k] = v;
+                                          if (k == EL - 1) {
+                                              const int base = idx - (EL - 1);
+                                              if constexpr (FP) {
+                                                  key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
+                                                                        [&](int kk) -> double& { return sacc[slot(base + kk, uu, kk)]; });
+                                              } else {
+                                                  key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
+                                                                        [&](int kk) -> u64& { return a1[uu * EL + kk]; });
+                                              }
                                           }
                                       });
         __syncthreads();  // the next digit's first round overwrites shared memory
@@ -285,43 +302,107 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         if constexpr (FP) return ntt::fcanon(ntt::fmodmul(ntt::to_fp(a), ntt::to_fp(c), ar.q, ar.qinv), ar.q, ar.qinv);
         else return mul_mod(a, c, mc);
     };
+    // each unit's EL words are contiguous: 16-byte loads and stores
 #pragma unroll
     for (int uu = 0; uu < PL; ++uu) {
         const int u = threadIdx.x + uu * T;
         if (UL % T != 0 && u >= UL) break;
-        const int base = (u / STRL) * GL + (u % STRL);
+        const int base = u * EL;
 #pragma unroll
-        for (int k = 0; k < EL; ++k) {
-            const int idx = base + k * STRL;
-            u64 r0, r1;
-            if constexpr (FP) {
-                r0 = ntt::fcanon(a0[uu * EL + k], ar.q, ar.qinv);
-                r1 = ntt::fcanon(sacc[ntt::swz(idx)], ar.q, ar.qinv);
-            } else {
-                r0 = reduce_2q(a0[uu * EL + k], q);
-                r1 = reduce_2q(a1[uu * EL + k], q);
-            }
-            u64 b0, b1;
-            if (mode == 0) {  // acc01 already holds (d0, d1)
-                b0 = o0[idx];
-                b1 = o1[idx];
-            } else {  // acc01 holds NTT(x); mode 1: d = x^2, mode 2: d = x * y
-                const u64 x0 = o0[idx], x1 = o1[idx];
-                if (mode == 1) {
-                    b0 = mulq(x0, x0);
-                    const u64 c = mulq(x0, x1);
-                    b1 = add_mod(c, c, q);
+        for (int k = 0; k < EL; k += 2) {
+            const int idx = base + k;
+            u64 r0[2], r1[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if constexpr (FP) {
+                    r0[h] = ntt::fcanon(a0[uu * EL + k + h], ar.q, ar.qinv);
+                    r1[h] = ntt::fcanon(sacc[slot(idx + h, uu, k + h)], ar.q, ar.qinv);
                 } else {
-                    const u64 v0 = y0[idx], v1 = y1[idx];
-                    b0 = mulq(x0, v0);
-                    b1 = add_mod(mulq(x0, v1), mulq(x1, v0), q);
+                    r0[h] = reduce_2q(a0[uu * EL + k + h], q);
+                    r1[h] = reduce_2q(a1[uu * EL + k + h], q);
                 }
             }
-            o0[idx] = add_mod(b0, r0, q);
-            o1[idx] = add_mod(b1, r1, q);
+            const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(o0 + idx);
+            const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(o1 + idx);
+            u64 b0[2], b1[2];
+            const u64 xa[2] = {x0.x, x0.y}, xb[2] = {x1.x, x1.y};
+            if (mode == 0) {  // acc01 already holds (d0, d1)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) b0[h] = xa[h], b1[h] = xb[h];
+            } else if (mode == 1) {  // acc01 holds NTT(x): d = x^2
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    b0[h] = mulq(xa[h], xa[h]);
+                    const u64 c = mulq(xa[h], xb[h]);
+                    b1[h] = add_mod(c, c, q);
+                }
+            } else {  // d = x * y
+                const ulonglong2 v0 = *reinterpret_cast<const ulonglong2*>(y0 + idx);
+                const ulonglong2 v1 = *reinterpret_cast<const ulonglong2*>(y1 + idx);
+                const u64 va[2] = {v0.x, v0.y}, vb[2] = {v1.x, v1.y};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    b0[h] = mulq(xa[h], va[h]);
+                    b1[h] = add_mod(mulq(xa[h], vb[h]), mulq(xb[h], va[h]), q);
+                }
+            }
+            *reinterpret_cast<ulonglong2*>(o0 + idx) = make_ulonglong2(add_mod(b0[0], r0[0], q), add_mod(b0[1], r0[1], q));
+            *reinterpret_cast<ulonglong2*>(o1 + idx) = make_ulonglong2(add_mod(b1[0], r1[0], q), add_mod(b1[1], r1[1], q));
         }
     }
 }
+
+// Unit-wise evk MACs: EL consecutive NTT outputs v[] at key positions
+// pos..pos+EL-1 of digit t, 16-byte loads of the key words.
+struct FpKey {
+    const double* evk_f;
+    long long key_stride, ioff;
+    double q, qinv;
+    template <int EL, class S1>
+    __device__ __forceinline__ void unit(int t, long long pos, const double* v, double* s0, S1 s1) const {
+        const double2* kb = reinterpret_cast<const double2*>(evk_f + (2LL * t) * key_stride + ioff + pos);
+        const double2* ka = reinterpret_cast<const double2*>(evk_f + (2LL * t + 1) * key_stride + ioff + pos);
+        double2 wb[EL / 2], wa[EL / 2];
+#pragma unroll
+        for (int k = 0; k < EL / 2; ++k) wb[k] = __ldg(kb + k), wa[k] = __ldg(ka + k);
+#pragma unroll
+        for (int k = 0; k < EL / 2; ++k) {
+            // |s| < D q < 2^48: exact sums
+            s0[2 * k] += ntt::fmodmul(v[2 * k], wb[k].x, q, qinv);
+            s0[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], wb[k].y, q, qinv);
+            s1(2 * k) += ntt::fmodmul(v[2 * k], wa[k].x, q, qinv);
+            s1(2 * k + 1) += ntt::fmodmul(v[2 * k + 1], wa[k].y, q, qinv);
+        }
+    }
+};
+
+struct IntKey {
+    const u64 *evk, *evk_sh;
+    long long key_stride, ioff;
+    u64 q, two_q;
+    template <int EL, class S1>
+    __device__ __forceinline__ void unit(int t, long long pos, const u64* v, u64* s0, S1 s1) const {
+        const long long kb = (2LL * t) * key_stride + ioff + pos, ka = kb + key_stride;
+        const ulonglong2* b = reinterpret_cast<const ulonglong2*>(evk + kb);
+        const ulonglong2* bs = reinterpret_cast<const ulonglong2*>(evk_sh + kb);
+        const ulonglong2* a = reinterpret_cast<const ulonglong2*>(evk + ka);
+        const ulonglong2* as = reinterpret_cast<const ulonglong2*>(evk_sh + ka);
+#pragma unroll
+        for (int k = 0; k < EL / 2; ++k) {
+            const ulonglong2 wb = __ldg(b + k), wbs = __ldg(bs + k), wa = __ldg(a + k), was = __ldg(as + k);
+            const u64 kbv[2] = {wb.x, wb.y}, kbs[2] = {wbs.x, wbs.y}, kav[2] = {wa.x, wa.y}, kas[2] = {was.x, was.y};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int e = 2 * k + h;
+                const u64 x0 = s0[e] + mul_shoup_lazy(v[e], kbv[h], kbs[h], q);
+                u64& r1 = s1(e);
+                const u64 x1 = r1 + mul_shoup_lazy(v[e], kav[h], kas[h], q);
+                s0[e] = x0 >= two_q ? x0 - two_q : x0;
+                r1 = x1 >= two_q ? x1 - two_q : x1;
+            }
+        }
+    }
+};
 
 // blockIdx.x = (ct * nsel + i - limb0) * nblocks + b over limbs [limb0, limb0 + nsel). FPK: this instantiation serves
 // the FP64 limbs (q < 2^42) and skips the others, or the reverse, so each
@@ -344,23 +425,11 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
     if (ntt::fp_limb(q) != FPK) return;
     if constexpr (FPK) {
         const ntt::FpArith ar{static_cast<double>(q), R.inv_q[i]};
-        auto key = [=](int t, long long pos, double v, double& s0, double& s1) {
-            const double kb = evk_f[(2LL * t) * key_stride + ioff + pos];
-            const double ka = evk_f[(2LL * t + 1) * key_stride + ioff + pos];
-            s0 += ntt::fmodmul(v, kb, ar.q, ar.qinv);  // |s| < D q < 2^48: exact sums
-            s1 += ntt::fmodmul(v, ka, ar.q, ar.qinv);
-        };
+        const FpKey key{evk_f, key_stride, ioff, ar.q, ar.qinv};
         ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd_f + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
     } else {
         const ntt::IntArith ar{q, q << 1};
-        const u64 two_q = q << 1;
-        auto key = [=](int t, long long pos, u64 v, u64& s0, u64& s1) {
-            const long long kb = (2LL * t) * key_stride + ioff + pos, ka = kb + key_stride;
-            const u64 x0 = s0 + mul_shoup_lazy(v, evk[kb], evk_sh[kb], q);
-            const u64 x1 = s1 + mul_shoup_lazy(v, evk[ka], evk_sh[ka], q);
-            s0 = x0 >= two_q ? x0 - two_q : x0;
-            s1 = x1 >= two_q ? x1 - two_q : x1;
-        };
+        const IntKey key{evk, evk_sh, key_stride, ioff, q, q << 1};
         ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
     }
 }

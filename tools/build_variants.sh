@@ -6,6 +6,8 @@ declare -A V
 V[na]=""
 V[nb]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT_COL=256 -DHECNN_KS_MINB=2"
 V[nc]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT_COL=512 -DHECNN_KS_MINB=2"
+V[e4]="-DHECNN_KS_LOGE=4"
+V[b12e4]="-DHECNN_KS_LOGB=12 -DHECNN_KS_LOGE=4 -DHECNN_KS_MAXT_COL=256 -DHECNN_KS_MINB=2"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
