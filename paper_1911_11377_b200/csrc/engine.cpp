@@ -322,8 +322,10 @@ Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, doubl
     dev.n = static_cast<int>(ring.n);
     dev.logn = static_cast<int>(ring.logn);
     dev.limbs = static_cast<int>(ring.limbs);
-    for (std::size_t i = 0; i < ring.limbs; ++i)
+    for (std::size_t i = 0; i < ring.limbs; ++i) {
         if (ring.primes[i] >= (1ull << 42)) dev.int_limbs |= (i < 64 ? 1ull << i : 0ull);
+        if (ring.primes[i] <= (1ull << 20)) dev.small_primes = true;
+    }
     if (ring.limbs > 64) throw std::invalid_argument("modulus chains longer than 64 limbs are not supported");
     dev.crt_words = static_cast<int>(ring.crt_words);
     sync();

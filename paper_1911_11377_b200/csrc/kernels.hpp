@@ -32,6 +32,7 @@ struct DevRing {
     const double* inv_f = nullptr;           // [limbs][n]
     const double* n_inv_f = nullptr;         // [limbs]
     unsigned long long int_limbs = 0;        // bit i: q_i >= 2^42 (integer-pipe path), for i < 64
+    bool small_primes = false;               // some q_i <= 2^20: key-switch digits need v mod q_i
 };
 
 // Optional per-kernel timing: CUDA events recorded on the launching stream

@@ -150,13 +150,13 @@ __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const u
 // The same column stages on the FP64 pipe (limbs with q < 2^42): values stay
 // below (C + 1) q < 2^45 in magnitude, so fmodmul stays exact without
 // corrections; the block's first round continues from these doubles.
-template <int LOGN, int C>
+template <int LOGN, int C, bool LIFT>
 __device__ __forceinline__ double column_value_fp(const u32* __restrict__ dig, const double* __restrict__ tw, u64 q,
                                                   double qd, double qinv, int r, int b) {
     constexpr int E = 1 << C, B = 1 << (LOGN - C);
     double x[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = ntt::to_fp(lift_digit(dig[r + k * B], q));
+    for (int k = 0; k < E; ++k) x[k] = ntt::to_fp(LIFT ? lift_digit(dig[r + k * B], q) : dig[r + k * B]);
 #pragma unroll
     for (int rho = 0; rho < C; ++rho) {
         const int half = E >> (rho + 1);
@@ -196,7 +196,9 @@ __device__ __forceinline__ double column_value_fp(const u32* __restrict__ dig, c
 // thread-private [slot][thread] layout (no barriers, no bank conflicts), and
 // the registers this frees hold the next digit's first-round inputs, loaded
 // while the current digit is transformed.
-template <int LOGN, int LOGB, int LOGE, int T, class A, class KeyAt>
+// LIFT: some prime of the chain is <= 2^20, so digits need v mod q_i
+// (ckks.hpp:622); otherwise every digit is already a residue.
+template <int LOGN, int LOGB, int LOGE, int T, bool LIFT, class A, class KeyAt>
 __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typename A::TW* tw, const u32* digits,
                                         KeyAt key, u64* acc01, int level, int D, long long ct, int i, int b, u64 q,
                                         int mode, const u64* fy) {
@@ -255,20 +257,18 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     };
     prefetch(0);
 
+    auto lift = [&](u32 v) -> u64 {
+        if constexpr (LIFT) return lift_digit(v, q);
+        else return v;
+    };
     for (int t = 0; t < D; ++t) {
         const u32* dig = digits + (ct * D + t) * n;
-        u32 cur[PREFETCH ? P0 * E0 : 1];
-        if constexpr (PREFETCH) {
-#pragma unroll
-            for (int k = 0; k < P0 * E0; ++k) cur[k] = pf[k];
-            if (t + 1 < D) prefetch(t + 1);  // lands while digit t is transformed
-        }
         auto first = [&](int r, int uu, int k) -> V {
             if constexpr (PREFETCH) {
                 (void)r;
-                return ntt::to_fp(lift_digit(cur[uu * E0 + k], q));
+                return ntt::to_fp(lift(pf[uu * E0 + k]));
             } else if constexpr (FP) {
-                return column_value_fp<LOGN, C>(dig, R.fwd_f + (static_cast<long long>(i) << LOGN), q, ar.q, ar.qinv, r, b);
+                return column_value_fp<LOGN, C, LIFT>(dig, R.fwd_f + (static_cast<long long>(i) << LOGN), q, ar.q, ar.qinv, r, b);
             } else {
                 return column_value<LOGN, C>(dig, itw, q, r, b);
             }
@@ -287,6 +287,11 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                                                                         [&](int kk) -> u64& { return a1[uu * EL + kk]; });
                                               }
                                           }
+                                      },
+                                      [&] {
+                                          // the first round has consumed pf: the next digit's
+                                          // inputs land while this one is transformed
+                                          if (t + 1 < D) prefetch(t + 1);
                                       });
         __syncthreads();  // the next digit's first round overwrites shared memory
     }
@@ -407,7 +412,7 @@ struct IntKey {
 // blockIdx.x = (ct * nsel + i - limb0) * nblocks + b over limbs [limb0, limb0 + nsel). FPK: this instantiation serves
 // the FP64 limbs (q < 2^42) and skips the others, or the reverse, so each
 // path gets its own register allocation; the host launches both.
-template <int LOGN, int LOGB, int LOGE, int T, int MINB, bool FPK>
+template <int LOGN, int LOGB, int LOGE, int T, int MINB, bool FPK, bool LIFT>
 __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
                                                  const u64* __restrict__ evk_sh, const double* __restrict__ evk_f,
                                                  u64* __restrict__ acc01, int level, int D, int limb0, int nsel,
@@ -426,11 +431,12 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
     if constexpr (FPK) {
         const ntt::FpArith ar{static_cast<double>(q), R.inv_q[i]};
         const FpKey key{evk_f, key_stride, ioff, ar.q, ar.qinv};
-        ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd_f + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
+        ks_body<LOGN, LOGB, LOGE, T, LIFT>(R, ar, R.fwd_f + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
     } else {
+        // primes >= 2^42 only: digits < 2^20 < q are residues already
         const ntt::IntArith ar{q, q << 1};
         const IntKey key{evk, evk_sh, key_stride, ioff, q, q << 1};
-        ks_body<LOGN, LOGB, LOGE, T>(R, ar, R.fwd + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
+        ks_body<LOGN, LOGB, LOGE, T, false>(R, ar, R.fwd + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
     }
 }
 
@@ -467,14 +473,24 @@ template <int LOGN>
 void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
                    u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy) {
     using P = KsPlan<LOGN>;
-    auto kfp = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true>;
-    auto kint = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false>;
+#ifdef HECNN_KS_FORCE_LIFT
+    const bool lift = true;
+#else
+    const bool lift = R.small_primes;
+#endif
+    auto kfp = lift ? k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, true>
+                              : k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, false>;
+    auto kint = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false, false>;
     // data + staged twiddles (u64 Shoup pairs on the integer path; double
     // twiddles + c1 accumulators on the FP64 path)
     const int smem = P::B * (8 + 16);
-    static bool init = (smem > 48 * 1024 ? (cudaFuncSetAttribute(kfp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                                           cudaFuncSetAttribute(kint, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true)
-                                        : true);
+    static bool init = (smem > 48 * 1024
+                            ? (cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, true>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                               cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, false>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                               cudaFuncSetAttribute(kint, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true)
+                            : true);
     (void)init;
     const int limbs = level + 1;
     const unsigned long long lmask = limbs >= 64 ? ~0ull : (1ull << limbs) - 1;

@@ -170,19 +170,27 @@ __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __r
     }
 }
 
+struct NoHook {
+    __device__ void operator()() const {}
+};
+
 // All forward rounds of a block: first round loads with `first`, last round
-// stores with `last`, the rest go through shared memory `s`.
-template <int LOGB, int LOGE, int T, class A, int S0 = 0, class First, class Last>
+// stores with `last`, the rest go through shared memory `s`. `after_first`
+// runs once the first round's inputs are consumed (e.g. to start loading the
+// next transform's inputs into the same registers).
+template <int LOGB, int LOGE, int T, class A, int S0 = 0, class First, class Last, class Hook = NoHook>
 __device__ __forceinline__ void fwd_block(typename A::V* s, const A& ar, const typename A::TW* tw, int b, int c,
-                                          First first, Last last) {
+                                          First first, Last last, Hook after_first = Hook{}) {
     using V = typename A::V;
     if constexpr (S0 < LOGB) {
         constexpr int R = round_size(LOGB, LOGE, S0);
         constexpr bool is_first = S0 == 0, is_last = S0 + R >= LOGB;
         if constexpr (is_first && is_last) {
             fwd_round<LOGB, R, S0, T>(ar, tw, b, c, first, last);
+            after_first();
         } else if constexpr (is_first) {
             fwd_round<LOGB, R, S0, T>(ar, tw, b, c, first, SmemStore<V>{s});
+            after_first();
             __syncthreads();
         } else if constexpr (is_last) {
             fwd_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, last);
@@ -190,7 +198,7 @@ __device__ __forceinline__ void fwd_block(typename A::V* s, const A& ar, const t
             fwd_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, SmemStore<V>{s});
             __syncthreads();
         }
-        fwd_block<LOGB, LOGE, T, A, S0 + R>(s, ar, tw, b, c, first, last);
+        fwd_block<LOGB, LOGE, T, A, S0 + R>(s, ar, tw, b, c, first, last, after_first);
     }
 }
 
