@@ -56,6 +56,14 @@ __device__ __forceinline__ u64 reduce128(u64 lo, u64 hi, const ModConst& m) {
     return rem >= m.q ? rem - m.q : rem;
 }
 
+// v mod q for a v that is almost always below 2q (a residue of a neighbouring
+// chain prime): one conditional subtraction, Barrett only when v >= 2q.
+__device__ __forceinline__ u64 reduce_near(u64 v, const ModConst& m) {
+    u64 r = v >= m.q ? v - m.q : v;
+    if (r >= m.q) r = reduce128(v, 0, m);
+    return r;
+}
+
 __device__ __forceinline__ u64 mul_mod(u64 a, u64 b, const ModConst& m) {
     return reduce128(a * b, mulhi(a, b), m);
 }

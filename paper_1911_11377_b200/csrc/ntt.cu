@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_sel(DevRing R, u64* _
         if constexpr (RESCALE) {
             const ModConst m = R.mod[limb];
             const u64 vt = top[i];
-            u64 centred = vt < m.q ? vt : reduce128(vt, 0, m);
+            u64 centred = reduce_near(vt, m);
             if (vt > (R.mod[L].q >> 1)) centred = sub_mod(centred, R.p_mod[L * R.limbs + limb], m.q);
             const ulonglong2 inv = R.inv_dropped[L * R.limbs + limb];
             o[i] = mul_shoup(sub_mod(c, centred, m.q), inv.x, inv.y, m.q);

@@ -135,12 +135,52 @@ struct SmemStore {
 
 // Forward round: block-local stages S0..S0+R-1; global stage = c + local;
 // `b` is the block index inside the N-point transform (twiddle offset).
+#ifndef HECNN_NTT_BATCH
+#define HECNN_NTT_BATCH 0
+#endif
 template <int LOGB, int R, int S0, int T, class A, class Load, class Store>
 __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __restrict__ tw, int b, int c, Load load,
                                           Store store) {
     using V = typename A::V;
     constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R;
     constexpr int PER = (UNITS + T - 1) / T;
+    if constexpr (HECNN_NTT_BATCH && PER > 1 && UNITS % T == 0 && PER * E <= 16 &&
+                  std::is_same<Store, SmemStore<V>>::value) {
+        // all of the thread's units loaded first, butterflies interleaved
+        // across units (2x the independent chains), then stored in order
+        V x[PER][E];
+#pragma unroll
+        for (int uu = 0; uu < PER; ++uu) {
+            const int u = threadIdx.x + uu * T;
+            const int base = (u / STRIDE) * G + u % STRIDE;
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                if constexpr (std::is_invocable_v<Load, int, int, int>) x[uu][k] = load(base + k * STRIDE, uu, k);
+                else x[uu][k] = load(base + k * STRIDE);
+            }
+        }
+#pragma unroll
+        for (int rho = 0; rho < R; ++rho) {
+            const int half = E >> (rho + 1);
+#pragma unroll
+            for (int blk = 0; blk < (1 << rho); ++blk) {
+#pragma unroll
+                for (int uu = 0; uu < PER; ++uu) {
+                    const int grp = (threadIdx.x + uu * T) / STRIDE;
+                    const typename A::TW w = tw[(1 << (c + S0 + rho)) + (b << (S0 + rho)) + (grp << rho) + blk];
+#pragma unroll
+                    for (int kk = 0; kk < half; ++kk) ar.ct(x[uu][blk * 2 * half + kk], x[uu][blk * 2 * half + kk + half], w);
+                }
+            }
+        }
+#pragma unroll
+        for (int uu = 0; uu < PER; ++uu) {
+            const int u = threadIdx.x + uu * T;
+            const int base = (u / STRIDE) * G + u % STRIDE;
+#pragma unroll
+            for (int k = 0; k < E; ++k) store(base + k * STRIDE, x[uu][k], uu, k);
+        }
+    } else {
 #pragma unroll
     for (int uu = 0; uu < PER; ++uu) {
         const int u = threadIdx.x + uu * T;
@@ -167,6 +207,7 @@ __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __r
         }
 #pragma unroll
         for (int k = 0; k < E; ++k) store(base + k * STRIDE, x[k], uu, k);
+    }
     }
 }
 

@@ -63,19 +63,42 @@ __global__ void k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict
     u64 v = src[static_cast<long long>(level) * R.n + j];
     if constexpr (SCALED) v = mul_shoup(v, c[level].x, c[level].y, p);
     const bool upper = v > (p >> 1);
+    // FP64 limbs (q_i < 2^42) when the dropped residue is an exact double:
+    // centre(v) mod q_i = fcentre(v) - [upper] (p mod q_i), any representative
+    // (the result is canonicalised once at the end)
+    const bool v_fp = v < (1ull << 51);
+    const double vf = v_fp ? ntt::to_fp(v) : 0.0;
     for (int i = 0; i < level; ++i) {
         const ModConst m = R.mod[i];
-        u64 centred = v < m.q ? v : reduce128(v, 0, m);
-        if (upper) centred = sub_mod(centred, R.p_mod[level * R.limbs + i], m.q);
         const ulonglong2 inv = R.inv_dropped[level * R.limbs + i];
-        u64 a = src[static_cast<long long>(i) * R.n + j];
-        if constexpr (SCALED) a = mul_shoup(a, c[i].x, c[i].y, m.q);
-        u64 r = mul_shoup(sub_mod(a, centred, m.q), inv.x, inv.y, m.q);
-        if constexpr (ADD) {
+        const u64 a = src[static_cast<long long>(i) * R.n + j];
+        u64 r;
+        if (v_fp && ntt::fp_limb(m.q)) {
+            const double q = static_cast<double>(m.q), qinv = R.inv_q[i];
+            double cen = ntt::fcentre(vf, q, qinv);
+            if (upper) cen -= ntt::to_fp(R.p_mod[level * R.limbs + i]);
+            double x = ntt::to_fp(a);
+            if constexpr (SCALED) x = ntt::fmodmul(x, ntt::to_fp(c[i].x), q, qinv);
+            double y = ntt::fmodmul(x - cen, ntt::to_fp(inv.x), q, qinv);
+            if constexpr (ADD) {
 #pragma unroll
-            for (int k = 0; k < kMaxTerms; ++k)
-                if (k < t.count) r = add_mod(r, __ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j), m.q);
-            if (t.c0 && j == 0 && (poly & 1) == 0) r = add_mod(r, t.c0[i], m.q);
+                for (int k = 0; k < kMaxTerms; ++k)
+                    if (k < t.count) y += ntt::to_fp(__ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j));
+                if (t.c0 && j == 0 && (poly & 1) == 0) y += ntt::to_fp(t.c0[i]);
+            }
+            r = ntt::fcanon(y, q, qinv);
+        } else {
+            u64 centred = reduce_near(v, m);
+            if (upper) centred = sub_mod(centred, R.p_mod[level * R.limbs + i], m.q);
+            u64 x = a;
+            if constexpr (SCALED) x = mul_shoup(x, c[i].x, c[i].y, m.q);
+            r = mul_shoup(sub_mod(x, centred, m.q), inv.x, inv.y, m.q);
+            if constexpr (ADD) {
+#pragma unroll
+                for (int k = 0; k < kMaxTerms; ++k)
+                    if (k < t.count) r = add_mod(r, __ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j), m.q);
+                if (t.c0 && j == 0 && (poly & 1) == 0) r = add_mod(r, t.c0[i], m.q);
+            }
         }
         dst[static_cast<long long>(i) * R.n + j] = r;
     }

@@ -7,7 +7,7 @@ V[na]=""
 V[nb]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT_COL=256 -DHECNN_KS_MINB=2"
 V[nc]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT_COL=512 -DHECNN_KS_MINB=2"
 V[e4]="-DHECNN_KS_LOGE=4"
-V[lift]="-DHECNN_KS_FORCE_LIFT"
+V[batch]="-DHECNN_NTT_BATCH=1"
 V[b12e4]="-DHECNN_KS_LOGB=12 -DHECNN_KS_LOGE=4 -DHECNN_KS_MAXT_COL=256 -DHECNN_KS_MINB=2"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
