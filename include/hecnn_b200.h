@@ -188,6 +188,32 @@ int hecnn_ct_add_const(hecnn_context* ctx, const hecnn_tensor* x, double c, hecn
 int hecnn_eval_activation(hecnn_context* ctx, const double* coefficients, size_t n_coefficients,
                           double interval_bound, const hecnn_tensor* x, hecnn_tensor** out);
 
+/* ---- wire format: CKKS blob v1 (ckks_serialize.hpp:3-152) ----------------
+ * Blobs are byte-identical to the reference's save_* output, so keys and
+ * ciphertexts move between the CPU reference and this engine as files.
+ * Save functions write into `buf` (`cap` bytes) and set *len to the blob
+ * size; buf == NULL only queries the size. Load functions require the blob's
+ * parameters to equal the context's (same_params, :145-148). Errors carry the
+ * reference's texts ("ckks blob: bad magic", "ckks blob: wrong object kind",
+ * "io: unexpected end of file", ... -> HECNN_ERUNTIME). */
+enum { HECNN_BLOB_SECRET_KEY = 1, HECNN_BLOB_PUBLIC_KEY = 2, HECNN_BLOB_EVAL_KEY = 3, HECNN_BLOB_CIPHERTEXT = 4 };
+/* read_header (:41-58) without a context: the kind is read from the blob;
+ * primes (capacity *nprimes, may be NULL) and *nprimes = chain length */
+int hecnn_blob_params(const uint8_t* blob, size_t len, int* kind, size_t* n, uint64_t* primes, size_t* nprimes,
+                      double* scale, double* sigma, int* degenerate);
+/* save_secret_key / save_public_key / save_evaluation_key (:79-114) of the
+ * context's keys, kind = HECNN_BLOB_*_KEY */
+int hecnn_blob_save_key(const hecnn_context* ctx, int kind, uint8_t* buf, size_t cap, size_t* len);
+/* load_*_key (:84-122) into the context (any of the three kinds, by `kind`) */
+int hecnn_blob_load_key(hecnn_context* ctx, int kind, const uint8_t* blob, size_t len);
+/* save_ciphertext (:124-130) of cell `cell` of a tensor */
+int hecnn_blob_save_ciphertext(hecnn_context* ctx, const hecnn_tensor* t, size_t cell, uint8_t* buf, size_t cap,
+                               size_t* len);
+/* load_ciphertext (:133-141) of `count` blobs into one tensor of `count`
+ * cells (TensorEncrypted's uniform level and scale, tensor.hpp:52-62) */
+int hecnn_blob_load_ciphertexts(hecnn_context* ctx, const uint8_t* const* blobs, const size_t* lens, size_t count,
+                                hecnn_tensor** out);
+
 /* ---- network tier ------------------------------------------------------- */
 enum {
     HECNN_LAYER_CONV2D = 0,

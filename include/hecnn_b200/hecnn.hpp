@@ -14,6 +14,9 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstring>
+#include <istream>
+#include <ostream>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -287,6 +290,135 @@ private:
     CkksParams par_;
     hecnn_context* ctx_ = nullptr;
 };
+
+// ---- ckks_serialize.hpp (CKKS blob v1) -----------------------------------------
+// Same byte layout as the reference and as the device codec behind
+// hecnn_blob_* (include/hecnn_b200.h): blobs written here load in the
+// reference and vice versa.
+enum class BlobKind : std::uint16_t { SecretKey = 1, PublicKey = 2, EvaluationKey = 3, Ciphertext = 4 };
+
+namespace b200_detail {
+template <class T>
+void put(std::ostream& os, T v) {
+    char b[sizeof(T)];
+    std::memcpy(b, &v, sizeof(T));
+    os.write(b, sizeof(T));
+}
+template <class T>
+T get(std::istream& is) {
+    char b[sizeof(T)];
+    is.read(b, sizeof(T));
+    if (is.gcount() != static_cast<std::streamsize>(sizeof(T))) throw std::runtime_error("io: unexpected end of file");
+    T v;
+    std::memcpy(&v, b, sizeof(T));
+    return v;
+}
+inline void put_header(std::ostream& os, BlobKind kind, const CkksParams& p) {
+    os.write("CKKS", 4);
+    put<std::uint16_t>(os, 1);
+    put<std::uint16_t>(os, static_cast<std::uint16_t>(kind));
+    put<std::uint32_t>(os, static_cast<std::uint32_t>(p.ring.n));
+    put<std::uint16_t>(os, static_cast<std::uint16_t>(p.ring.primes.size()));
+    for (u64 q : p.ring.primes) put<u64>(os, q);
+    put<double>(os, p.scale);
+    put<double>(os, p.sigma);
+    put<std::uint8_t>(os, p.degenerate_noise ? 1 : 0);
+}
+inline CkksParams get_header(std::istream& is, BlobKind want) {
+    char magic[4];
+    is.read(magic, 4);
+    if (is.gcount() != 4) throw std::runtime_error("io: unexpected end of file");
+    if (std::memcmp(magic, "CKKS", 4) != 0) throw std::runtime_error("ckks blob: bad magic");
+    if (get<std::uint16_t>(is) != 1) throw std::runtime_error("ckks blob: unsupported version");
+    if (get<std::uint16_t>(is) != static_cast<std::uint16_t>(want)) throw std::runtime_error("ckks blob: wrong object kind");
+    CkksParams p;
+    p.ring.n = get<std::uint32_t>(is);
+    p.ring.primes.resize(get<std::uint16_t>(is));
+    for (u64& q : p.ring.primes) q = get<u64>(is);
+    p.scale = get<double>(is);
+    p.sigma = get<double>(is);
+    p.degenerate_noise = get<std::uint8_t>(is) != 0;
+    return p;
+}
+inline void put_poly(std::ostream& os, const RingPoly& r) {
+    put<std::uint16_t>(os, static_cast<std::uint16_t>(r.level));
+    put<std::uint8_t>(os, static_cast<std::uint8_t>(r.rep));
+    for (const auto& row : r.rns) os.write(reinterpret_cast<const char*>(row.data()), static_cast<std::streamsize>(row.size() * 8));
+}
+inline RingPoly get_poly(std::istream& is, std::size_t n) {
+    RingPoly r;
+    r.level = get<std::uint16_t>(is);
+    r.rep = static_cast<Rep>(get<std::uint8_t>(is));
+    r.rns.assign(r.level + 1, std::vector<u64>(n));
+    for (auto& row : r.rns) {
+        is.read(reinterpret_cast<char*>(row.data()), static_cast<std::streamsize>(n * 8));
+        if (is.gcount() != static_cast<std::streamsize>(n * 8)) throw std::runtime_error("io: unexpected end of file");
+    }
+    return r;
+}
+}  // namespace b200_detail
+
+inline void save_secret_key(std::ostream& os, const CkksParams& p, const SecretKey& sk) {
+    b200_detail::put_header(os, BlobKind::SecretKey, p);
+    b200_detail::put_poly(os, sk.s);
+}
+inline std::pair<CkksParams, SecretKey> load_secret_key(std::istream& is) {
+    CkksParams p = b200_detail::get_header(is, BlobKind::SecretKey);
+    SecretKey sk{b200_detail::get_poly(is, p.ring.n)};
+    return {std::move(p), std::move(sk)};
+}
+inline void save_public_key(std::ostream& os, const CkksParams& p, const PublicKey& pk) {
+    b200_detail::put_header(os, BlobKind::PublicKey, p);
+    b200_detail::put_poly(os, pk.b);
+    b200_detail::put_poly(os, pk.a);
+}
+inline std::pair<CkksParams, PublicKey> load_public_key(std::istream& is) {
+    CkksParams p = b200_detail::get_header(is, BlobKind::PublicKey);
+    PublicKey pk;
+    pk.b = b200_detail::get_poly(is, p.ring.n);
+    pk.a = b200_detail::get_poly(is, p.ring.n);
+    return {std::move(p), std::move(pk)};
+}
+inline void save_evaluation_key(std::ostream& os, const CkksParams& p, const EvaluationKey& evk) {
+    b200_detail::put_header(os, BlobKind::EvaluationKey, p);
+    b200_detail::put<std::uint16_t>(os, static_cast<std::uint16_t>(evk.base_bits));
+    b200_detail::put<std::uint16_t>(os, static_cast<std::uint16_t>(evk.pairs.size()));
+    for (const auto& pr : evk.pairs) {
+        b200_detail::put_poly(os, pr.first);
+        b200_detail::put_poly(os, pr.second);
+    }
+}
+inline std::pair<CkksParams, EvaluationKey> load_evaluation_key(std::istream& is) {
+    CkksParams p = b200_detail::get_header(is, BlobKind::EvaluationKey);
+    EvaluationKey evk;
+    evk.base_bits = b200_detail::get<std::uint16_t>(is);
+    const std::size_t count = b200_detail::get<std::uint16_t>(is);
+    for (std::size_t t = 0; t < count; ++t) {
+        RingPoly b = b200_detail::get_poly(is, p.ring.n);
+        evk.pairs.emplace_back(std::move(b), b200_detail::get_poly(is, p.ring.n));
+    }
+    return {std::move(p), std::move(evk)};
+}
+inline void save_ciphertext(std::ostream& os, const CkksParams& p, const Ciphertext& ct) {
+    b200_detail::put_header(os, BlobKind::Ciphertext, p);
+    b200_detail::put<double>(os, ct.scale);
+    b200_detail::put<std::uint16_t>(os, static_cast<std::uint16_t>(ct.level));
+    b200_detail::put_poly(os, ct.c0);
+    b200_detail::put_poly(os, ct.c1);
+}
+inline std::pair<CkksParams, Ciphertext> load_ciphertext(std::istream& is) {
+    CkksParams p = b200_detail::get_header(is, BlobKind::Ciphertext);
+    Ciphertext ct;
+    ct.scale = b200_detail::get<double>(is);
+    ct.level = b200_detail::get<std::uint16_t>(is);
+    ct.c0 = b200_detail::get_poly(is, p.ring.n);
+    ct.c1 = b200_detail::get_poly(is, p.ring.n);
+    return {std::move(p), std::move(ct)};
+}
+inline bool same_params(const CkksParams& a, const CkksParams& b) {
+    return a.ring.n == b.ring.n && a.ring.primes == b.ring.primes && a.scale == b.scale && a.sigma == b.sigma &&
+           a.degenerate_noise == b.degenerate_noise;
+}
 
 // ---- presets.hpp (built-ins, presets.hpp:33-49) ------------------------------------
 inline CkksParams preset_params(const std::string& name, bool degenerate_noise = false) {

@@ -136,6 +136,37 @@ class RefEngine:
         lib().ref_export_keys(self.keys, _p(s), _p(b), _p(a), _p(evk))
         return s, b, a, evk
 
+    # ---- ckks_serialize.hpp (blob v1), the reference's own writer/reader
+    def save_key(self, kind: int) -> bytes:
+        """save_secret_key / save_public_key / save_evaluation_key (kind 1/2/3)."""
+        n = ctypes.c_size_t()
+        _check(lib().ref_save_key(self.h, self.keys, int(kind), None, ctypes.c_size_t(0), ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        _check(lib().ref_save_key(self.h, self.keys, int(kind), buf, n, ctypes.byref(n)))
+        return buf.raw[:n.value]
+
+    def save_ciphertext(self, ct: np.ndarray, level: int, scale: float) -> bytes:
+        ct = np.ascontiguousarray(ct, dtype=np.uint64)
+        n = ctypes.c_size_t()
+        args = (self.h, _p(ct), ctypes.c_size_t(level), ctypes.c_double(scale))
+        _check(lib().ref_save_ciphertext(*args, None, ctypes.c_size_t(0), ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        _check(lib().ref_save_ciphertext(*args, buf, n, ctypes.byref(n)))
+        return buf.raw[:n.value]
+
+    def load_ciphertext(self, blob: bytes):
+        """load_ciphertext: (words [2][level+1][n], level, scale)."""
+        out = np.empty(2 * (self.top + 1) * self.n, dtype=np.uint64)
+        lv, sc = ctypes.c_uint32(), ctypes.c_double()
+        _check(lib().ref_load_ciphertext(blob, ctypes.c_size_t(len(blob)), _p(out), ctypes.c_size_t(out.size),
+                                         ctypes.byref(lv), ctypes.byref(sc)))
+        return out[:2 * (lv.value + 1) * self.n].reshape(2, lv.value + 1, self.n), lv.value, sc.value
+
+    @staticmethod
+    def load_key_check(blob: bytes, kind: int):
+        """Runs the reference's load_*_key; raises its error for a rejected blob."""
+        _check(lib().ref_load_key_check(blob, ctypes.c_size_t(len(blob)), int(kind)))
+
     def encrypt(self, slots, seed: int, scale: Optional[float] = None) -> np.ndarray:
         v = np.ascontiguousarray(slots, dtype=np.float64)
         out = np.empty((2, self.top + 1, self.n), dtype=np.uint64)

@@ -13,6 +13,9 @@
 #include <memory>
 #include <string>
 
+#include <sstream>
+
+#include "hecnn/ckks_serialize.hpp"
 #include "hecnn/layers.hpp"
 #include "hecnn/model_io.hpp"
 #include "hecnn/presets.hpp"
@@ -485,6 +488,66 @@ int ref_time_mul(void* e, void* k, size_t level, size_t count, unsigned threads,
             for (std::size_t i = b; i < en; ++i) out[i] = eng.mul(xs[i], ys[i], ks->eval);
         });
         *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+// ---- ckks_serialize.hpp (blob v1): the reference's own save_* / load_*
+// Writes the blob into `buf` (cap bytes); *len = blob size (buf may be null
+// to query it).
+static int blob_out(const std::string& b, uint8_t* buf, size_t cap, size_t* len) {
+    *len = b.size();
+    if (buf) {
+        if (cap < b.size()) throw std::invalid_argument("ref: blob buffer too small");
+        std::memcpy(buf, b.data(), b.size());
+    }
+    return 0;
+}
+
+// kind 1 secret, 2 public, 3 evaluation (BlobKind, ckks_serialize.hpp:17-22)
+int ref_save_key(void* e, void* k, int kind, uint8_t* buf, size_t cap, size_t* len) {
+    return guard([&] {
+        const CkksEngine& eng = static_cast<RefEngine*>(e)->eng;
+        KeySet* ks = static_cast<KeySet*>(k);
+        std::ostringstream os;
+        if (kind == 1) save_secret_key(os, eng.params(), ks->secret);
+        else if (kind == 2) save_public_key(os, eng.params(), ks->public_key);
+        else save_evaluation_key(os, eng.params(), ks->eval);
+        blob_out(os.str(), buf, cap, len);
+    });
+}
+
+int ref_save_ciphertext(void* e, const uint64_t* ct, size_t level, double scale, uint8_t* buf, size_t cap, size_t* len) {
+    return guard([&] {
+        const CkksEngine& eng = static_cast<RefEngine*>(e)->eng;
+        std::ostringstream os;
+        save_ciphertext(os, eng.params(), ct_from(eng, ct, level, scale));
+        blob_out(os.str(), buf, cap, len);
+    });
+}
+
+// load_ciphertext (ckks_serialize.hpp:133-141): words [2][level+1][n] out
+int ref_load_ciphertext(const uint8_t* blob, size_t len, uint64_t* out, size_t cap_words, uint32_t* level,
+                        double* scale) {
+    return guard([&] {
+        std::istringstream is(std::string(reinterpret_cast<const char*>(blob), len));
+        auto [p, ct] = load_ciphertext(is);
+        const std::size_t n = p.ring.n, words = 2 * (ct.level + 1) * n;
+        if (cap_words < words) throw std::invalid_argument("ref: output too small");
+        poly_to(ct.c0, out);
+        poly_to(ct.c1, out + (ct.level + 1) * n);
+        *level = ct.level;
+        *scale = ct.scale;
+    });
+}
+
+// load_secret_key / load_public_key / load_evaluation_key by kind; returns
+// the error text of a rejected blob through ref_last_error()
+int ref_load_key_check(const uint8_t* blob, size_t len, int kind) {
+    return guard([&] {
+        std::istringstream is(std::string(reinterpret_cast<const char*>(blob), len));
+        if (kind == 1) (void)load_secret_key(is);
+        else if (kind == 2) (void)load_public_key(is);
+        else (void)load_evaluation_key(is);
     });
 }
 

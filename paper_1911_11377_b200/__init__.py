@@ -47,6 +47,8 @@ EXPORTED_SYMBOLS = (
     "hecnn_profile_enable", "hecnn_profile_reset", "hecnn_profile_read", "hecnn_modmul_peak",
     "hecnn_tensor_copy_to_device", "hecnn_host_encode_real", "hecnn_host_decode_real",
     "hecnn_host_encryption_randomness", "hecnn_fp64_modmul_peak", "hecnn_context_trim",
+    "hecnn_blob_params", "hecnn_blob_save_key", "hecnn_blob_load_key", "hecnn_blob_save_ciphertext",
+    "hecnn_blob_load_ciphertexts",
 )
 
 _lib = None
@@ -126,6 +128,11 @@ _SIGNATURES = {
     "hecnn_model_destroy": [_V],
     "hecnn_model_depth_cost": [_V, _PSZ],
     "hecnn_forward_encrypted": [_V, _V, _V, _U64, _PV, _PD],
+    "hecnn_blob_params": [_V, _SZ, ctypes.POINTER(ctypes.c_int), _PSZ, _V, _PSZ, _PD, _PD, ctypes.POINTER(ctypes.c_int)],
+    "hecnn_blob_save_key": [_V, _I, _V, _SZ, _PSZ],
+    "hecnn_blob_load_key": [_V, _I, _V, _SZ],
+    "hecnn_blob_save_ciphertext": [_V, _V, _SZ, _V, _SZ, _PSZ],
+    "hecnn_blob_load_ciphertexts": [_V, _PV, _PSZ, _SZ, _PV],
 }
 
 
@@ -932,3 +939,83 @@ def forward_encrypted(model, x: EncryptedTensor, eng: CkksEngine, seed: int = 1,
     if layer_seconds is not None:
         layer_seconds[:] = list(secs[:nl])
     return EncryptedTensor(eng, h)
+
+
+# ---------------------------------------------------------------- wire format
+# CKKS blob v1 (ckks_serialize.hpp): byte-identical to the reference's
+# save_* output; the native codec decodes straight into device tensors/keys.
+
+BLOB_SECRET_KEY, BLOB_PUBLIC_KEY, BLOB_EVAL_KEY, BLOB_CIPHERTEXT = 1, 2, 3, 4
+
+
+def _blob_call(fn, *args) -> bytes:
+    size = ctypes.c_size_t()
+    _check(fn(*args, None, ctypes.c_size_t(0), ctypes.byref(size)))
+    buf = ctypes.create_string_buffer(size.value)
+    _check(fn(*args, buf, ctypes.c_size_t(size.value), ctypes.byref(size)))
+    return buf.raw[:size.value]
+
+
+def blob_params(blob: bytes):
+    """read_header (ckks_serialize.hpp:41-58): (kind, CkksParams) of a blob."""
+    kind, n, cnt = ctypes.c_int(), ctypes.c_size_t(), ctypes.c_size_t(0)
+    scale, sigma, deg = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    _check(lib().hecnn_blob_params(blob, len(blob), ctypes.byref(kind), ctypes.byref(n), None, ctypes.byref(cnt),
+                                   ctypes.byref(scale), ctypes.byref(sigma), ctypes.byref(deg)))
+    primes = np.empty(cnt.value, dtype=np.uint64)
+    _check(lib().hecnn_blob_params(blob, len(blob), None, None, _ptr(primes), ctypes.byref(cnt), None, None, None))
+    return kind.value, CkksParams(n.value, [int(q) for q in primes], scale.value, sigma.value, bool(deg.value))
+
+
+def save_secret_key(eng: "CkksEngine") -> bytes:
+    """save_secret_key (ckks_serialize.hpp:79-82) of the engine's secret key."""
+    return _blob_call(lib().hecnn_blob_save_key, eng.ctx, BLOB_SECRET_KEY)
+
+
+def save_public_key(eng: "CkksEngine") -> bytes:
+    """save_public_key (ckks_serialize.hpp:90-94)."""
+    return _blob_call(lib().hecnn_blob_save_key, eng.ctx, BLOB_PUBLIC_KEY)
+
+
+def save_evaluation_key(eng: "CkksEngine") -> bytes:
+    """save_evaluation_key (ckks_serialize.hpp:104-112)."""
+    return _blob_call(lib().hecnn_blob_save_key, eng.ctx, BLOB_EVAL_KEY)
+
+
+def load_key(eng: "CkksEngine", kind: int, blob: bytes) -> "CkksEngine":
+    """load_secret_key / load_public_key / load_evaluation_key into the engine
+    (the blob's parameters must equal the engine's)."""
+    _check(lib().hecnn_blob_load_key(eng.ctx, int(kind), blob, len(blob)))
+    return eng
+
+
+def load_secret_key(eng: "CkksEngine", blob: bytes) -> "CkksEngine":
+    return load_key(eng, BLOB_SECRET_KEY, blob)
+
+
+def load_public_key(eng: "CkksEngine", blob: bytes) -> "CkksEngine":
+    return load_key(eng, BLOB_PUBLIC_KEY, blob)
+
+
+def load_evaluation_key(eng: "CkksEngine", blob: bytes) -> "CkksEngine":
+    return load_key(eng, BLOB_EVAL_KEY, blob)
+
+
+def save_ciphertext(eng: "CkksEngine", t: EncryptedTensor, cell: int = 0) -> bytes:
+    """save_ciphertext (ckks_serialize.hpp:124-130) of one cell of a tensor."""
+    return _blob_call(lib().hecnn_blob_save_ciphertext, eng.ctx, t.handle, ctypes.c_size_t(cell))
+
+
+def load_ciphertexts(eng: "CkksEngine", blobs) -> EncryptedTensor:
+    """load_ciphertext (ckks_serialize.hpp:133-141) of each blob, as the cells
+    of one device tensor (shared level and scale, tensor.hpp:52-62)."""
+    blobs = [bytes(b) for b in blobs]
+    ptrs = (ctypes.c_void_p * len(blobs))(*[ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p) for b in blobs])
+    lens = (ctypes.c_size_t * len(blobs))(*[len(b) for b in blobs])
+    h = ctypes.c_void_p()
+    _check(lib().hecnn_blob_load_ciphertexts(eng.ctx, ptrs, lens, ctypes.c_size_t(len(blobs)), ctypes.byref(h)))
+    return eng._wrap(h)
+
+
+def load_ciphertext(eng: "CkksEngine", blob: bytes) -> EncryptedTensor:
+    return load_ciphertexts(eng, [blob])

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 
+#include "blob.hpp"
 #include "engine.hpp"
 #include "hecnn_b200.h"
 
@@ -542,6 +543,172 @@ int hecnn_forward_encrypted(hecnn_context* ctx, const hecnn_model* m, const hecn
                             hecnn_tensor** out, double* layer_seconds) {
     return guard([&] {
         *out = wrap(ctx, forward_encrypted(C(ctx), const_cast<hecnn_model*>(m)->m, T(x), seed, layer_seconds));
+    });
+}
+
+
+// ---------------------------------------------------------------- CKKS blob v1
+
+namespace {
+
+blob::Params ctx_params(const Context& c) {
+    blob::Params p;
+    p.n = c.n();
+    p.primes = c.ring.primes;
+    p.scale = c.scale;
+    p.sigma = c.sigma;
+    p.degenerate = c.degenerate;
+    return p;
+}
+
+void emit(const std::vector<uint8_t>& b, uint8_t* buf, size_t cap, size_t* len) {
+    if (!len) throw std::invalid_argument("blob: null length pointer");
+    *len = b.size();
+    if (!buf) return;
+    if (cap < b.size()) throw std::invalid_argument("blob: buffer too small");
+    std::memcpy(buf, b.data(), b.size());
+}
+
+void require_same(const blob::Params& p, const Context& c) {
+    if (!blob::same(p, ctx_params(c))) throw std::invalid_argument("ckks blob: parameters differ from the context");
+}
+
+}  // namespace
+
+int hecnn_blob_params(const uint8_t* blob, size_t len, int* kind, size_t* n, uint64_t* primes, size_t* nprimes,
+                      double* scale, double* sigma, int* degenerate) {
+    return guard([&] {
+        uint16_t k = 0;  // peeked so the header check accepts any kind; a short blob fails in the reader
+        if (blob && len >= 8) std::memcpy(&k, blob + 6, 2);
+        blob::Reader r(blob, len);
+        const blob::Params p = r.header(static_cast<blob::Kind>(k));
+        if (kind) *kind = k;
+        if (n) *n = p.n;
+        if (nprimes) {
+            if (primes && *nprimes < p.primes.size()) throw std::invalid_argument("blob: primes buffer too small");
+            if (primes) std::memcpy(primes, p.primes.data(), p.primes.size() * 8);
+            *nprimes = p.primes.size();
+        }
+        if (scale) *scale = p.scale;
+        if (sigma) *sigma = p.sigma;
+        if (degenerate) *degenerate = p.degenerate ? 1 : 0;
+    });
+}
+
+int hecnn_blob_save_key(const hecnn_context* ctx, int kind, uint8_t* buf, size_t cap, size_t* len) {
+    return guard([&] {
+        Context& c = *const_cast<hecnn_context*>(ctx)->ctx;
+        const std::size_t L = c.top(), n = c.n(), poly = (L + 1) * n;
+        blob::Writer w;
+        if (kind == HECNN_BLOB_SECRET_KEY) {
+            if (!c.has_secret) throw std::invalid_argument("no secret key");
+            w.header(blob::kSecret, ctx_params(c));
+            w.poly(static_cast<uint16_t>(L), 0, c.secret_host.data(), n);  // Coeff
+        } else if (kind == HECNN_BLOB_PUBLIC_KEY) {
+            if (!c.has_pk) throw std::invalid_argument("no public key");
+            std::vector<u64> ba(2 * poly);
+            c.download(ba.data(), c.pk.get(), 2 * poly * 8);
+            w.header(blob::kPublic, ctx_params(c));
+            w.poly(static_cast<uint16_t>(L), 1, ba.data(), n);  // b, NTT
+            w.poly(static_cast<uint16_t>(L), 1, ba.data() + poly, n);
+        } else if (kind == HECNN_BLOB_EVAL_KEY) {
+            if (!c.evk_digits) throw std::invalid_argument("no evaluation key");
+            std::vector<u64> evk(c.evk_digits * 2 * poly);
+            c.download(evk.data(), c.evk.get(), evk.size() * 8);
+            w.header(blob::kEval, ctx_params(c));
+            w.le<uint16_t>(20);  // base_bits (kRelinBaseBits)
+            w.le<uint16_t>(static_cast<uint16_t>(c.evk_digits));
+            for (std::size_t t = 0; t < 2 * c.evk_digits; ++t) w.poly(static_cast<uint16_t>(L), 1, evk.data() + t * poly, n);
+        } else {
+            throw std::invalid_argument("blob: unknown key kind");
+        }
+        emit(w.bytes(), buf, cap, len);
+    });
+}
+
+int hecnn_blob_load_key(hecnn_context* ctx, int kind, const uint8_t* data, size_t len) {
+    return guard([&] {
+        Context& c = C(ctx);
+        const std::size_t L = c.top(), n = c.n(), poly = (L + 1) * n;
+        if (kind < HECNN_BLOB_SECRET_KEY || kind > HECNN_BLOB_EVAL_KEY) throw std::invalid_argument("blob: unknown key kind");
+        blob::Reader r(data, len);
+        require_same(r.header(static_cast<blob::Kind>(kind)), c);
+        auto top_poly = [&](u64* dst, uint8_t want_rep, const char* what) {
+            const auto [level, rep] = r.poly(dst, n, poly);
+            if (level != L || rep != want_rep)
+                throw std::invalid_argument(std::string("ckks blob: ") + what + " must be a top-level " +
+                                            (want_rep ? "NTT" : "coefficient") + "-domain polynomial");
+        };
+        if (kind == HECNN_BLOB_SECRET_KEY) {
+            std::vector<u64> s(poly);
+            top_poly(s.data(), 0, "secret key");
+            import_keys(c, s.data(), nullptr, nullptr, nullptr, 0);
+        } else if (kind == HECNN_BLOB_PUBLIC_KEY) {
+            std::vector<u64> b(poly), a(poly);
+            top_poly(b.data(), 1, "public key");
+            top_poly(a.data(), 1, "public key");
+            import_keys(c, nullptr, b.data(), a.data(), nullptr, 0);
+        } else {
+            if (r.le<uint16_t>() != 20) throw std::invalid_argument("mul: unexpected evk digit base");
+            const std::size_t D = r.le<uint16_t>();
+            std::vector<u64> evk(D * 2 * poly);
+            for (std::size_t t = 0; t < 2 * D; ++t) top_poly(evk.data() + t * poly, 1, "evaluation key");
+            import_keys(c, nullptr, nullptr, nullptr, evk.data(), D);
+        }
+    });
+}
+
+int hecnn_blob_save_ciphertext(hecnn_context* ctx, const hecnn_tensor* t, size_t cell, uint8_t* buf, size_t cap,
+                               size_t* len) {
+    return guard([&] {
+        Context& c = C(ctx);
+        const Tensor& x = T(t);
+        if (cell >= x.cells) throw std::invalid_argument("blob: cell index out of range");
+        const std::size_t n = c.n(), rows = (x.level + 1) * n;
+        std::vector<u64> words(2 * rows);
+        c.download(words.data(), x.cell(cell), words.size() * 8);
+        blob::Writer w;
+        w.header(blob::kCipher, ctx_params(c));
+        w.le<double>(x.scale);
+        w.le<uint16_t>(static_cast<uint16_t>(x.level));
+        w.poly(static_cast<uint16_t>(x.level), 0, words.data(), n);  // c0, Coeff
+        w.poly(static_cast<uint16_t>(x.level), 0, words.data() + rows, n);
+        emit(w.bytes(), buf, cap, len);
+    });
+}
+
+int hecnn_blob_load_ciphertexts(hecnn_context* ctx, const uint8_t* const* blobs, const size_t* lens, size_t count,
+                                hecnn_tensor** out) {
+    return guard([&] {
+        Context& c = C(ctx);
+        if (!count) throw std::invalid_argument("blob: no ciphertexts");
+        const std::size_t n = c.n(), cap = (c.top() + 1) * n;
+        std::vector<u64> host;
+        uint32_t level = 0;
+        double scale = 0.0;
+        for (std::size_t k = 0; k < count; ++k) {
+            blob::Reader r(blobs[k], lens[k]);
+            require_same(r.header(blob::kCipher), c);
+            const double s = r.le<double>();
+            const uint32_t l = r.le<uint16_t>();
+            if (l > c.top()) throw std::invalid_argument("ckks blob: ciphertext level exceeds the context's chain");
+            if (k == 0) {
+                level = l, scale = s;
+                host.resize(count * 2 * (level + 1) * n);
+            } else if (l != level || s != scale) {
+                // TensorEncrypted keeps one (scale, level) for all cells (tensor.hpp:52-62)
+                throw std::invalid_argument("blob: ciphertexts of one tensor must share level and scale");
+            }
+            u64* dst = host.data() + k * 2 * (level + 1) * n;
+            for (int comp = 0; comp < 2; ++comp) {
+                const auto [pl, rep] = r.poly(dst + comp * (level + 1) * n, n, cap);
+                if (pl != level || rep != 0)
+                    throw std::invalid_argument("ckks blob: ciphertext polynomials must be coefficient-domain at the ciphertext level");
+            }
+        }
+        TensorPtr t = make_tensor(c, count, level, scale);
+        c.upload(t->data(), host.data(), host.size() * 8);
+        *out = wrap(ctx, std::move(t));
     });
 }
 

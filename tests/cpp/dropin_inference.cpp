@@ -51,6 +51,12 @@ int main(int argc, char** argv) {
     for (const auto* poly : {&o.c0, &o.c1})
         for (const auto& row : poly->rns) of.write(reinterpret_cast<const char*>(row.data()), row.size() * 8);
     of.write(reinterpret_cast<const char*>(logits.data.data()), logits.data.size() * 8);
+    // ckks_serialize.hpp: the logits ciphertext and the evaluation key as blobs
+    if (argc >= 4) {
+        std::ofstream bf(argv[3], std::ios::binary);
+        save_ciphertext(bf, params, o);
+        save_evaluation_key(bf, params, keys.eval);
+    }
     for (std::size_t i = 0; i < logits.batch; ++i) std::printf("image %zu logit %.8f\n", i, logits.at(i, 0));
     std::printf("layers: %zu timed\n", secs.size());
     return 0;

@@ -27,7 +27,7 @@ def test_cpp_dropin_matches_reference(ref, tmp_path):
     for arr in (spec.weights[0], spec.biases[0], spec.weights[3], spec.biases[3], imgs.reshape(-1)):
         blob += np.uint64(arr.size).tobytes() + np.ascontiguousarray(arr, np.float64).tobytes()
     (tmp_path / "in.bin").write_bytes(blob)
-    out = subprocess.run([str(exe), str(tmp_path / "in.bin"), str(tmp_path / "out.bin")], check=True,
+    out = subprocess.run([str(exe), str(tmp_path / "in.bin"), str(tmp_path / "out.bin"), str(tmp_path / "blobs.bin")], check=True,
                          capture_output=True, text=True).stdout
     assert "image 3 logit" in out
     raw = (tmp_path / "out.bin").read_bytes()
@@ -46,3 +46,7 @@ def test_cpp_dropin_matches_reference(ref, tmp_path):
     assert np.array_equal(r.decrypt_tensor(y, 4)[:, 0], logits)
     plain = ref.forward_plain(spec, imgs)[:, 0]
     assert np.max(np.abs(logits - plain)) < 1e-2
+    # ckks_serialize.hpp through the drop-in: byte-identical to the reference's blobs
+    blobs = (tmp_path / "blobs.bin").read_bytes()
+    ct_blob = r.save_ciphertext(y.words()[0], level, scale)
+    assert blobs == ct_blob + r.save_key(3)
