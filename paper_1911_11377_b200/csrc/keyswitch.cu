@@ -213,6 +213,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     // c1 accumulator slots: thread-private [slot][thread] when every thread
     // owns PL whole units (fits the B-word region), else at swizzled positions
     constexpr bool PRIV = UL % T == 0;
+    static_assert(!ntt::Split<LOGB, LOGE, T>::on || UL % T == 0, "split blocks own whole last-round units");
     // first round (S0 = 0): unit u owns positions u + k * STR0, k < E0
     constexpr int R0 = ntt::round_size(LOGB, LOGE, 0), E0 = 1 << R0, U0 = B >> R0, P0 = (U0 + T - 1) / T;
     constexpr int STR0 = U0;
@@ -280,8 +281,18 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                                           if (k == EL - 1) {
                                               const int base = idx - (EL - 1);
                                               if constexpr (FP) {
+#if defined(HECNN_KS_ABLATE_MAC)
+                                                  // ablation: NTT only (outputs summed, no key, no c1)
+#pragma unroll
+                                                  for (int kk = 0; kk < EL; ++kk) a0[uu * EL + kk] += stash[kk];
+#elif defined(HECNN_KS_ABLATE_SACC)
+                                                  // ablation: key MAC, c1 folded into the c0 registers
+                                                  key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
+                                                                        [&](int kk) -> double& { return a0[uu * EL + kk]; });
+#else
                                                   key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
                                                                         [&](int kk) -> double& { return sacc[slot(base + kk, uu, kk)]; });
+#endif
                                               } else {
                                                   key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
                                                                         [&](int kk) -> u64& { return a1[uu * EL + kk]; });
@@ -312,7 +323,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     for (int uu = 0; uu < PL; ++uu) {
         const int u = threadIdx.x + uu * T;
         if (UL % T != 0 && u >= UL) break;
-        const int base = u * EL;
+        const int base = ntt::fwd_last_base<LOGB, LOGE, T>(uu);
 #pragma unroll
         for (int k = 0; k < EL; k += 2) {
             const int idx = base + k;

@@ -140,7 +140,7 @@ struct SmemStore {
 #endif
 template <int LOGB, int R, int S0, int T, class A, class Load, class Store>
 __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __restrict__ tw, int b, int c, Load load,
-                                          Store store) {
+                                          Store store, int tid) {
     using V = typename A::V;
     constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R;
     constexpr int PER = (UNITS + T - 1) / T;
@@ -151,7 +151,7 @@ __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __r
         V x[PER][E];
 #pragma unroll
         for (int uu = 0; uu < PER; ++uu) {
-            const int u = threadIdx.x + uu * T;
+            const int u = tid + uu * T;
             const int base = (u / STRIDE) * G + u % STRIDE;
 #pragma unroll
             for (int k = 0; k < E; ++k) {
@@ -166,7 +166,7 @@ __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __r
             for (int blk = 0; blk < (1 << rho); ++blk) {
 #pragma unroll
                 for (int uu = 0; uu < PER; ++uu) {
-                    const int grp = (threadIdx.x + uu * T) / STRIDE;
+                    const int grp = (tid + uu * T) / STRIDE;
                     const typename A::TW w = tw[(1 << (c + S0 + rho)) + (b << (S0 + rho)) + (grp << rho) + blk];
 #pragma unroll
                     for (int kk = 0; kk < half; ++kk) ar.ct(x[uu][blk * 2 * half + kk], x[uu][blk * 2 * half + kk + half], w);
@@ -175,7 +175,7 @@ __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __r
         }
 #pragma unroll
         for (int uu = 0; uu < PER; ++uu) {
-            const int u = threadIdx.x + uu * T;
+            const int u = tid + uu * T;
             const int base = (u / STRIDE) * G + u % STRIDE;
 #pragma unroll
             for (int k = 0; k < E; ++k) store(base + k * STRIDE, x[uu][k], uu, k);
@@ -183,7 +183,7 @@ __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __r
     } else {
 #pragma unroll
     for (int uu = 0; uu < PER; ++uu) {
-        const int u = threadIdx.x + uu * T;
+        const int u = tid + uu * T;
         if (UNITS % T != 0 && u >= UNITS) break;
         const int grp = u / STRIDE, col = u % STRIDE;
         const int base = grp * G + col;
@@ -215,44 +215,99 @@ struct NoHook {
     __device__ void operator()() const {}
 };
 
+#ifndef HECNN_NTT_SPLIT
+#define HECNN_NTT_SPLIT 1
+#endif
+// Group split: after the first forward round (stages 0..R0-1) the block falls
+// apart into NG = 2^R0 independent sub-blocks of B >> R0 words, so the later
+// rounds of sub-block g run on its own TG = T / NG threads (whole warps) and
+// synchronise with a named barrier over those warps instead of the whole CTA
+// (the inverse mirrors it: local rounds first, the global round last). Warps
+// drift apart between the two CTA-wide barriers, so one warp group's shared
+// memory traffic overlaps another's FP64 butterflies.
+template <int LOGB, int LOGE, int T>
+struct Split {
+    static constexpr int R0 = round_size(LOGB, LOGE, 0);
+    static constexpr int NG = 1 << R0, TG = T / NG, LB = LOGB - R0;
+    static constexpr bool on = HECNN_NTT_SPLIT && R0 < LOGB && LB >= 8 && NG > 1 && NG <= 15 && T % NG == 0 &&
+                               TG % 32 == 0;
+};
+
+__device__ __forceinline__ void group_sync(int g, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(nthreads) : "memory");
+}
+
+// The rounds of one (sub-)block after its first: loads from `s`, the last
+// round stores with `last`; `sync` separates rounds.
+template <int LOGB, int LOGE, int T, class A, int S0, class Last, class Sync>
+__device__ __forceinline__ void fwd_rest(typename A::V* s, const A& ar, const typename A::TW* tw, int b, int c, Last last,
+                                         Sync sync, int tid) {
+    using V = typename A::V;
+    if constexpr (S0 < LOGB) {
+        constexpr int R = round_size(LOGB, LOGE, S0);
+        if constexpr (S0 + R >= LOGB) {
+            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, last, tid);
+        } else {
+            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, SmemStore<V>{s}, tid);
+            sync();
+            fwd_rest<LOGB, LOGE, T, A, S0 + R>(s, ar, tw, b, c, last, sync, tid);
+        }
+    }
+}
+
 // All forward rounds of a block: first round loads with `first`, last round
 // stores with `last`, the rest go through shared memory `s`. `after_first`
 // runs once the first round's inputs are consumed (e.g. to start loading the
 // next transform's inputs into the same registers).
-template <int LOGB, int LOGE, int T, class A, int S0 = 0, class First, class Last, class Hook = NoHook>
+template <int LOGB, int LOGE, int T, class A, class First, class Last, class Hook = NoHook>
 __device__ __forceinline__ void fwd_block(typename A::V* s, const A& ar, const typename A::TW* tw, int b, int c,
                                           First first, Last last, Hook after_first = Hook{}) {
     using V = typename A::V;
-    if constexpr (S0 < LOGB) {
-        constexpr int R = round_size(LOGB, LOGE, S0);
-        constexpr bool is_first = S0 == 0, is_last = S0 + R >= LOGB;
-        if constexpr (is_first && is_last) {
-            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, first, last);
-            after_first();
-        } else if constexpr (is_first) {
-            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, first, SmemStore<V>{s});
-            after_first();
-            __syncthreads();
-        } else if constexpr (is_last) {
-            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, last);
+    constexpr int R0 = round_size(LOGB, LOGE, 0);
+    if constexpr (R0 >= LOGB) {
+        fwd_round<LOGB, R0, 0, T>(ar, tw, b, c, first, last, threadIdx.x);
+        after_first();
+    } else {
+        fwd_round<LOGB, R0, 0, T>(ar, tw, b, c, first, SmemStore<V>{s}, threadIdx.x);
+        after_first();
+        __syncthreads();
+        using SP = Split<LOGB, LOGE, T>;
+        if constexpr (SP::on) {
+            const int g = threadIdx.x / SP::TG, lt = threadIdx.x % SP::TG;
+            constexpr int BL = 1 << SP::LB;
+            fwd_rest<SP::LB, LOGE, SP::TG, A, 0>(
+                s + g * BL, ar, tw, (b << R0) + g, c + R0,
+                [&](int i, V v, int uu, int k) { last(g * BL + i, v, uu, k); }, [g] { group_sync(g, SP::TG); }, lt);
         } else {
-            fwd_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, SmemStore<V>{s});
-            __syncthreads();
+            fwd_rest<LOGB, LOGE, T, A, R0>(s, ar, tw, b, c, last, [] { __syncthreads(); }, threadIdx.x);
         }
-        fwd_block<LOGB, LOGE, T, A, S0 + R>(s, ar, tw, b, c, first, last, after_first);
+    }
+}
+
+// Block position of the calling thread's unit slot `uu` in the last forward
+// round (whose units are runs of 2^RL consecutive words).
+template <int LOGB, int LOGE, int T>
+__device__ __forceinline__ int fwd_last_base(int uu) {
+    constexpr int RL = LOGB - last_round_start(LOGB, LOGE);
+    using SP = Split<LOGB, LOGE, T>;
+    if constexpr (SP::on && round_size(LOGB, LOGE, 0) < LOGB) {
+        const int g = threadIdx.x / SP::TG, lt = threadIdx.x % SP::TG;
+        return (g << SP::LB) + ((lt + uu * SP::TG) << RL);
+    } else {
+        return (static_cast<int>(threadIdx.x) + uu * T) << RL;
     }
 }
 
 // Inverse round: stages S0+R-1 down to S0.
 template <int LOGB, int R, int S0, int T, class A, class Load, class Store>
 __device__ __forceinline__ void inv_round(const A& ar, const typename A::TW* __restrict__ tw, int b, int c, Load load,
-                                          Store store) {
+                                          Store store, int tid) {
     using V = typename A::V;
     constexpr int B = 1 << LOGB, G = B >> S0, STRIDE = G >> R, E = 1 << R, UNITS = B >> R;
     constexpr int PER = (UNITS + T - 1) / T;
 #pragma unroll
     for (int uu = 0; uu < PER; ++uu) {
-        const int u = threadIdx.x + uu * T;
+        const int u = tid + uu * T;
         if (UNITS % T != 0 && u >= UNITS) break;
         const int grp = u / STRIDE, col = u % STRIDE;
         const int base = grp * G + col;
@@ -278,28 +333,51 @@ __device__ __forceinline__ void inv_round(const A& ar, const typename A::TW* __r
     }
 }
 
-// All inverse rounds: the forward decomposition traversed backwards; the
-// round with the highest S0 runs first and loads with `first`, the S0 = 0
-// round runs last and stores with `last`.
-template <int LOGB, int LOGE, int T, class A, int S0 = 0, class First, class Last>
-__device__ __forceinline__ void inv_block(typename A::V* s, const A& ar, const typename A::TW* tw, int b, int c,
-                                          First first, Last last) {
+// Inverse rounds S0 .. of a (sub-)block, highest S0 first; the round with the
+// highest S0 loads with `first`, the S0 = 0 round stores with `last` (or into
+// `s` when STORE_LAST is false, for a caller that continues the transform).
+template <int LOGB, int LOGE, int T, class A, int S0, class First, class Last, class Sync>
+__device__ __forceinline__ void inv_rest(typename A::V* s, const A& ar, const typename A::TW* tw, int b, int c,
+                                         First first, Last last, Sync sync, int tid) {
     using V = typename A::V;
     if constexpr (S0 < LOGB) {
         constexpr int R = round_size(LOGB, LOGE, S0);
         constexpr bool runs_first = S0 + R >= LOGB, runs_last = S0 == 0;
-        inv_block<LOGB, LOGE, T, A, S0 + R>(s, ar, tw, b, c, first, last);
+        inv_rest<LOGB, LOGE, T, A, S0 + R>(s, ar, tw, b, c, first, last, sync, tid);
         if constexpr (runs_first && runs_last) {
-            inv_round<LOGB, R, S0, T>(ar, tw, b, c, first, last);
+            inv_round<LOGB, R, S0, T>(ar, tw, b, c, first, last, tid);
         } else if constexpr (runs_first) {
-            inv_round<LOGB, R, S0, T>(ar, tw, b, c, first, SmemStore<V>{s});
-            __syncthreads();
+            inv_round<LOGB, R, S0, T>(ar, tw, b, c, first, SmemStore<V>{s}, tid);
+            sync();
         } else if constexpr (runs_last) {
-            inv_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, last);
+            inv_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, last, tid);
         } else {
-            inv_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, SmemStore<V>{s});
-            __syncthreads();
+            inv_round<LOGB, R, S0, T>(ar, tw, b, c, SmemLoad<V>{s}, SmemStore<V>{s}, tid);
+            sync();
         }
+    }
+}
+
+// All inverse rounds: the forward decomposition traversed backwards; the
+// round with the highest S0 runs first and loads with `first`, the S0 = 0
+// round runs last and stores with `last`. With the group split the rounds
+// above R0 run per sub-block (named barriers), then one CTA barrier, then the
+// global S0 = 0 round.
+template <int LOGB, int LOGE, int T, class A, class First, class Last>
+__device__ __forceinline__ void inv_block(typename A::V* s, const A& ar, const typename A::TW* tw, int b, int c,
+                                          First first, Last last) {
+    using V = typename A::V;
+    using SP = Split<LOGB, LOGE, T>;
+    if constexpr (SP::on) {
+        constexpr int R0 = SP::R0, BL = 1 << SP::LB;
+        const int g = threadIdx.x / SP::TG, lt = threadIdx.x % SP::TG;
+        inv_rest<SP::LB, LOGE, SP::TG, A, 0>(
+            s + g * BL, ar, tw, (b << R0) + g, c + R0, [&](int i) { return first(g * BL + i); }, SmemStore<V>{s + g * BL},
+            [g] { group_sync(g, SP::TG); }, lt);
+        __syncthreads();
+        inv_round<LOGB, R0, 0, T>(ar, tw, b, c, SmemLoad<V>{s}, last, threadIdx.x);
+    } else {
+        inv_rest<LOGB, LOGE, T, A, 0>(s, ar, tw, b, c, first, last, [] { __syncthreads(); }, threadIdx.x);
     }
 }
 

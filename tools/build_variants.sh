@@ -8,6 +8,9 @@ V[nb]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT_COL=256 -DHECNN_KS_MINB=2"
 V[nc]="-DHECNN_KS_LOGB=12 -DHECNN_KS_MAXT_COL=512 -DHECNN_KS_MINB=2"
 V[e4]="-DHECNN_KS_LOGE=4"
 V[batch]="-DHECNN_NTT_BATCH=1"
+V[nomac]="-DHECNN_KS_ABLATE_MAC"
+V[nosplit]="-DHECNN_NTT_SPLIT=0"
+V[nosacc]="-DHECNN_KS_ABLATE_SACC"
 V[b12e4]="-DHECNN_KS_LOGB=12 -DHECNN_KS_LOGE=4 -DHECNN_KS_MAXT_COL=256 -DHECNN_KS_MINB=2"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
