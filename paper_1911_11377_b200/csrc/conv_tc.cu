@@ -1,0 +1,340 @@
+// Plaintext-weight x ciphertext conv layers on the 5th-generation tensor
+// cores (tcgen05.mma kind::i8, accumulators in TMEM) for limbs with q < 2^40:
+// conv2d_encrypted (layers.hpp:174-211) -> mul_scalar_mac (ckks.hpp:448-465)
+// summed over the taps of every output pixel.
+//
+// Per (component, limb) row, pixel p and a block of 128 coefficients j:
+//   Y[j][oc] = sum_k X[k][j] W[k][oc] mod q,  X[k][j] = x[src(p, k)][comp][limb][j]
+// Both factors are residues below 2^40: X = sum_a 2^8a X_a, W = sum_b 2^8b W_b
+// (bytes), and Y = sum_s 2^8s D_s with D_s = sum_{a+b=s} X_a W_b (s = 0..8),
+// each D_s an exact int32 while K <= 6144 (<= 5 * 255^2 * K < 2^31).
+//
+// The byte-plane diagonals fold into the MMA addressing: the B operand is the
+// weight tile with all five byte planes side by side, N = 5 x 48 columns
+// (b, oc), and the MMA of ciphertext plane a writes TMEM columns starting at
+// a x 48, so column s x 48 + oc accumulates exactly sum_{a+b=s} X_a W_b: five
+// 128 x 240 x 32 MMAs per 32-tap step, 9 x 48 = 432 accumulator columns, no
+// wasted products. The epilogue reads D_s with tcgen05.ld and reduces
+// sum_s D_s (2^8s mod q) with the exact FP64 modmul (ntt_core.cuh).
+//
+// Roles: warps 0-7 gather the ciphertext words (thread t: coefficient row
+// j0 + t % 128, taps of K half t / 128; coalesced across the warp, the next
+// step's words in flight while the current step is converted), split them
+// into byte planes and write them with the weight tile into a STAGES-deep
+// shared-memory ring in the UMMA K-major no-swizzle layout (8 x 16-byte core
+// matrices), then run the epilogue of their TMEM lanes (channel half t / 128);
+// warp 8 owns TMEM and one elected thread issues the MMAs. mbarriers order the
+// ring (full: 256 producer arrivals after a proxy fence; empty:
+// tcgen05.commit) and the accumulator (ready: commit; free: 256 epilogue
+// arrivals after the lanes are read and re-zeroed).
+// Modular sums are order independent, so the words equal the reference's
+// sequential accumulation.
+
+#include <stdexcept>
+
+#include "ntt_core.cuh"
+
+namespace hecnn_b200 {
+
+namespace {
+
+constexpr int TC_M = 128;                 // coefficients per tile (TMEM lanes)
+constexpr int TC_OC = 48;                 // output channels per tile
+constexpr int TC_N = 5 * TC_OC;           // B columns: (weight byte b, oc)
+constexpr int TC_COLS = 9 * TC_OC;        // accumulator columns: (shift class s, oc)
+constexpr int TC_STAGES = 4;
+constexpr int TC_A_BYTES = TC_M * 32;     // one ciphertext byte plane, 32 taps
+constexpr int TC_B_BYTES = TC_N * 32;     // weight tile, 32 taps
+constexpr int TC_STAGE_BYTES = 5 * TC_A_BYTES + TC_B_BYTES;
+constexpr int TC_PRODUCERS = 256;        // 8 warps: (row j, K half) per thread
+constexpr int TC_THREADS = TC_PRODUCERS + 32;
+constexpr int TC_MMA_WARP = TC_PRODUCERS / 32;
+constexpr int TC_SMEM = TC_STAGES * TC_STAGE_BYTES + 2048;  // + 1 KB alignment slack + barriers, TMEM address
+
+__device__ __forceinline__ uint32_t s_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// K-major, no swizzle: core matrices of 8 rows x 16 B (128 B contiguous); the
+// two 16-byte K halves 128 B apart (LBO), row groups 256 B apart (SBO).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    uint64_t d = (saddr >> 4) & 0x3FFF;
+    d |= static_cast<uint64_t>(128 >> 4) << 16;
+    d |= static_cast<uint64_t>(256 >> 4) << 32;
+    d |= 1ull << 46;  // descriptor version (sm_100)
+    return d;
+}
+// kind::i8 instruction descriptor: D s32, A/B unsigned 8-bit, both K-major, M x N
+constexpr uint32_t kIdesc = (2u << 4) | (static_cast<uint32_t>(TC_N >> 3) << 17) | (static_cast<uint32_t>(TC_M >> 4) << 24);
+
+__device__ __forceinline__ int core_off(int row, int k) { return (row >> 3) * 256 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("{.reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0];}" ::"r"(s_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{.reg .pred P1;\n"
+        "WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;}" ::"r"(s_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 4x4 byte transpose of four 32-bit words: p[a] = byte a of each word, word u in byte u.
+__device__ __forceinline__ void transpose4(unsigned l0, unsigned l1, unsigned l2, unsigned l3, unsigned* p) {
+    const unsigned x01 = __byte_perm(l0, l1, 0x5140), x01h = __byte_perm(l0, l1, 0x7362);
+    const unsigned x23 = __byte_perm(l2, l3, 0x5140), x23h = __byte_perm(l2, l3, 0x7362);
+    p[0] = __byte_perm(x01, x23, 0x5410);
+    p[1] = __byte_perm(x01, x23, 0x7632);
+    p[2] = __byte_perm(x01h, x23h, 0x5410);
+    p[3] = __byte_perm(x01h, x23h, 0x7632);
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void tmem_zero16(uint32_t addr) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
+                 "r"(0u));
+}
+
+// blockIdx.x = ((row * nj) + jb) * groups + pixel group; a CTA runs every
+// (pixel, oc tile) of its group over one 128-coefficient column block.
+__global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g, const u64* __restrict__ x,
+                                                          u64* __restrict__ y, int level, int limb0, int nl, int groups,
+                                                          int pg) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
+    uint64_t* full = bars;                    // [STAGES]
+    uint64_t* empty = bars + TC_STAGES;       // [STAGES]
+    uint64_t* acc_ready = bars + 2 * TC_STAGES;
+    uint64_t* acc_free = acc_ready + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 1);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int limbs = level + 1;
+    const long long poly_words = static_cast<long long>(limbs) * R.n;
+    const long long cell_words = 2 * poly_words;
+    const int nj = R.n / TC_M;
+    const long long bid = blockIdx.x;
+    const long long cb = bid / groups;
+    const int p_begin = static_cast<int>(bid - cb * groups) * pg, p_end = min(p_begin + pg, g.pixels);
+    const int jb = static_cast<int>(cb % nj);
+    const int row = static_cast<int>(cb / nj);
+    const int comp = row / nl, i = limb0 + row % nl;
+    const int j0 = jb * TC_M;
+    const long long col_base = comp * poly_words + static_cast<long long>(i) * R.n + j0;
+    const int tiles = (g.oc + TC_OC - 1) / TC_OC;
+    const int items = (p_end - p_begin) * tiles;
+    const int ks_n = g.ksteps;
+
+    if (warp == TC_MMA_WARP) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_addr(tmem_slot)), "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(full + s, TC_PRODUCERS);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(acc_ready, 1);
+        mbar_init(acc_free, TC_PRODUCERS);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < TC_MMA_WARP) {
+        const int r = tid & (TC_M - 1), kh = tid / TC_M;  // coefficient row, K half / channel half
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        constexpr int HOC = TC_OC / 2;
+        auto zero_acc = [&] {
+            // this thread's channel half of every shift class (the plane ranges overlap,
+            // so every MMA accumulates onto a zeroed accumulator)
+#pragma unroll
+            for (int s = 0; s < 9; ++s) {
+                const uint32_t a = lane_base + s * TC_OC + kh * HOC;
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(a), "r"(0u));
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(a + 8), "r"(0u));
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+        };
+        zero_acc();
+        mbar_arrive(acc_free);  // phase 0 of acc_free: the accumulator is free for item 0
+
+        const u64* xcol = x + col_base + r;
+        const u64 q = R.mod[i].q;
+        const double qd = static_cast<double>(q), qinv = R.inv_q[i];
+        const double* cs = g.shift + i * 9;
+        const uint4* wt_limb = g.wtc + static_cast<long long>(i) * tiles * ks_n * (TC_B_BYTES / 16);
+        const bool short_k = ks_n <= 48;  // D_s < 2^29: three classes per exact double
+        const int total = items * ks_n;
+        // this thread's 16 tap words of global step gs (item gs / ks_n, step gs % ks_n)
+        auto gather = [&](int gs, u64 (&w)[16]) {
+            const int it = gs / ks_n, ks = gs - it * ks_n;
+            const int* src = g.src + static_cast<long long>(p_begin + it / tiles) * g.kpad + ks * 32 + kh * 16;
+#pragma unroll
+            for (int kk = 0; kk < 16; kk += 4) {
+                const int4 t4 = __ldg(reinterpret_cast<const int4*>(src + kk));
+                w[kk] = t4.x >= 0 ? __ldg(xcol + t4.x * cell_words) : 0;
+                w[kk + 1] = t4.y >= 0 ? __ldg(xcol + t4.y * cell_words) : 0;
+                w[kk + 2] = t4.z >= 0 ? __ldg(xcol + t4.z * cell_words) : 0;
+                w[kk + 3] = t4.w >= 0 ? __ldg(xcol + t4.w * cell_words) : 0;
+            }
+        };
+        u64 cur[16], nxt[16];
+        if (total > 0) gather(0, cur);
+        for (int gs = 0; gs < total; ++gs) {
+            const int it = gs / ks_n, ks = gs - it * ks_n;
+            if (gs + 1 < total) gather(gs + 1, nxt);  // in flight while this step is converted
+            const int stage = gs % TC_STAGES;
+            if (gs >= TC_STAGES) mbar_wait(empty + stage, ((gs / TC_STAGES) - 1) & 1);
+            unsigned char* st = smem + stage * TC_STAGE_BYTES;
+            // byte planes a = 0..4 of row r, this thread's 16 taps
+            unsigned pl[5][4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const u64* ww = cur + 4 * c;
+                unsigned p4[4];
+                transpose4(static_cast<unsigned>(ww[0]), static_cast<unsigned>(ww[1]), static_cast<unsigned>(ww[2]),
+                           static_cast<unsigned>(ww[3]), p4);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) pl[a][c] = p4[a];
+                const unsigned h0 = static_cast<unsigned>(ww[0] >> 32), h1 = static_cast<unsigned>(ww[1] >> 32);
+                const unsigned h2 = static_cast<unsigned>(ww[2] >> 32), h3 = static_cast<unsigned>(ww[3] >> 32);
+                pl[4][c] = __byte_perm(__byte_perm(h0, h1, 0x0040), __byte_perm(h2, h3, 0x0040), 0x5410);
+            }
+#pragma unroll
+            for (int a = 0; a < 5; ++a)
+                *reinterpret_cast<uint4*>(st + a * TC_A_BYTES + core_off(r, kh * 16)) =
+                    make_uint4(pl[a][0], pl[a][1], pl[a][2], pl[a][3]);
+            // the weight tile (already in the core-matrix layout)
+            const int ot = it % tiles;
+            const uint4* wsrc = wt_limb + (static_cast<long long>(ot) * ks_n + ks) * (TC_B_BYTES / 16);
+            uint4* wdst = reinterpret_cast<uint4*>(st + 5 * TC_A_BYTES);
+            for (int c = tid; c < TC_B_BYTES / 16; c += TC_PRODUCERS) wdst[c] = __ldg(wsrc + c);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+            mbar_arrive(full + stage);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) cur[u] = nxt[u];
+            if (ks != ks_n - 1) continue;
+
+            // epilogue of item it: D_s from TMEM (lane = this coefficient), this channel half
+            mbar_wait(acc_ready, it & 1);
+            tc_fence_after();
+            const int p = p_begin + it / tiles;
+            const int j = j0 + r;
+#pragma unroll 1
+            for (int c0 = kh * HOC; c0 < kh * HOC + HOC; c0 += 8) {
+                uint32_t d[9][8];
+#pragma unroll
+                for (int s = 0; s < 9; ++s) tmem_ld8(lane_base + s * TC_OC + c0, d[s]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int o = 0; o < 8; ++o) {
+                    const int oc = ot * TC_OC + c0 + o;
+                    auto D = [&](int s) { return static_cast<double>(d[s][o]); };
+                    double v;
+                    if (short_k) {
+                        v = ntt::fmodmul(D(0) + 256.0 * D(1) + 65536.0 * D(2), __ldg(cs + 0), qd, qinv);
+                        v += ntt::fmodmul(D(3) + 256.0 * D(4) + 65536.0 * D(5), __ldg(cs + 3), qd, qinv);
+                        v += ntt::fmodmul(D(6) + 256.0 * D(7) + 65536.0 * D(8), __ldg(cs + 6), qd, qinv);
+                    } else {
+                        v = 0.0;
+#pragma unroll
+                        for (int s = 0; s < 9; ++s) v += ntt::fmodmul(D(s), __ldg(cs + s), qd, qinv);
+                    }
+                    if (oc < g.oc) {
+                        u64 res = ntt::fcanon(v, qd, qinv);
+                        if (g.bias && comp == 0 && j == 0) res = add_mod(res, g.bias[static_cast<long long>(oc) * limbs + i], q);
+                        y[(static_cast<long long>(p) * g.out_stride_pixel + oc) * cell_words + col_base + r] = res;
+                    }
+                }
+            }
+            zero_acc();
+            mbar_arrive(acc_free);
+        }
+    } else {
+        // MMA issuer: one elected thread of warp 8
+        if ((tid & 31) == 0) {
+            const uint32_t a0 = s_addr(smem);
+            int gs = 0;
+            for (int it = 0; it < items; ++it) {
+                mbar_wait(acc_free, it & 1);  // epilogue of item it-1 read and re-zeroed the accumulator
+                tc_fence_after();
+                for (int ks = 0; ks < ks_n; ++ks, ++gs) {
+                    const int stage = gs % TC_STAGES;
+                    mbar_wait(full + stage, (gs / TC_STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = a0 + stage * TC_STAGE_BYTES;
+                    const uint64_t db = umma_desc(sa + 5 * TC_A_BYTES);
+#pragma unroll
+                    for (int a = 0; a < 5; ++a) {
+                        const uint64_t da = umma_desc(sa + a * TC_A_BYTES);
+                        asm volatile(
+                            "{.reg .pred p; setp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;}" ::"r"(tmem + a * TC_OC),
+                            "l"(da), "l"(db), "r"(kIdesc), "r"(1u));
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     s_addr(empty + stage))
+                                 : "memory");
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 s_addr(acc_ready))
+                             : "memory");
+            }
+        }
+        __syncwarp();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == TC_MMA_WARP) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    }
+}
+
+}  // namespace
+
+int tc_oc_tile() { return TC_OC; }
+
+bool tc_mac_supported(const DevRing& R, const ImmaMac& g) {
+    // one exact int32 chunk (K <= 6144); short K stays on mma.sync (the
+    // per-tile epilogue would dominate a handful of MMAs)
+    return g.wtc && R.n % TC_M == 0 && g.ksteps >= 8 && g.ksteps <= 192;
+}
+
+void tc_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level, int limb0, int limb1, const Launch& L) {
+    const int nl = limb1 - limb0;
+    if (!g.pixels || !g.oc || nl <= 0) return;
+    if (!tc_mac_supported(R, g)) throw std::invalid_argument("tc_mac: unsupported shape");
+    static bool init = (cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM), true);
+    (void)init;
+    const long long rows = 2LL * nl, nj = R.n / TC_M;
+    // pixel groups: enough CTAs for every SM, long runs of (pixel, oc tile) items per CTA
+    const long long cols = rows * nj;
+    int pg = 1;
+    while (pg < g.pixels && cols * ((g.pixels + 2 * pg - 1) / (2 * pg)) >= 4 * 148) pg *= 2;
+    const int groups = (g.pixels + pg - 1) / pg;
+    const long long blocks = cols * groups;
+    if (blocks > 0x7fffffffLL) throw std::runtime_error("tc_mac: grid too large");
+    const double ncols = double(rows) * R.n;
+    L.begin("k_conv_tc", double(g.pixels) * g.K * g.oc * ncols,
+            8.0 * ncols * (double(g.pixels) * g.oc + double(g.pixels) * g.K));
+    k_conv_tc<<<static_cast<unsigned>(blocks), TC_THREADS, TC_SMEM, L.stream>>>(R, g, x, y, level, limb0, nl, groups, pg);
+    L.count();
+    check_launch("tc_mac");
+}
+
+}  // namespace hecnn_b200

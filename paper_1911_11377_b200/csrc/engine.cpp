@@ -1092,6 +1092,37 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
     std::vector<int> sp(pixels * kpad, -1);
     for (std::size_t p = 0; p < pixels; ++p)
         for (std::size_t k = 0; k < K; ++k) sp[p * kpad + k] = src[p * K + k];
+    // tcgen05 weight tiles: per (limb, 48-channel tile, 32-tap step) the B
+    // operand of conv_tc.cu, rows n = b * 48 + o (weight byte b of channel o),
+    // in the UMMA K-major core-matrix layout (8 rows x 16 taps per 128 B)
+    const std::size_t TOC = static_cast<std::size_t>(tc_oc_tile()), ttiles = (oc + TOC - 1) / TOC;
+    const std::size_t tile_bytes = 5 * TOC * 32, wtc_bytes = limbs * ttiles * ksteps * tile_bytes;
+    const char* no_tc = std::getenv("HECNN_NO_TCGEN05");
+    if (!(no_tc && *no_tc == '1') && lc.pixels > 1 && ksteps <= 192 && C.n() % 128 == 0 && wtc_bytes <= (std::size_t(1) << 30)) {
+        std::vector<std::uint8_t> t(wtc_bytes, 0);
+        for (std::size_t i = 0; i < limbs; ++i) {
+            if (!imma_limb(C, i)) continue;
+            for (std::size_t ot = 0; ot < ttiles; ++ot)
+                for (std::size_t ks = 0; ks < ksteps; ++ks) {
+                    std::uint8_t* tile = t.data() + ((i * ttiles + ot) * ksteps + ks) * tile_bytes;
+                    for (std::size_t o = 0; o < TOC; ++o) {
+                        const std::size_t oo = ot * TOC + o;
+                        if (oo >= oc) continue;
+                        for (std::size_t k = 0; k < 32; ++k) {
+                            const std::size_t kk = ks * 32 + k;
+                            if (kk >= K) continue;
+                            const u64 v = w[(i * rows + kk) * oc_pad + oo].x;
+                            for (std::size_t b = 0; b < 5; ++b) {
+                                const std::size_t n = b * TOC + o;
+                                tile[(n >> 3) * 256 + (k >> 4) * 128 + (n & 7) * 16 + (k & 15)] =
+                                    static_cast<std::uint8_t>(v >> (8 * b));
+                            }
+                        }
+                    }
+                }
+        }
+        lc.wtc = C.upload_vec(t);
+    }
     lc.wfrag = C.upload_vec(frag);
     lc.shift = C.upload_vec(sh);
     lc.src_pad = C.upload_vec(sp);
@@ -1202,9 +1233,12 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
         if (lc.ksteps) {
             ImmaMac im{lc.src_pad.as<int>() + p0 * lc.kpad, lc.wfrag.as<uint4>(), bit->second.as<u64>(),
                        lc.shift.as<double>(), static_cast<int>(m), lc.K, lc.kpad, lc.ksteps, lc.oc, lc.oc_tiles, lc.oc,
-                       lc.wfrag_wide.as<uint4>(), lc.shift_wide.as<ulonglong2>()};
+                       lc.wfrag_wide.as<uint4>(), lc.shift_wide.as<ulonglong2>(), lc.wtc.as<uint4>()};
             for_limb_runs(C, limbs, [&](std::size_t l0, std::size_t l1, bool tc) {
-                if (tc || lc.wide_ok)
+                if (tc && tc_mac_supported(C.dev, im))
+                    tc_mac(C.dev, im, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
+                           static_cast<int>(l1), L);
+                else if (tc || lc.wide_ok)
                     imma_mac(C.dev, im, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
                              static_cast<int>(l1), !tc, L);
                 else gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
