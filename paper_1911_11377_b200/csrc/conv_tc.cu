@@ -41,7 +41,6 @@ namespace {
 constexpr int TC_M = 128;                 // coefficients per tile (TMEM lanes)
 constexpr int TC_OC = 48;                 // output channels per tile
 constexpr int TC_N = 5 * TC_OC;           // B columns: (weight byte b, oc)
-constexpr int TC_COLS = 9 * TC_OC;        // accumulator columns: (shift class s, oc)
 constexpr int TC_STAGES = 4;
 constexpr int TC_A_BYTES = TC_M * 32;     // one ciphertext byte plane, 32 taps
 constexpr int TC_B_BYTES = TC_N * 32;     // weight tile, 32 taps
@@ -99,10 +98,6 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                  : "r"(addr));
 }
-__device__ __forceinline__ void tmem_zero16(uint32_t addr) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr),
-                 "r"(0u));
-}
 
 // blockIdx.x = ((row * nj) + jb) * groups + pixel group; a CTA runs every
 // (pixel, oc tile) of its group over one 128-coefficient column block.
@@ -110,7 +105,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
                                                           u64* __restrict__ y, int level, int limb0, int nl, int groups,
                                                           int pg) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KB-aligned base, by offset so the compiler keeps shared-space stores
+    unsigned char* smem = smem_raw + ((1024u - (s_addr(smem_raw) & 1023u)) & 1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
     uint64_t* full = bars;                    // [STAGES]
     uint64_t* empty = bars + TC_STAGES;       // [STAGES]
@@ -123,16 +119,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
     const long long poly_words = static_cast<long long>(limbs) * R.n;
     const long long cell_words = 2 * poly_words;
     const int nj = R.n / TC_M;
+    // blockIdx.x = (column block * pixels + pixel) * tiles + oc tile: the CTAs
+    // resident at any time cover a few column blocks, whose slice of every
+    // input cell (cells x 1 KB) stays L2-resident while all pixels and channel
+    // tiles gather from it
+    const int tiles = (g.oc + TC_OC - 1) / TC_OC;
     const long long bid = blockIdx.x;
-    const long long cb = bid / groups;
-    const int p_begin = static_cast<int>(bid - cb * groups) * pg, p_end = min(p_begin + pg, g.pixels);
+    const int tile0 = static_cast<int>(bid % tiles);
+    const long long pix_cb = bid / tiles;
+    const long long cb = pix_cb / g.pixels;
+    const int p_begin = static_cast<int>(pix_cb - cb * g.pixels);
+    (void)groups, (void)pg;
     const int jb = static_cast<int>(cb % nj);
     const int row = static_cast<int>(cb / nj);
     const int comp = row / nl, i = limb0 + row % nl;
     const int j0 = jb * TC_M;
     const long long col_base = comp * poly_words + static_cast<long long>(i) * R.n + j0;
-    const int tiles = (g.oc + TC_OC - 1) / TC_OC;
-    const int items = (p_end - p_begin) * tiles;
+    constexpr int items = 1;  // one (pixel, oc tile) per CTA
     const int ks_n = g.ksteps;
 
     if (warp == TC_MMA_WARP) {
@@ -179,17 +182,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
         const uint4* wt_limb = g.wtc + static_cast<long long>(i) * tiles * ks_n * (TC_B_BYTES / 16);
         const bool short_k = ks_n <= 48;  // D_s < 2^29: three classes per exact double
         const int total = items * ks_n;
+        const int ot = tile0;
         // this thread's 16 tap words of global step gs (item gs / ks_n, step gs % ks_n)
         auto gather = [&](int gs, u64 (&w)[16]) {
             const int it = gs / ks_n, ks = gs - it * ks_n;
-            const int* src = g.src + static_cast<long long>(p_begin + it / tiles) * g.kpad + ks * 32 + kh * 16;
+            const int* src = g.src + static_cast<long long>(p_begin + it) * g.kpad + ks * 32 + kh * 16;
 #pragma unroll
             for (int kk = 0; kk < 16; kk += 4) {
                 const int4 t4 = __ldg(reinterpret_cast<const int4*>(src + kk));
-                w[kk] = t4.x >= 0 ? __ldg(xcol + t4.x * cell_words) : 0;
-                w[kk + 1] = t4.y >= 0 ? __ldg(xcol + t4.y * cell_words) : 0;
-                w[kk + 2] = t4.z >= 0 ? __ldg(xcol + t4.z * cell_words) : 0;
-                w[kk + 3] = t4.w >= 0 ? __ldg(xcol + t4.w * cell_words) : 0;
+                // branch-free: padding taps (-1) load cell 0 and are masked to zero
+                const int tt[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const u64 v = __ldg(xcol + static_cast<long long>(max(tt[u], 0)) * cell_words);
+                    w[kk + u] = tt[u] >= 0 ? v : 0;
+                }
             }
         };
         u64 cur[16], nxt[16];
@@ -219,12 +226,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
                 *reinterpret_cast<uint4*>(st + a * TC_A_BYTES + core_off(r, kh * 16)) =
                     make_uint4(pl[a][0], pl[a][1], pl[a][2], pl[a][3]);
             // the weight tile (already in the core-matrix layout)
-            const int ot = it % tiles;
-            const uint4* wsrc = wt_limb + (static_cast<long long>(ot) * ks_n + ks) * (TC_B_BYTES / 16);
-            uint4* wdst = reinterpret_cast<uint4*>(st + 5 * TC_A_BYTES);
-            for (int c = tid; c < TC_B_BYTES / 16; c += TC_PRODUCERS) wdst[c] = __ldg(wsrc + c);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
-            mbar_arrive(full + stage);
+            if (tid == 0) {
+                // the weight tile (already in the core-matrix layout): one bulk copy on
+                // the async proxy, counted on the same barrier as transaction bytes
+                const uint4* wsrc = wt_limb + (static_cast<long long>(ot) * ks_n + ks) * (TC_B_BYTES / 16);
+                asm volatile("{.reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;}" ::"r"(s_addr(full + stage)),
+                             "r"(TC_B_BYTES)
+                             : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 s_addr(st + 5 * TC_A_BYTES)),
+                             "l"(wsrc), "r"(TC_B_BYTES), "r"(s_addr(full + stage))
+                             : "memory");
+            } else {
+                mbar_arrive(full + stage);
+            }
 #pragma unroll
             for (int u = 0; u < 16; ++u) cur[u] = nxt[u];
             if (ks != ks_n - 1) continue;
@@ -232,7 +248,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
             // epilogue of item it: D_s from TMEM (lane = this coefficient), this channel half
             mbar_wait(acc_ready, it & 1);
             tc_fence_after();
-            const int p = p_begin + it / tiles;
+            const int p = p_begin + it;
             const int j = j0 + r;
 #pragma unroll 1
             for (int c0 = kh * HOC; c0 < kh * HOC + HOC; c0 += 8) {
@@ -322,12 +338,9 @@ void tc_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level,
     static bool init = (cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM), true);
     (void)init;
     const long long rows = 2LL * nl, nj = R.n / TC_M;
-    // pixel groups: enough CTAs for every SM, long runs of (pixel, oc tile) items per CTA
     const long long cols = rows * nj;
-    int pg = 1;
-    while (pg < g.pixels && cols * ((g.pixels + 2 * pg - 1) / (2 * pg)) >= 4 * 148) pg *= 2;
-    const int groups = (g.pixels + pg - 1) / pg;
-    const long long blocks = cols * groups;
+    const int pg = 1, groups = g.pixels;
+    const long long blocks = cols * g.pixels * ((g.oc + TC_OC - 1) / TC_OC);
     if (blocks > 0x7fffffffLL) throw std::runtime_error("tc_mac: grid too large");
     const double ncols = double(rows) * R.n;
     L.begin("k_conv_tc", double(g.pixels) * g.K * g.oc * ncols,
