@@ -48,7 +48,9 @@ constexpr int TC_STAGE_BYTES = 5 * TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_PRODUCERS = 256;        // 8 warps: (row j, K half) per thread
 constexpr int TC_THREADS = TC_PRODUCERS + 32;
 constexpr int TC_MMA_WARP = TC_PRODUCERS / 32;
-constexpr int TC_SMEM = TC_STAGES * TC_STAGE_BYTES + 2048;  // + 1 KB alignment slack + barriers, TMEM address
+constexpr int TC_GDEPTH = 3;             // gathered-word staging depth (steps in flight per thread)
+constexpr int TC_GSTAGE_BYTES = TC_PRODUCERS * 16 * 8;
+constexpr int TC_SMEM = TC_STAGES * TC_STAGE_BYTES + TC_GDEPTH * TC_GSTAGE_BYTES + 2048;  // + alignment slack, barriers
 
 __device__ __forceinline__ uint32_t s_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -107,7 +109,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1 KB-aligned base, by offset so the compiler keeps shared-space stores
     unsigned char* smem = smem_raw + ((1024u - (s_addr(smem_raw) & 1023u)) & 1023u);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES);
+    u64* gstage = reinterpret_cast<u64*>(smem + TC_STAGES * TC_STAGE_BYTES);  // [GDEPTH][16 words][producers]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES + TC_GDEPTH * TC_GSTAGE_BYTES);
     uint64_t* full = bars;                    // [STAGES]
     uint64_t* empty = bars + TC_STAGES;       // [STAGES]
     uint64_t* acc_ready = bars + 2 * TC_STAGES;
@@ -183,27 +186,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
         const bool short_k = ks_n <= 48;  // D_s < 2^29: three classes per exact double
         const int total = items * ks_n;
         const int ot = tile0;
-        // this thread's 16 tap words of global step gs (item gs / ks_n, step gs % ks_n)
-        auto gather = [&](int gs, u64 (&w)[16]) {
+        // this thread's 16 tap words of global step gs (item gs / ks_n, step gs % ks_n),
+        // gathered with cp.async into the staging ring (padding taps, -1,
+        // zero-fill); each thread reads back only its own words, so
+        // cp.async.wait_group alone orders the staging ring
+        auto gather = [&](int gs) {
             const int it = gs / ks_n, ks = gs - it * ks_n;
             const int* src = g.src + static_cast<long long>(p_begin + it) * g.kpad + ks * 32 + kh * 16;
+            u64* dst = gstage + (gs % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid;
 #pragma unroll
             for (int kk = 0; kk < 16; kk += 4) {
                 const int4 t4 = __ldg(reinterpret_cast<const int4*>(src + kk));
-                // branch-free: padding taps (-1) load cell 0 and are masked to zero
                 const int tt[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const u64 v = __ldg(xcol + static_cast<long long>(max(tt[u], 0)) * cell_words);
-                    w[kk + u] = tt[u] >= 0 ? v : 0;
+                    const u64* from = xcol + static_cast<long long>(max(tt[u], 0)) * cell_words;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s_addr(dst + (kk + u) * TC_PRODUCERS)),
+                                 "l"(from), "r"(tt[u] >= 0 ? 8 : 0)
+                                 : "memory");
                 }
             }
         };
-        u64 cur[16], nxt[16];
-        if (total > 0) gather(0, cur);
+#pragma unroll
+        for (int d = 0; d < TC_GDEPTH; ++d) {
+            if (d < total) gather(d);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         for (int gs = 0; gs < total; ++gs) {
             const int it = gs / ks_n, ks = gs - it * ks_n;
-            if (gs + 1 < total) gather(gs + 1, nxt);  // in flight while this step is converted
+            asm volatile("cp.async.wait_group %0;" ::"n"(TC_GDEPTH - 1) : "memory");  // step gs landed
+            u64 cur[16];
+            {
+                const u64* from = gstage + (gs % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) cur[u] = from[u * TC_PRODUCERS];
+            }
             const int stage = gs % TC_STAGES;
             if (gs >= TC_STAGES) mbar_wait(empty + stage, ((gs / TC_STAGES) - 1) & 1);
             unsigned char* st = smem + stage * TC_STAGE_BYTES;
@@ -226,6 +243,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
                 *reinterpret_cast<uint4*>(st + a * TC_A_BYTES + core_off(r, kh * 16)) =
                     make_uint4(pl[a][0], pl[a][1], pl[a][2], pl[a][3]);
             // the weight tile (already in the core-matrix layout)
+            // refill the staging slot just read (its words are consumed: the plane stores used them)
+            if (gs + TC_GDEPTH < total) gather(gs + TC_GDEPTH);
+            asm volatile("cp.async.commit_group;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
             if (tid == 0) {
                 // the weight tile (already in the core-matrix layout): one bulk copy on
@@ -241,8 +261,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
             } else {
                 mbar_arrive(full + stage);
             }
-#pragma unroll
-            for (int u = 0; u < 16; ++u) cur[u] = nxt[u];
             if (ks != ks_n - 1) continue;
 
             // epilogue of item it: D_s from TMEM (lane = this coefficient), this channel half
