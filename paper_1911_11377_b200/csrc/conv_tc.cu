@@ -41,14 +41,20 @@ namespace {
 constexpr int TC_M = 128;                 // coefficients per tile (TMEM lanes)
 constexpr int TC_OC = 48;                 // output channels per tile
 constexpr int TC_N = 5 * TC_OC;           // B columns: (weight byte b, oc)
-constexpr int TC_STAGES = 4;
+#ifndef HECNN_TC_STAGES
+#define HECNN_TC_STAGES 4
+#endif
+#ifndef HECNN_TC_GDEPTH
+#define HECNN_TC_GDEPTH 3
+#endif
+constexpr int TC_STAGES = HECNN_TC_STAGES;
 constexpr int TC_A_BYTES = TC_M * 32;     // one ciphertext byte plane, 32 taps
 constexpr int TC_B_BYTES = TC_N * 32;     // weight tile, 32 taps
 constexpr int TC_STAGE_BYTES = 5 * TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_PRODUCERS = 256;        // 8 warps: (row j, K half) per thread
 constexpr int TC_THREADS = TC_PRODUCERS + 32;
 constexpr int TC_MMA_WARP = TC_PRODUCERS / 32;
-constexpr int TC_GDEPTH = 3;             // gathered-word staging depth (steps in flight per thread)
+constexpr int TC_GDEPTH = HECNN_TC_GDEPTH;  // gathered-word staging depth (steps in flight per thread)
 constexpr int TC_GSTAGE_BYTES = TC_PRODUCERS * 16 * 8;
 constexpr int TC_SMEM = TC_STAGES * TC_STAGE_BYTES + TC_GDEPTH * TC_GSTAGE_BYTES + 2048;  // + alignment slack, barriers
 
@@ -186,25 +192,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
         const bool short_k = ks_n <= 48;  // D_s < 2^29: three classes per exact double
         const int total = items * ks_n;
         const int ot = tile0;
-        // this thread's 16 tap words of global step gs (item gs / ks_n, step gs % ks_n),
-        // gathered with cp.async into the staging ring (padding taps, -1,
-        // zero-fill); each thread reads back only its own words, so
-        // cp.async.wait_group alone orders the staging ring
+        // this thread's 16 tap words of step gs, gathered with cp.async into the
+        // staging ring (padding taps, -1, zero-fill); each thread reads back
+        // only its own words, so cp.async.wait_group alone orders the ring.
+        // Steps are gathered in order; the tap indices of the next one are
+        // loaded one gather ahead so their latency is off the issue path.
+        const int* src_p = g.src + static_cast<long long>(p_begin) * g.kpad + kh * 16;
+        int4 taps[4];
+        auto load_taps = [&](int gs) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) taps[c] = __ldg(reinterpret_cast<const int4*>(src_p + gs * 32 + 4 * c));
+        };
+        load_taps(0);
         auto gather = [&](int gs) {
-            const int it = gs / ks_n, ks = gs - it * ks_n;
-            const int* src = g.src + static_cast<long long>(p_begin + it) * g.kpad + ks * 32 + kh * 16;
             u64* dst = gstage + (gs % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid;
+            int tt[16];
 #pragma unroll
-            for (int kk = 0; kk < 16; kk += 4) {
-                const int4 t4 = __ldg(reinterpret_cast<const int4*>(src + kk));
-                const int tt[4] = {t4.x, t4.y, t4.z, t4.w};
+            for (int c = 0; c < 4; ++c) tt[4 * c] = taps[c].x, tt[4 * c + 1] = taps[c].y, tt[4 * c + 2] = taps[c].z, tt[4 * c + 3] = taps[c].w;
+            if (gs + 1 < total) load_taps(gs + 1);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const u64* from = xcol + static_cast<long long>(max(tt[u], 0)) * cell_words;
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s_addr(dst + (kk + u) * TC_PRODUCERS)),
-                                 "l"(from), "r"(tt[u] >= 0 ? 8 : 0)
-                                 : "memory");
-                }
+            for (int u = 0; u < 16; ++u) {
+                const u64* from = xcol + static_cast<long long>(max(tt[u], 0)) * cell_words;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s_addr(dst + u * TC_PRODUCERS)), "l"(from),
+                             "r"(tt[u] >= 0 ? 8 : 0)
+                             : "memory");
             }
         };
 #pragma unroll
@@ -213,7 +224,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
         for (int gs = 0; gs < total; ++gs) {
-            const int it = gs / ks_n, ks = gs - it * ks_n;
+            constexpr int it = 0;
+            const int ks = gs;
             asm volatile("cp.async.wait_group %0;" ::"n"(TC_GDEPTH - 1) : "memory");  // step gs landed
             u64 cur[16];
             {

@@ -10,6 +10,9 @@ V[e4]="-DHECNN_KS_LOGE=4"
 V[batch]="-DHECNN_NTT_BATCH=1"
 V[nomac]="-DHECNN_KS_ABLATE_MAC"
 V[nosplit]="-DHECNN_NTT_SPLIT=0"
+V[col512]="-DHECNN_KS_MAXT_COL=512"
+V[tc34]="-DHECNN_TC_STAGES=3 -DHECNN_TC_GDEPTH=4"
+V[tc25]="-DHECNN_TC_STAGES=2 -DHECNN_TC_GDEPTH=5"
 V[nosacc]="-DHECNN_KS_ABLATE_SACC"
 V[b12e4]="-DHECNN_KS_LOGB=12 -DHECNN_KS_LOGE=4 -DHECNN_KS_MAXT_COL=256 -DHECNN_KS_MINB=2"
 for name in "${!V[@]}"; do
