@@ -27,6 +27,11 @@
 // ring (full: 256 producer arrivals after a proxy fence; empty:
 // tcgen05.commit) and the accumulator (ready: commit; free: 256 epilogue
 // arrivals after the lanes are read and re-zeroed).
+// The 60-bit limb (WIDE) runs the same kernel with the six balanced signed
+// base-256 digits of the weight integers W = round(w * Delta) (one copy for
+// every limb) against the eight bytes of the ciphertext words: B = 6 x 32
+// columns (signed), eight A planes, 13 x 32 = 416 accumulator columns, and a
+// 64-bit Shoup fold of the 13 classes (|D_s| <= 6 * 128 * 255 * K < 2^31).
 // Modular sums are order independent, so the words equal the reference's
 // sequential accumulation.
 
@@ -38,25 +43,39 @@ namespace hecnn_b200 {
 
 namespace {
 
-constexpr int TC_M = 128;                 // coefficients per tile (TMEM lanes)
-constexpr int TC_OC = 48;                 // output channels per tile
-constexpr int TC_N = 5 * TC_OC;           // B columns: (weight byte b, oc)
-#ifndef HECNN_TC_STAGES
-#define HECNN_TC_STAGES 4
+#ifndef HECNN_TC_MIN_KSTEPS
+#define HECNN_TC_MIN_KSTEPS 8
 #endif
 #ifndef HECNN_TC_GDEPTH
 #define HECNN_TC_GDEPTH 3
 #endif
-constexpr int TC_STAGES = HECNN_TC_STAGES;
-constexpr int TC_A_BYTES = TC_M * 32;     // one ciphertext byte plane, 32 taps
-constexpr int TC_B_BYTES = TC_N * 32;     // weight tile, 32 taps
-constexpr int TC_STAGE_BYTES = 5 * TC_A_BYTES + TC_B_BYTES;
-constexpr int TC_PRODUCERS = 256;        // 8 warps: (row j, K half) per thread
+
+constexpr int TC_M = 128;                   // coefficients per tile (TMEM lanes)
+constexpr int TC_PRODUCERS = 256;           // 8 warps: (row j, K half) per thread
 constexpr int TC_THREADS = TC_PRODUCERS + 32;
 constexpr int TC_MMA_WARP = TC_PRODUCERS / 32;
 constexpr int TC_GDEPTH = HECNN_TC_GDEPTH;  // gathered-word staging depth (steps in flight per thread)
 constexpr int TC_GSTAGE_BYTES = TC_PRODUCERS * 16 * 8;
-constexpr int TC_SMEM = TC_STAGES * TC_STAGE_BYTES + TC_GDEPTH * TC_GSTAGE_BYTES + 2048;  // + alignment slack, barriers
+constexpr int TC_A_BYTES = TC_M * 32;       // one ciphertext byte plane, 32 taps
+
+template <bool WIDE>
+struct TcShape {
+    static constexpr int NA = WIDE ? 8 : 5;        // ciphertext byte planes
+    static constexpr int NB = WIDE ? 6 : 5;        // weight byte / signed-digit planes
+    static constexpr int OC = WIDE ? 32 : 48;      // output channels per tile
+    static constexpr int N = NB * OC;              // B columns (b, oc): 192 / 240
+    static constexpr int NS = NA + NB - 1;         // shift classes: 13 / 9
+    static constexpr int STAGES = WIDE ? 3 : 4;
+    static constexpr int B_BYTES = N * 32;
+    static constexpr int STAGE_BYTES = NA * TC_A_BYTES + B_BYTES;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + TC_GDEPTH * TC_GSTAGE_BYTES + 2048;  // + alignment slack, barriers
+    // kind::i8 instruction descriptor: D s32, A unsigned 8-bit, B unsigned (signed
+    // digits when WIDE), both K-major, M x N
+    static constexpr uint32_t IDESC = (2u << 4) | ((WIDE ? 1u : 0u) << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+                                      (static_cast<uint32_t>(TC_M >> 4) << 24);
+    static_assert(NS * OC <= 512, "accumulator exceeds the TMEM columns");
+    static_assert(SMEM <= 227 * 1024, "shared memory");
+};
 
 __device__ __forceinline__ uint32_t s_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -69,8 +88,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
     d |= 1ull << 46;  // descriptor version (sm_100)
     return d;
 }
-// kind::i8 instruction descriptor: D s32, A/B unsigned 8-bit, both K-major, M x N
-constexpr uint32_t kIdesc = (2u << 4) | (static_cast<uint32_t>(TC_N >> 3) << 17) | (static_cast<uint32_t>(TC_M >> 4) << 24);
 
 __device__ __forceinline__ int core_off(int row, int k) { return (row >> 3) * 256 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15); }
 
@@ -106,20 +123,27 @@ __device__ __forceinline__ void tmem_ld8(uint32_t addr, uint32_t (&v)[8]) {
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                  : "r"(addr));
 }
+__device__ __forceinline__ void tmem_zero8(uint32_t addr) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr), "r"(0u));
+}
 
-// blockIdx.x = ((row * nj) + jb) * groups + pixel group; a CTA runs every
-// (pixel, oc tile) of its group over one 128-coefficient column block.
+// blockIdx.x = (column block * pixels + pixel) * tiles + oc tile: the CTAs
+// resident at any time cover a few column blocks, whose slice of every input
+// cell (cells x 1 KB) stays L2-resident while all pixels and channel tiles
+// gather from it. One (pixel, oc tile) per CTA.
+template <bool WIDE>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g, const u64* __restrict__ x,
-                                                          u64* __restrict__ y, int level, int limb0, int nl, int groups,
-                                                          int pg) {
+                                                          u64* __restrict__ y, int level, int limb0, int nl) {
+    using S = TcShape<WIDE>;
+    constexpr int NA = S::NA, NS = S::NS, OC = S::OC, STAGES = S::STAGES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1 KB-aligned base, by offset so the compiler keeps shared-space stores
     unsigned char* smem = smem_raw + ((1024u - (s_addr(smem_raw) & 1023u)) & 1023u);
-    u64* gstage = reinterpret_cast<u64*>(smem + TC_STAGES * TC_STAGE_BYTES);  // [GDEPTH][16 words][producers]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * TC_STAGE_BYTES + TC_GDEPTH * TC_GSTAGE_BYTES);
-    uint64_t* full = bars;                    // [STAGES]
-    uint64_t* empty = bars + TC_STAGES;       // [STAGES]
-    uint64_t* acc_ready = bars + 2 * TC_STAGES;
+    u64* gstage = reinterpret_cast<u64*>(smem + STAGES * S::STAGE_BYTES);  // [GDEPTH][16 words][producers]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES + TC_GDEPTH * TC_GSTAGE_BYTES);
+    uint64_t* full = bars;               // [STAGES]
+    uint64_t* empty = bars + STAGES;     // [STAGES]
+    uint64_t* acc_ready = bars + 2 * STAGES;
     uint64_t* acc_free = acc_ready + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 1);
 
@@ -128,23 +152,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
     const long long poly_words = static_cast<long long>(limbs) * R.n;
     const long long cell_words = 2 * poly_words;
     const int nj = R.n / TC_M;
-    // blockIdx.x = (column block * pixels + pixel) * tiles + oc tile: the CTAs
-    // resident at any time cover a few column blocks, whose slice of every
-    // input cell (cells x 1 KB) stays L2-resident while all pixels and channel
-    // tiles gather from it
-    const int tiles = (g.oc + TC_OC - 1) / TC_OC;
+    const int tiles = (g.oc + OC - 1) / OC;
     const long long bid = blockIdx.x;
-    const int tile0 = static_cast<int>(bid % tiles);
+    const int ot = static_cast<int>(bid % tiles);
     const long long pix_cb = bid / tiles;
     const long long cb = pix_cb / g.pixels;
-    const int p_begin = static_cast<int>(pix_cb - cb * g.pixels);
-    (void)groups, (void)pg;
+    const int p = static_cast<int>(pix_cb - cb * g.pixels);
     const int jb = static_cast<int>(cb % nj);
     const int row = static_cast<int>(cb / nj);
     const int comp = row / nl, i = limb0 + row % nl;
     const int j0 = jb * TC_M;
     const long long col_base = comp * poly_words + static_cast<long long>(i) * R.n + j0;
-    constexpr int items = 1;  // one (pixel, oc tile) per CTA
     const int ks_n = g.ksteps;
 
     if (warp == TC_MMA_WARP) {
@@ -152,7 +170,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        for (int s = 0; s < TC_STAGES; ++s) {
+        for (int s = 0; s < STAGES; ++s) {
             mbar_init(full + s, TC_PRODUCERS);
             mbar_init(empty + s, 1);
         }
@@ -168,48 +186,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
     if (warp < TC_MMA_WARP) {
         const int r = tid & (TC_M - 1), kh = tid / TC_M;  // coefficient row, K half / channel half
         const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-        constexpr int HOC = TC_OC / 2;
-        auto zero_acc = [&] {
-            // this thread's channel half of every shift class (the plane ranges overlap,
-            // so every MMA accumulates onto a zeroed accumulator)
+        constexpr int HOC = OC / 2;
+        static_assert(HOC % 8 == 0, "epilogue chunks of 8 channels");
+        // this thread's channel half of every shift class starts at zero (the plane
+        // ranges overlap, so every MMA accumulates)
 #pragma unroll
-            for (int s = 0; s < 9; ++s) {
-                const uint32_t a = lane_base + s * TC_OC + kh * HOC;
-                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(a), "r"(0u));
-                asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(a + 8), "r"(0u));
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            tc_fence_before();
-        };
-        zero_acc();
-        mbar_arrive(acc_free);  // phase 0 of acc_free: the accumulator is free for item 0
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+            for (int c = 0; c < HOC; c += 8) tmem_zero8(lane_base + s * OC + kh * HOC + c);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(acc_free);  // the accumulator is ready for the MMAs
 
         const u64* xcol = x + col_base + r;
-        const u64 q = R.mod[i].q;
-        const double qd = static_cast<double>(q), qinv = R.inv_q[i];
-        const double* cs = g.shift + i * 9;
-        const uint4* wt_limb = g.wtc + static_cast<long long>(i) * tiles * ks_n * (TC_B_BYTES / 16);
-        const bool short_k = ks_n <= 48;  // D_s < 2^29: three classes per exact double
-        const int total = items * ks_n;
-        const int ot = tile0;
-        // this thread's 16 tap words of step gs, gathered with cp.async into the
+        const uint4* wt = (WIDE ? g.wtc_wide : g.wtc + static_cast<long long>(i) * tiles * ks_n * (S::B_BYTES / 16)) +
+                          static_cast<long long>(ot) * ks_n * (S::B_BYTES / 16);
+        // this thread's 16 tap words of step ks, gathered with cp.async into the
         // staging ring (padding taps, -1, zero-fill); each thread reads back
         // only its own words, so cp.async.wait_group alone orders the ring.
         // Steps are gathered in order; the tap indices of the next one are
         // loaded one gather ahead so their latency is off the issue path.
-        const int* src_p = g.src + static_cast<long long>(p_begin) * g.kpad + kh * 16;
+        const int* src_p = g.src + static_cast<long long>(p) * g.kpad + kh * 16;
         int4 taps[4];
-        auto load_taps = [&](int gs) {
+        auto load_taps = [&](int ks) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) taps[c] = __ldg(reinterpret_cast<const int4*>(src_p + gs * 32 + 4 * c));
+            for (int c = 0; c < 4; ++c) taps[c] = __ldg(reinterpret_cast<const int4*>(src_p + ks * 32 + 4 * c));
         };
         load_taps(0);
-        auto gather = [&](int gs) {
-            u64* dst = gstage + (gs % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid;
+        auto gather = [&](int ks) {
+            u64* dst = gstage + (ks % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid;
             int tt[16];
 #pragma unroll
             for (int c = 0; c < 4; ++c) tt[4 * c] = taps[c].x, tt[4 * c + 1] = taps[c].y, tt[4 * c + 2] = taps[c].z, tt[4 * c + 3] = taps[c].w;
-            if (gs + 1 < total) load_taps(gs + 1);
+            if (ks + 1 < ks_n) load_taps(ks + 1);
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 const u64* from = xcol + static_cast<long long>(max(tt[u], 0)) * cell_words;
@@ -220,24 +229,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
         };
 #pragma unroll
         for (int d = 0; d < TC_GDEPTH; ++d) {
-            if (d < total) gather(d);
+            if (d < ks_n) gather(d);
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
-        for (int gs = 0; gs < total; ++gs) {
-            constexpr int it = 0;
-            const int ks = gs;
-            asm volatile("cp.async.wait_group %0;" ::"n"(TC_GDEPTH - 1) : "memory");  // step gs landed
+        for (int ks = 0; ks < ks_n; ++ks) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(TC_GDEPTH - 1) : "memory");  // step ks landed
             u64 cur[16];
             {
-                const u64* from = gstage + (gs % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid;
+                const u64* from = gstage + (ks % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid;
 #pragma unroll
                 for (int u = 0; u < 16; ++u) cur[u] = from[u * TC_PRODUCERS];
             }
-            const int stage = gs % TC_STAGES;
-            if (gs >= TC_STAGES) mbar_wait(empty + stage, ((gs / TC_STAGES) - 1) & 1);
-            unsigned char* st = smem + stage * TC_STAGE_BYTES;
-            // byte planes a = 0..4 of row r, this thread's 16 taps
-            unsigned pl[5][4];
+            const int stage = ks % STAGES;
+            if (ks >= STAGES) mbar_wait(empty + stage, ((ks / STAGES) - 1) & 1);
+            unsigned char* st = smem + stage * S::STAGE_BYTES;
+            // byte planes a < NA of row r, this thread's 16 taps
+            unsigned pl[NA][4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const u64* ww = cur + 4 * c;
@@ -248,50 +255,72 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
                 for (int a = 0; a < 4; ++a) pl[a][c] = p4[a];
                 const unsigned h0 = static_cast<unsigned>(ww[0] >> 32), h1 = static_cast<unsigned>(ww[1] >> 32);
                 const unsigned h2 = static_cast<unsigned>(ww[2] >> 32), h3 = static_cast<unsigned>(ww[3] >> 32);
-                pl[4][c] = __byte_perm(__byte_perm(h0, h1, 0x0040), __byte_perm(h2, h3, 0x0040), 0x5410);
+                if constexpr (WIDE) {
+                    transpose4(h0, h1, h2, h3, p4);
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) pl[4 + a][c] = p4[a];
+                } else {
+                    pl[4][c] = __byte_perm(__byte_perm(h0, h1, 0x0040), __byte_perm(h2, h3, 0x0040), 0x5410);
+                }
             }
 #pragma unroll
-            for (int a = 0; a < 5; ++a)
+            for (int a = 0; a < NA; ++a)
                 *reinterpret_cast<uint4*>(st + a * TC_A_BYTES + core_off(r, kh * 16)) =
                     make_uint4(pl[a][0], pl[a][1], pl[a][2], pl[a][3]);
-            // the weight tile (already in the core-matrix layout)
             // refill the staging slot just read (its words are consumed: the plane stores used them)
-            if (gs + TC_GDEPTH < total) gather(gs + TC_GDEPTH);
+            if (ks + TC_GDEPTH < ks_n) gather(ks + TC_GDEPTH);
             asm volatile("cp.async.commit_group;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
             if (tid == 0) {
                 // the weight tile (already in the core-matrix layout): one bulk copy on
                 // the async proxy, counted on the same barrier as transaction bytes
-                const uint4* wsrc = wt_limb + (static_cast<long long>(ot) * ks_n + ks) * (TC_B_BYTES / 16);
+                const uint4* wsrc = wt + static_cast<long long>(ks) * (S::B_BYTES / 16);
                 asm volatile("{.reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;}" ::"r"(s_addr(full + stage)),
-                             "r"(TC_B_BYTES)
+                             "r"(S::B_BYTES)
                              : "memory");
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                                 s_addr(st + 5 * TC_A_BYTES)),
-                             "l"(wsrc), "r"(TC_B_BYTES), "r"(s_addr(full + stage))
+                                 s_addr(st + NA * TC_A_BYTES)),
+                             "l"(wsrc), "r"(S::B_BYTES), "r"(s_addr(full + stage))
                              : "memory");
             } else {
                 mbar_arrive(full + stage);
             }
-            if (ks != ks_n - 1) continue;
+        }
 
-            // epilogue of item it: D_s from TMEM (lane = this coefficient), this channel half
-            mbar_wait(acc_ready, it & 1);
-            tc_fence_after();
-            const int p = p_begin + it;
-            const int j = j0 + r;
+        // epilogue: D_s from TMEM (lane = this coefficient), this channel half
+        mbar_wait(acc_ready, 0);
+        tc_fence_after();
+        const u64 q = R.mod[i].q;
+        const int j = j0 + r;
 #pragma unroll 1
-            for (int c0 = kh * HOC; c0 < kh * HOC + HOC; c0 += 8) {
-                uint32_t d[9][8];
+        for (int c0 = kh * HOC; c0 < kh * HOC + HOC; c0 += 8) {
+            uint32_t d[NS][8];
 #pragma unroll
-                for (int s = 0; s < 9; ++s) tmem_ld8(lane_base + s * TC_OC + c0, d[s]);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int s = 0; s < NS; ++s) tmem_ld8(lane_base + s * OC + c0, d[s]);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int o = 0; o < 8; ++o) {
-                    const int oc = ot * TC_OC + c0 + o;
+            for (int o = 0; o < 8; ++o) {
+                const int oc = ot * OC + c0 + o;
+                u64 res;
+                if constexpr (WIDE) {
+                    // classes in pairs: |D_s + 2^8 D_s+1| < 2^31 * 257 < 2^40 <= q, so one
+                    // conditional add of q makes the pair canonical
+                    const ulonglong2* cs = g.shift_wide + i * 16;
+                    res = 0;
+#pragma unroll
+                    for (int s = 0; s < NS; s += 2) {
+                        long long t = static_cast<int>(d[s][o]);
+                        if (s + 1 < NS) t += static_cast<long long>(static_cast<int>(d[s + 1][o])) * 256;
+                        const u64 rr = t >= 0 ? static_cast<u64>(t) : q - static_cast<u64>(-t);
+                        const ulonglong2 k = __ldg(cs + s);
+                        res = add_mod(res, mul_shoup(rr, k.x, k.y, q), q);
+                    }
+                } else {
+                    const double qd = static_cast<double>(q), qinv = R.inv_q[i];
+                    const double* cs = g.shift + i * 9;
                     auto D = [&](int s) { return static_cast<double>(d[s][o]); };
                     double v;
-                    if (short_k) {
+                    if (ks_n <= 48) {  // D_s < 2^29: three classes per exact double
                         v = ntt::fmodmul(D(0) + 256.0 * D(1) + 65536.0 * D(2), __ldg(cs + 0), qd, qinv);
                         v += ntt::fmodmul(D(3) + 256.0 * D(4) + 65536.0 * D(5), __ldg(cs + 3), qd, qinv);
                         v += ntt::fmodmul(D(6) + 256.0 * D(7) + 65536.0 * D(8), __ldg(cs + 6), qd, qinv);
@@ -300,48 +329,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
 #pragma unroll
                         for (int s = 0; s < 9; ++s) v += ntt::fmodmul(D(s), __ldg(cs + s), qd, qinv);
                     }
-                    if (oc < g.oc) {
-                        u64 res = ntt::fcanon(v, qd, qinv);
-                        if (g.bias && comp == 0 && j == 0) res = add_mod(res, g.bias[static_cast<long long>(oc) * limbs + i], q);
-                        y[(static_cast<long long>(p) * g.out_stride_pixel + oc) * cell_words + col_base + r] = res;
-                    }
+                    res = ntt::fcanon(v, qd, qinv);
+                }
+                if (oc < g.oc) {
+                    if (g.bias && comp == 0 && j == 0) res = add_mod(res, g.bias[static_cast<long long>(oc) * limbs + i], q);
+                    y[(static_cast<long long>(p) * g.out_stride_pixel + oc) * cell_words + col_base + r] = res;
                 }
             }
-            zero_acc();
-            mbar_arrive(acc_free);
         }
-    } else {
+    } else if ((tid & 31) == 0) {
         // MMA issuer: one elected thread of warp 8
-        if ((tid & 31) == 0) {
-            const uint32_t a0 = s_addr(smem);
-            int gs = 0;
-            for (int it = 0; it < items; ++it) {
-                mbar_wait(acc_free, it & 1);  // epilogue of item it-1 read and re-zeroed the accumulator
-                tc_fence_after();
-                for (int ks = 0; ks < ks_n; ++ks, ++gs) {
-                    const int stage = gs % TC_STAGES;
-                    mbar_wait(full + stage, (gs / TC_STAGES) & 1);
-                    tc_fence_after();
-                    const uint32_t sa = a0 + stage * TC_STAGE_BYTES;
-                    const uint64_t db = umma_desc(sa + 5 * TC_A_BYTES);
+        const uint32_t a0 = s_addr(smem);
+        mbar_wait(acc_free, 0);  // the producers zeroed the accumulator
+        tc_fence_after();
+        for (int ks = 0; ks < ks_n; ++ks) {
+            const int stage = ks % STAGES;
+            mbar_wait(full + stage, (ks / STAGES) & 1);
+            tc_fence_after();
+            const uint32_t sa = a0 + stage * S::STAGE_BYTES;
+            const uint64_t db = umma_desc(sa + NA * TC_A_BYTES);
 #pragma unroll
-                    for (int a = 0; a < 5; ++a) {
-                        const uint64_t da = umma_desc(sa + a * TC_A_BYTES);
-                        asm volatile(
-                            "{.reg .pred p; setp.ne.b32 p, %4, 0;\n"
-                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;}" ::"r"(tmem + a * TC_OC),
-                            "l"(da), "l"(db), "r"(kIdesc), "r"(1u));
-                    }
-                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                     s_addr(empty + stage))
-                                 : "memory");
-                }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 s_addr(acc_ready))
-                             : "memory");
+            for (int a = 0; a < NA; ++a) {
+                const uint64_t da = umma_desc(sa + a * TC_A_BYTES);
+                asm volatile(
+                    "{.reg .pred p; setp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;}" ::"r"(tmem + a * OC),
+                    "l"(da), "l"(db), "r"(S::IDESC), "r"(1u));
             }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             s_addr(empty + stage))
+                         : "memory");
         }
-        __syncwarp();
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_addr(acc_ready))
+                     : "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -353,31 +373,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
 
 }  // namespace
 
-int tc_oc_tile() { return TC_OC; }
+int tc_oc_tile(bool wide) { return wide ? TcShape<true>::OC : TcShape<false>::OC; }
 
-bool tc_mac_supported(const DevRing& R, const ImmaMac& g) {
+bool tc_mac_supported(const DevRing& R, const ImmaMac& g, bool wide) {
     // one exact int32 chunk (K <= 6144); short K stays on mma.sync (the
     // per-tile epilogue would dominate a handful of MMAs)
-    return g.wtc && R.n % TC_M == 0 && g.ksteps >= 8 && g.ksteps <= 192;
+    return (wide ? g.wtc_wide != nullptr : g.wtc != nullptr) && R.n % TC_M == 0 && g.ksteps >= HECNN_TC_MIN_KSTEPS &&
+           g.ksteps <= 192;
 }
 
-void tc_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level, int limb0, int limb1, const Launch& L) {
+void tc_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level, int limb0, int limb1, bool wide,
+            const Launch& L) {
     const int nl = limb1 - limb0;
     if (!g.pixels || !g.oc || nl <= 0) return;
-    if (!tc_mac_supported(R, g)) throw std::invalid_argument("tc_mac: unsupported shape");
-    static bool init = (cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM), true);
+    if (!tc_mac_supported(R, g, wide)) throw std::invalid_argument("tc_mac: unsupported shape");
+    auto kern = wide ? k_conv_tc<true> : k_conv_tc<false>;
+    const int smem = wide ? TcShape<true>::SMEM : TcShape<false>::SMEM;
+    const int oc_tile = tc_oc_tile(wide);
+    static bool init = (cudaFuncSetAttribute(k_conv_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcShape<true>::SMEM),
+                        cudaFuncSetAttribute(k_conv_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcShape<false>::SMEM),
+                        true);
     (void)init;
     const long long rows = 2LL * nl, nj = R.n / TC_M;
-    const long long cols = rows * nj;
-    const int pg = 1, groups = g.pixels;
-    const long long blocks = cols * g.pixels * ((g.oc + TC_OC - 1) / TC_OC);
+    const long long blocks = rows * nj * g.pixels * ((g.oc + oc_tile - 1) / oc_tile);
     if (blocks > 0x7fffffffLL) throw std::runtime_error("tc_mac: grid too large");
     const double ncols = double(rows) * R.n;
-    L.begin("k_conv_tc", double(g.pixels) * g.K * g.oc * ncols,
+    L.begin(wide ? "k_conv_tc_wide" : "k_conv_tc", double(g.pixels) * g.K * g.oc * ncols,
             8.0 * ncols * (double(g.pixels) * g.oc + double(g.pixels) * g.K));
-    k_conv_tc<<<static_cast<unsigned>(blocks), TC_THREADS, TC_SMEM, L.stream>>>(R, g, x, y, level, limb0, nl, groups, pg);
+    kern<<<static_cast<unsigned>(blocks), TC_THREADS, smem, L.stream>>>(R, g, x, y, level, limb0, nl);
     L.count();
-    check_launch("tc_mac");
+    check_launch(wide ? "tc_mac_wide" : "tc_mac");
 }
 
 }  // namespace hecnn_b200

@@ -1095,7 +1095,7 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
     // tcgen05 weight tiles: per (limb, 48-channel tile, 32-tap step) the B
     // operand of conv_tc.cu, rows n = b * 48 + o (weight byte b of channel o),
     // in the UMMA K-major core-matrix layout (8 rows x 16 taps per 128 B)
-    const std::size_t TOC = static_cast<std::size_t>(tc_oc_tile()), ttiles = (oc + TOC - 1) / TOC;
+    const std::size_t TOC = static_cast<std::size_t>(tc_oc_tile(false)), ttiles = (oc + TOC - 1) / TOC;
     const std::size_t tile_bytes = 5 * TOC * 32, wtc_bytes = limbs * ttiles * ksteps * tile_bytes;
     const char* no_tc = std::getenv("HECNN_NO_TCGEN05");
     if (!(no_tc && *no_tc == '1') && lc.pixels > 1 && ksteps <= 192 && C.n() % 128 == 0 && wtc_bytes <= (std::size_t(1) << 30)) {
@@ -1122,6 +1122,33 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
                 }
         }
         lc.wtc = C.upload_vec(t);
+        if (wide_ok) {
+            // the 60-bit limb: the balanced signed base-256 digits of W (one copy for all
+            // limbs), rows n = b * 32 + o of 192 per 32-tap step
+            const std::size_t WOC = static_cast<std::size_t>(tc_oc_tile(true)), wtiles = (oc + WOC - 1) / WOC;
+            const std::size_t wtile_bytes = 6 * WOC * 32;
+            std::vector<std::uint8_t> tw(wtiles * ksteps * wtile_bytes, 0);
+            for (std::size_t ot = 0; ot < wtiles; ++ot)
+                for (std::size_t ks = 0; ks < ksteps; ++ks) {
+                    std::uint8_t* tile = tw.data() + (ot * ksteps + ks) * wtile_bytes;
+                    for (std::size_t o = 0; o < WOC; ++o) {
+                        const std::size_t oo = ot * WOC + o;
+                        if (oo >= oc) continue;
+                        for (std::size_t k = 0; k < 32; ++k) {
+                            const std::size_t kk = ks * 32 + k;
+                            if (kk >= K) continue;
+                            std::int64_t v = W[kk * oc + oo];
+                            for (std::size_t b = 0; b < 6; ++b) {
+                                const std::int8_t dgt = static_cast<std::int8_t>(v & 0xFF);  // balanced digit
+                                v = (v - dgt) / 256;
+                                const std::size_t n = b * WOC + o;
+                                tile[(n >> 3) * 256 + (k >> 4) * 128 + (n & 7) * 16 + (k & 15)] = static_cast<std::uint8_t>(dgt);
+                            }
+                        }
+                    }
+                }
+            lc.wtc_wide = C.upload_vec(tw);
+        }
     }
     lc.wfrag = C.upload_vec(frag);
     lc.shift = C.upload_vec(sh);
@@ -1233,11 +1260,12 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
         if (lc.ksteps) {
             ImmaMac im{lc.src_pad.as<int>() + p0 * lc.kpad, lc.wfrag.as<uint4>(), bit->second.as<u64>(),
                        lc.shift.as<double>(), static_cast<int>(m), lc.K, lc.kpad, lc.ksteps, lc.oc, lc.oc_tiles, lc.oc,
-                       lc.wfrag_wide.as<uint4>(), lc.shift_wide.as<ulonglong2>(), lc.wtc.as<uint4>()};
+                       lc.wfrag_wide.as<uint4>(), lc.shift_wide.as<ulonglong2>(), lc.wtc.as<uint4>(),
+                       lc.wtc_wide.as<uint4>()};
             for_limb_runs(C, limbs, [&](std::size_t l0, std::size_t l1, bool tc) {
-                if (tc && tc_mac_supported(C.dev, im))
+                if ((tc || lc.wide_ok) && tc_mac_supported(C.dev, im, !tc))
                     tc_mac(C.dev, im, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
-                           static_cast<int>(l1), L);
+                           static_cast<int>(l1), !tc, L);
                 else if (tc || lc.wide_ok)
                     imma_mac(C.dev, im, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
                              static_cast<int>(l1), !tc, L);

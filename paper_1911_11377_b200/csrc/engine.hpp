@@ -193,7 +193,7 @@ struct Model {
         // integer tensor-core path (limbs with q < 2^40): fragment-ordered weight
         // byte planes, 2^8s mod q table, taps padded to whole 32-tap steps
         DevBuf wfrag, shift, src_pad, wfrag_wide, shift_wide;
-        DevBuf wtc;  // tcgen05 weight tiles (conv_tc.cu), when the shape qualifies
+        DevBuf wtc, wtc_wide;  // tcgen05 weight tiles (conv_tc.cu), when the shape qualifies
         int kpad = 0, ksteps = 0, oc_tiles = 0;
         bool wide_ok = false;  // limbs with q >= 2^40 also on the tensor cores (signed weight digits)
     };

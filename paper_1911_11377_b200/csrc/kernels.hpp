@@ -182,12 +182,16 @@ struct ImmaMac {
     // tcgen05 path (conv_tc.cu): [limbs][ceil(oc/48)][ksteps] weight tiles of
     // 240 (byte plane, oc) rows x 32 taps in the UMMA K-major core-matrix layout
     const uint4* wtc = nullptr;
+    // the 60-bit limb on tcgen05: [ceil(oc/32)][ksteps] tiles of 192 (signed digit b, oc) rows x 32 taps
+    const uint4* wtc_wide = nullptr;
 };
 bool imma_mac_supported(const DevRing& R, std::size_t K);
 // 5th-gen tensor-core conv (tcgen05.mma kind::i8, TMEM accumulators), limbs q < 2^40
-int tc_oc_tile();
-bool tc_mac_supported(const DevRing& R, const ImmaMac& g);
-void tc_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level, int limb0, int limb1, const Launch& L);
+// (wide: the limbs with q >= 2^40, signed weight digits)
+int tc_oc_tile(bool wide);
+bool tc_mac_supported(const DevRing& R, const ImmaMac& g, bool wide);
+void tc_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level, int limb0, int limb1, bool wide,
+            const Launch& L);
 void imma_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level, int limb0, int limb1, bool wide,
               const Launch& L);
 // 2x2-style average pool: out cell p sums srcs[p][0..taps) then multiplies by w (shoup), level kept

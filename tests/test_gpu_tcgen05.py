@@ -1,5 +1,6 @@
 """GPU: the conv layers on the 5th-generation tensor cores (csrc/conv_tc.cu,
-tcgen05.mma kind::i8 with TMEM accumulators, K >= 256 taps).
+tcgen05.mma kind::i8 with TMEM accumulators, K >= 256 taps; the 40-bit limbs
+as u8 x u8 byte planes, the 60-bit limb as signed weight digits x u8).
 
 The kernel must give the reference's words (mul_scalar_mac summed over the
 taps, ckks.hpp:448-465 via layers.hpp:174-211). Checked directly against the
@@ -53,6 +54,7 @@ def test_tcgen05_conv_matches_reference(ref, oc, k, cin, valid):
     rx = r.encrypt_tensor(data, spec.input, seed=5)
     ty, prof = _run(eng, spec, tx, {})
     assert "k_conv_tc" in prof, "the tcgen05 conv did not run"
+    assert "k_conv_tc_wide" in prof, "the 60-bit limb did not run on tcgen05"
     ry, _ = r.forward_encrypted(spec, rx, seed=6)
     assert ty.level == ry.info()[1] and ty.scale == ry.info()[2]
     assert np.array_equal(ty.words(), ry.words())
@@ -74,7 +76,7 @@ def test_tcgen05_conv_c5_ring_matches_gather_mac():
     x = eng.tensor_from_words(words, level, p.scale)
     x.set_shape(spec.input, p.n // 2)
     a, prof = _run(eng, spec, x, {"HECNN_NO_IMMA": "0"})
-    assert "k_conv_tc" in prof
+    assert "k_conv_tc" in prof and "k_conv_tc_wide" in prof
     b, prof_b = _run(eng, spec, x, {"HECNN_NO_IMMA": "1"})
     assert "k_conv_tc" not in prof_b
     assert (a.level, a.scale) == (b.level, b.scale)
