@@ -217,7 +217,14 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     // first round (S0 = 0): unit u owns positions u + k * STR0, k < E0
     constexpr int R0 = ntt::round_size(LOGB, LOGE, 0), E0 = 1 << R0, U0 = B >> R0, P0 = (U0 + T - 1) / T;
     constexpr int STR0 = U0;
-    constexpr bool PREFETCH = FP && C == 0;
+#ifndef HECNN_KS_PF_COL
+#define HECNN_KS_PF_COL 0
+#endif
+    // FP64 path: the next digit's first-round inputs are loaded into registers
+    // while the current digit is transformed; with one column stage (C = 1) the
+    // two inputs of each element's column butterfly are prefetched
+    constexpr bool PREFETCH = FP && (C == 0 || (HECNN_KS_PF_COL && C == 1));
+    constexpr int PFW = C == 0 ? 1 : 2;  // words per first-round element
     const long long n = 1LL << LOGN;
     const long long blk_off = static_cast<long long>(b) << LOGB;
     const ulonglong2* itw = R.fwd + (static_cast<long long>(i) << LOGN);  // integer twiddles for the column stages
@@ -243,7 +250,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
 #pragma unroll
     for (int k = 0; k < (FP ? 1 : PL * EL); ++k) a1[k] = V(0);
 
-    u32 pf[PREFETCH ? P0 * E0 : 1];
+    u32 pf[PREFETCH ? P0 * E0 * PFW : 1];
     auto prefetch = [&](int t) {
         if constexpr (PREFETCH) {
             const u32* dig = digits + (ct * D + t) * n;
@@ -252,10 +259,14 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                 const int u = threadIdx.x + uu * T;
 #pragma unroll
                 for (int k = 0; k < E0; ++k)
-                    pf[uu * E0 + k] = (U0 % T != 0 && u >= U0) ? 0u : __ldg(dig + u + k * STR0);
+#pragma unroll
+                    for (int h = 0; h < PFW; ++h)
+                        pf[(uu * E0 + k) * PFW + h] = (U0 % T != 0 && u >= U0) ? 0u : __ldg(dig + u + k * STR0 + h * B);
             }
         }
     };
+    // the column stage's twiddle (stage 0 of the N-point transform) for C = 1
+    const double w_col = (PREFETCH && C == 1) ? R.fwd_f[(static_cast<long long>(i) << LOGN) + 1] : 0.0;
     prefetch(0);
 
     auto lift = [&](u32 v) -> u64 {
@@ -265,9 +276,14 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     for (int t = 0; t < D; ++t) {
         const u32* dig = digits + (ct * D + t) * n;
         auto first = [&](int r, int uu, int k) -> V {
-            if constexpr (PREFETCH) {
+            if constexpr (PREFETCH && C == 0) {
                 (void)r;
                 return ntt::to_fp(lift(pf[uu * E0 + k]));
+            } else if constexpr (PREFETCH) {
+                (void)r;
+                const double x0 = ntt::to_fp(lift(pf[(uu * E0 + k) * 2])), x1 = ntt::to_fp(lift(pf[(uu * E0 + k) * 2 + 1]));
+                const double v = ntt::fmodmul(x1, w_col, ar.q, ar.qinv);
+                return b == 0 ? x0 + v : x0 - v;
             } else if constexpr (FP) {
                 return column_value_fp<LOGN, C, LIFT>(dig, R.fwd_f + (static_cast<long long>(i) << LOGN), q, ar.q, ar.qinv, r, b);
             } else {

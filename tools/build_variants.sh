@@ -11,6 +11,10 @@ V[batch]="-DHECNN_NTT_BATCH=1"
 V[nomac]="-DHECNN_KS_ABLATE_MAC"
 V[nosplit]="-DHECNN_NTT_SPLIT=0"
 V[col512]="-DHECNN_KS_MAXT_COL=512"
+V[tcmin4]="-DHECNN_TC_MIN_KSTEPS=4"
+V[rsu4]="-DHECNN_RESCALE_UNROLL=4"
+V[pfcol]="-DHECNN_KS_PF_COL=1 -DHECNN_KS_MAXT_COL=512"
+V[pfcol1k]="-DHECNN_KS_PF_COL=1"
 V[tc34]="-DHECNN_TC_STAGES=3 -DHECNN_TC_GDEPTH=4"
 V[tc25]="-DHECNN_TC_STAGES=2 -DHECNN_TC_GDEPTH=5"
 V[nosacc]="-DHECNN_KS_ABLATE_SACC"
