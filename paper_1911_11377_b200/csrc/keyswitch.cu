@@ -116,6 +116,51 @@ __global__ void __launch_bounds__(128) k_crt_digits(DevRing R, const u64* __rest
 
 __device__ __forceinline__ u64 lift_digit(u32 v, u64 q) { return v < q ? v : v % q; }
 
+// ---- tensor memory / bulk-copy helpers (FP64 path with HECNN_KS_TMEM) -------
+__device__ __forceinline__ uint32_t ks_saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void ks_mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{.reg .pred P1;\n"
+        "WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;}" ::"r"(ks_saddr(b)),
+        "r"(parity)
+        : "memory");
+}
+// one bulk copy of `bytes` from global into shared memory, completing on `bar`
+[[maybe_unused]] __device__ __forceinline__ void ks_bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of dst before the async write
+    asm volatile("{.reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;}" ::"r"(ks_saddr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(ks_saddr(dst)),
+                 "l"(src), "r"(bytes), "r"(ks_saddr(bar))
+                 : "memory");
+}
+// EL doubles of this thread's TMEM lane at column `col` (2 x 32-bit columns each)
+template <int EL>
+__device__ __forceinline__ void tmem_ld_d(uint32_t addr, double (&v)[EL]) {
+    static_assert(EL == 4, "4-word units");
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < EL; ++k) v[k] = __hiloint2double(static_cast<int>(r[2 * k + 1]), static_cast<int>(r[2 * k]));
+}
+template <int EL>
+__device__ __forceinline__ void tmem_st_d(uint32_t addr, const double (&v)[EL]) {
+    static_assert(EL == 4, "4-word units");
+    uint32_t r[8];
+#pragma unroll
+    for (int k = 0; k < EL; ++k) {
+        r[2 * k] = static_cast<uint32_t>(__double2loint(v[k]));
+        r[2 * k + 1] = static_cast<uint32_t>(__double2hiint(v[k]));
+    }
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
 // Value at block-local position r after the C column stages (block b): only
 // the butterflies on the path to output b are evaluated (2^C - 1 products).
 template <int LOGN, int C>
@@ -229,8 +274,41 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     const long long blk_off = static_cast<long long>(b) << LOGB;
     const ulonglong2* itw = R.fwd + (static_cast<long long>(i) << LOGN);  // integer twiddles for the column stages
 
+#ifndef HECNN_KS_TMEM
+#define HECNN_KS_TMEM 1
+#endif
+    // TM: the c1 accumulators live in tensor memory (thread-private lane
+    // columns, tcgen05.ld/st) and the shared-memory region they used holds
+    // the digit's b_t slice, bulk-copied in while the previous digit's
+    // transform runs; a_t still streams from L2
+    constexpr bool TM = FP && PRIV && HECNN_KS_TMEM && EL == 4;
     TW* stw = reinterpret_cast<TW*>(smem + B);
-    double* sacc = reinterpret_cast<double*>(smem + 2 * B);  // FP path: c1 accumulators
+    double* sacc = reinterpret_cast<double*>(smem + 2 * B);  // FP path: c1 accumulators (TM: b_t staging)
+    uint64_t* bbar = reinterpret_cast<uint64_t*>(smem + 3 * B);
+    constexpr int TCOLS = (T / 128) * 2 * PL * EL <= 32 ? 32 : ((T / 128) * 2 * PL * EL <= 64 ? 64 : ((T / 128) * 2 * PL * EL <= 128 ? 128 : 256));
+    uint32_t tm_lane = 0;
+    if constexpr (TM) {
+        __shared__ uint32_t tm_slot;
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ks_saddr(&tm_slot)), "n"(TCOLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(bbar)));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int w = threadIdx.x >> 5;
+        tm_lane = tm_slot + (static_cast<uint32_t>((w & 3) * 32) << 16) + static_cast<uint32_t>((w >> 2) * 2 * PL * EL);
+        const double z[EL] = {};
+#pragma unroll
+        for (int uu = 0; uu < PL; ++uu) tmem_st_d<EL>(tm_lane + uu * 2 * EL, z);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (threadIdx.x == 0)
+            ks_bulk_load(sacc, key.evk_f + key.ioff + blk_off, B * 8, bbar);  // b_0 of this block
+    }
     auto slot = [&](int idx, int uu, int k) -> int {
         if constexpr (PRIV) { (void)idx; return (uu * EL + k) * T + threadIdx.x; }
         else { (void)uu; (void)k; return ntt::swz(idx); }
@@ -239,7 +317,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         const int s = 31 - __clz(j), m = j - (1 << s);
         stw[j] = tw[(1 << (s + C)) + (b << s) + m];
     }
-    if constexpr (FP) {
+    if constexpr (FP && !TM) {
         for (int j = threadIdx.x; j < B; j += T) sacc[j] = 0.0;
     }
     __syncthreads();  // table complete before the first round reads it
@@ -306,8 +384,14 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                                                   key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
                                                                         [&](int kk) -> double& { return a0[uu * EL + kk]; });
 #else
-                                                  key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
-                                                                        [&](int kk) -> double& { return sacc[slot(base + kk, uu, kk)]; });
+                                                  if constexpr (TM) {
+                                                      ks_mbar_wait(bbar, t & 1);  // b_t landed
+                                                      key.template unit_tm<EL>(t, blk_off + base, stash, a0 + uu * EL,
+                                                                               sacc + base, tm_lane + uu * 2 * EL);
+                                                  } else {
+                                                      key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
+                                                                            [&](int kk) -> double& { return sacc[slot(base + kk, uu, kk)]; });
+                                                  }
 #endif
                                               } else {
                                                   key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
@@ -320,7 +404,12 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                                           // inputs land while this one is transformed
                                           if (t + 1 < D) prefetch(t + 1);
                                       });
+        if constexpr (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         __syncthreads();  // the next digit's first round overwrites shared memory
+        if constexpr (TM) {
+            if (threadIdx.x == 0 && t + 1 < D)
+                ks_bulk_load(sacc, key.evk_f + (2LL * (t + 1)) * key.key_stride + key.ioff + blk_off, B * 8, bbar);
+        }
     }
     const int limbs = level + 1;
     u64* o0 = acc01 + ((ct * 2) * limbs + i) * n + blk_off;
@@ -340,6 +429,8 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         const int u = threadIdx.x + uu * T;
         if (UL % T != 0 && u >= UL) break;
         const int base = ntt::fwd_last_base<LOGB, LOGE, T>(uu);
+        double c1u[EL];
+        if constexpr (TM) tmem_ld_d<EL>(tm_lane + uu * 2 * EL, c1u);
 #pragma unroll
         for (int k = 0; k < EL; k += 2) {
             const int idx = base + k;
@@ -348,7 +439,8 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
             for (int h = 0; h < 2; ++h) {
                 if constexpr (FP) {
                     r0[h] = ntt::fcanon(a0[uu * EL + k + h], ar.q, ar.qinv);
-                    r1[h] = ntt::fcanon(sacc[slot(idx + h, uu, k + h)], ar.q, ar.qinv);
+                    if constexpr (TM) r1[h] = ntt::fcanon(c1u[k + h], ar.q, ar.qinv);
+                    else r1[h] = ntt::fcanon(sacc[slot(idx + h, uu, k + h)], ar.q, ar.qinv);
                 } else {
                     r0[h] = reduce_2q(a0[uu * EL + k + h], q);
                     r1[h] = reduce_2q(a1[uu * EL + k + h], q);
@@ -382,6 +474,14 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
             *reinterpret_cast<ulonglong2*>(o1 + idx) = make_ulonglong2(add_mod(b1[0], r1[0], q), add_mod(b1[1], r1[1], q));
         }
     }
+    if constexpr (TM) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_lane), "n"(TCOLS));  // warp 0: the allocated base
+        }
+    }
 }
 
 // Unit-wise evk MACs: EL consecutive NTT outputs v[] at key positions
@@ -405,6 +505,31 @@ struct FpKey {
             s1(2 * k) += ntt::fmodmul(v[2 * k], wa[k].x, q, qinv);
             s1(2 * k + 1) += ntt::fmodmul(v[2 * k + 1], wa[k].y, q, qinv);
         }
+    }
+    // b_t from the shared-memory stage, a_t from L2, c1 read-modify-written in
+    // this thread's tensor-memory columns
+    template <int EL>
+    __device__ __forceinline__ void unit_tm(int t, long long pos, const double* v, double* s0, const double* bst,
+                                            uint32_t tcol) const {
+        const double2* ka = reinterpret_cast<const double2*>(evk_f + (2LL * t + 1) * key_stride + ioff + pos);
+        double2 wa[EL / 2];
+#pragma unroll
+        for (int k = 0; k < EL / 2; ++k) wa[k] = __ldg(ka + k);
+        const double2* kb = reinterpret_cast<const double2*>(bst);
+#pragma unroll
+        for (int k = 0; k < EL / 2; ++k) {
+            const double2 wb = kb[k];
+            s0[2 * k] += ntt::fmodmul(v[2 * k], wb.x, q, qinv);
+            s0[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], wb.y, q, qinv);
+        }
+        double c1[EL];
+        tmem_ld_d<EL>(tcol, c1);
+#pragma unroll
+        for (int k = 0; k < EL / 2; ++k) {
+            c1[2 * k] += ntt::fmodmul(v[2 * k], wa[k].x, q, qinv);
+            c1[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], wa[k].y, q, qinv);
+        }
+        tmem_st_d<EL>(tcol, c1);
     }
 };
 
@@ -510,7 +635,7 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
     auto kint = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false, false>;
     // data + staged twiddles (u64 Shoup pairs on the integer path; double
     // twiddles + c1 accumulators on the FP64 path)
-    const int smem = P::B * (8 + 16);
+    const int smem = P::B * (8 + 16) + 64;  // + the b_t stage's mbarrier
     static bool init = (smem > 48 * 1024
                             ? (cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, true>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),

@@ -15,6 +15,10 @@ V[tcmin4]="-DHECNN_TC_MIN_KSTEPS=4"
 V[rsu4]="-DHECNN_RESCALE_UNROLL=4"
 V[pfcol]="-DHECNN_KS_PF_COL=1 -DHECNN_KS_MAXT_COL=512"
 V[pfcol1k]="-DHECNN_KS_PF_COL=1"
+V[n256m4]="-DHECNN_NTT_MAXT=256 -DHECNN_NTT_MINB=4"
+V[n1024]="-DHECNN_NTT_MAXT=1024 -DHECNN_NTT_MINB=1"
+V[ne4]="-DHECNN_NTT_LOGE=4"
+V[notm]="-DHECNN_KS_TMEM=0"
 V[tc34]="-DHECNN_TC_STAGES=3 -DHECNN_TC_GDEPTH=4"
 V[tc25]="-DHECNN_TC_STAGES=2 -DHECNN_TC_GDEPTH=5"
 V[nosacc]="-DHECNN_KS_ABLATE_SACC"
