@@ -282,10 +282,15 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     // the digit's b_t slice, bulk-copied in while the previous digit's
     // transform runs; a_t still streams from L2
     constexpr bool TM = FP && PRIV && HECNN_KS_TMEM && EL == 4;
+    // TM2: c0 in tensor memory too; the registers it frees hold this thread's
+    // a_t words, loaded one digit ahead, so the last round reads no evk from L2
+    constexpr bool TM2 = TM && HECNN_KS_TMEM >= 2;
+    constexpr int TCW = (TM2 ? 4 : 2) * PL * EL;  // tensor-memory columns per thread
     TW* stw = reinterpret_cast<TW*>(smem + B);
     double* sacc = reinterpret_cast<double*>(smem + 2 * B);  // FP path: c1 accumulators (TM: b_t staging)
     uint64_t* bbar = reinterpret_cast<uint64_t*>(smem + 3 * B);
-    constexpr int TCOLS = (T / 128) * 2 * PL * EL <= 32 ? 32 : ((T / 128) * 2 * PL * EL <= 64 ? 64 : ((T / 128) * 2 * PL * EL <= 128 ? 128 : 256));
+    constexpr int TNEED = (T / 128) * TCW;
+    constexpr int TCOLS = TNEED <= 32 ? 32 : (TNEED <= 64 ? 64 : (TNEED <= 128 ? 128 : (TNEED <= 256 ? 256 : 512)));
     uint32_t tm_lane = 0;
     if constexpr (TM) {
         __shared__ uint32_t tm_slot;
@@ -301,10 +306,10 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int w = threadIdx.x >> 5;
-        tm_lane = tm_slot + (static_cast<uint32_t>((w & 3) * 32) << 16) + static_cast<uint32_t>((w >> 2) * 2 * PL * EL);
+        tm_lane = tm_slot + (static_cast<uint32_t>((w & 3) * 32) << 16) + static_cast<uint32_t>((w >> 2) * TCW);
         const double z[EL] = {};
 #pragma unroll
-        for (int uu = 0; uu < PL; ++uu) tmem_st_d<EL>(tm_lane + uu * 2 * EL, z);
+        for (int uu = 0; uu < TCW / (2 * EL); ++uu) tmem_st_d<EL>(tm_lane + uu * 2 * EL, z);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         if (threadIdx.x == 0)
             ks_bulk_load(sacc, key.evk_f + key.ioff + blk_off, B * 8, bbar);  // b_0 of this block
@@ -322,9 +327,27 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     }
     __syncthreads();  // table complete before the first round reads it
 
-    V a0[PL * EL], a1[FP ? 1 : PL * EL];
+    V a0[PL * EL], a1[FP ? 1 : PL * EL];  // TM2: a0 holds the a_t words of the last-round units
 #pragma unroll
     for (int k = 0; k < PL * EL; ++k) a0[k] = V(0);
+    // c1 (TM) and c0 (TM2) tensor-memory columns of unit slot uu
+    const uint32_t c1col = tm_lane + (TM2 ? 2 * PL * EL : 0);
+    auto load_a = [&](int t) {
+        if constexpr (TM2) {
+#pragma unroll
+            for (int uu = 0; uu < PL; ++uu) {
+                const double2* ka = reinterpret_cast<const double2*>(key.evk_f + (2LL * t + 1) * key.key_stride + key.ioff + blk_off +
+                                                                     ntt::fwd_last_base<LOGB, LOGE, T>(uu));
+#pragma unroll
+                for (int k = 0; k < EL / 2; ++k) {
+                    const double2 w2 = __ldg(ka + k);
+                    a0[uu * EL + 2 * k] = w2.x;
+                    a0[uu * EL + 2 * k + 1] = w2.y;
+                }
+            }
+        }
+    };
+    if constexpr (TM2) load_a(0);
 #pragma unroll
     for (int k = 0; k < (FP ? 1 : PL * EL); ++k) a1[k] = V(0);
 
@@ -384,7 +407,11 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                                                   key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
                                                                         [&](int kk) -> double& { return a0[uu * EL + kk]; });
 #else
-                                                  if constexpr (TM) {
+                                                  if constexpr (TM2) {
+                                                      ks_mbar_wait(bbar, t & 1);  // b_t landed
+                                                      key.template unit_tm2<EL>(t, blk_off + base, stash, a0 + uu * EL, sacc + base,
+                                                                                tm_lane + uu * 2 * EL, c1col + uu * 2 * EL, t + 1 < D);
+                                                  } else if constexpr (TM) {
                                                       ks_mbar_wait(bbar, t & 1);  // b_t landed
                                                       key.template unit_tm<EL>(t, blk_off + base, stash, a0 + uu * EL,
                                                                                sacc + base, tm_lane + uu * 2 * EL);
@@ -429,8 +456,9 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         const int u = threadIdx.x + uu * T;
         if (UL % T != 0 && u >= UL) break;
         const int base = ntt::fwd_last_base<LOGB, LOGE, T>(uu);
-        double c1u[EL];
-        if constexpr (TM) tmem_ld_d<EL>(tm_lane + uu * 2 * EL, c1u);
+        double c1u[EL], c0u[EL];
+        if constexpr (TM) tmem_ld_d<EL>(c1col + uu * 2 * EL, c1u);
+        if constexpr (TM2) tmem_ld_d<EL>(tm_lane + uu * 2 * EL, c0u);
 #pragma unroll
         for (int k = 0; k < EL; k += 2) {
             const int idx = base + k;
@@ -438,7 +466,8 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if constexpr (FP) {
-                    r0[h] = ntt::fcanon(a0[uu * EL + k + h], ar.q, ar.qinv);
+                    if constexpr (TM2) r0[h] = ntt::fcanon(c0u[k + h], ar.q, ar.qinv);
+                    else r0[h] = ntt::fcanon(a0[uu * EL + k + h], ar.q, ar.qinv);
                     if constexpr (TM) r1[h] = ntt::fcanon(c1u[k + h], ar.q, ar.qinv);
                     else r1[h] = ntt::fcanon(sacc[slot(idx + h, uu, k + h)], ar.q, ar.qinv);
                 } else {
@@ -504,6 +533,35 @@ struct FpKey {
             s0[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], wb[k].y, q, qinv);
             s1(2 * k) += ntt::fmodmul(v[2 * k], wa[k].x, q, qinv);
             s1(2 * k + 1) += ntt::fmodmul(v[2 * k + 1], wa[k].y, q, qinv);
+        }
+    }
+    // TM2: b_t from the shared-memory stage, a_t from registers (reloaded
+    // with a_{t+1} for the next digit), c0 and c1 in tensor memory
+    template <int EL>
+    __device__ __forceinline__ void unit_tm2(int t, long long pos, const double* v, double* a, const double* bst,
+                                             uint32_t c0col, uint32_t c1col, bool more) const {
+        double c0[EL], c1[EL];
+        tmem_ld_d<EL>(c0col, c0);
+        tmem_ld_d<EL>(c1col, c1);
+        const double2* kb = reinterpret_cast<const double2*>(bst);
+#pragma unroll
+        for (int k = 0; k < EL / 2; ++k) {
+            const double2 wb = kb[k];
+            c0[2 * k] += ntt::fmodmul(v[2 * k], wb.x, q, qinv);
+            c0[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], wb.y, q, qinv);
+            c1[2 * k] += ntt::fmodmul(v[2 * k], a[2 * k], q, qinv);
+            c1[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], a[2 * k + 1], q, qinv);
+        }
+        tmem_st_d<EL>(c0col, c0);
+        tmem_st_d<EL>(c1col, c1);
+        if (more) {  // this unit's a_{t+1}, in flight until the next digit's last round
+            const double2* ka = reinterpret_cast<const double2*>(evk_f + (2LL * t + 3) * key_stride + ioff + pos);
+#pragma unroll
+            for (int k = 0; k < EL / 2; ++k) {
+                const double2 w2 = __ldg(ka + k);
+                a[2 * k] = w2.x;
+                a[2 * k + 1] = w2.y;
+            }
         }
     }
     // b_t from the shared-memory stage, a_t from L2, c1 read-modify-written in
