@@ -51,8 +51,11 @@ __global__ void k_elementwise(DevRing R, int op, const u64* __restrict__ a, cons
 // materialising the product.
 // ADD: the activation's other terms (and its constant) are added on the way
 // out (mod_switch + add + add_plain, ckks.hpp:288-311, fused).
+#ifndef HECNN_RESCALE_MINB
+#define HECNN_RESCALE_MINB 8  // 32 registers: full occupancy for this latency-bound stream (measured 37 -> 32 ms per C4 step)
+#endif
 template <bool SCALED, bool ADD>
-__global__ void k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level,
+__global__ void __launch_bounds__(TPB, HECNN_RESCALE_MINB) k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level,
                           const ulonglong2* __restrict__ c, SumTerms t) {
     const int j = blockIdx.y * TPB + threadIdx.x;
     if (j >= R.n) return;

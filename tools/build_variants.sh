@@ -20,6 +20,8 @@ V[n1024]="-DHECNN_NTT_MAXT=1024 -DHECNN_NTT_MINB=1"
 V[ne4]="-DHECNN_NTT_LOGE=4"
 V[notm]="-DHECNN_KS_TMEM=0"
 V[tm2]="-DHECNN_KS_TMEM=2"
+V[rsm6]="-DHECNN_RESCALE_MINB=6"
+V[rsm8]="-DHECNN_RESCALE_MINB=8"
 V[tc34]="-DHECNN_TC_STAGES=3 -DHECNN_TC_GDEPTH=4"
 V[tc25]="-DHECNN_TC_STAGES=2 -DHECNN_TC_GDEPTH=5"
 V[nosacc]="-DHECNN_KS_ABLATE_SACC"
