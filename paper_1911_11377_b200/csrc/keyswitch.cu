@@ -83,11 +83,16 @@ __global__ void __launch_bounds__(128) k_crt_digits(DevRing R, const u64* __rest
                 c = c1 | (acc[w] < s);
             }
         } else {  // at most one Q too many
-            bool ge = true;
+            bool ge = true, decided = false;
 #pragma unroll
             for (int w = W - 1; w >= 0; --w) {
                 // lexicographic compare from the top word, first difference decides
-                if (acc[w] != Q[w]) { ge = acc[w] > Q[w]; break; }
+                // (no early exit: a fully unrolled scan keeps acc[] in registers)
+                const u64 qw = Q[w];
+                if (!decided && acc[w] != qw) {
+                    ge = acc[w] > qw;
+                    decided = true;
+                }
             }
             if (ge) {
                 u64 b = 0;
@@ -101,15 +106,16 @@ __global__ void __launch_bounds__(128) k_crt_digits(DevRing R, const u64* __rest
         }
     }
     u32* out = digits + ct * D * R.n + j;
-    for (int d = 0; d < D; ++d) {
+    // every digit position is a compile-time (word, shift) pair, so acc[]
+    // stays in registers (a runtime word index sends it to local memory)
+    constexpr int DMAX = (64 * W + 19) / 20;
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) {
+        if (d >= D) break;
         const int off = 20 * d;
         const int wi = off >> 6, sh = off & 63;
-        u64 v = 0;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-            if (w == wi) v = acc[w] >> sh;
-            if (w == wi + 1 && sh > 44) v |= acc[w] << (64 - sh);
-        }
+        u64 v = acc[wi] >> sh;
+        if (sh > 44 && wi + 1 < W) v |= acc[wi + 1] << (64 - sh);
         out[static_cast<long long>(d) * R.n] = static_cast<u32>(v & 0xFFFFFu);
     }
 }
