@@ -22,6 +22,8 @@ V[notm]="-DHECNN_KS_TMEM=0"
 V[tm2]="-DHECNN_KS_TMEM=2"
 V[rsm6]="-DHECNN_RESCALE_MINB=6"
 V[rsm8]="-DHECNN_RESCALE_MINB=8"
+V[dm5]="-DHECNN_DIRECT_MINB=5"
+V[dm6]="-DHECNN_DIRECT_MINB=6"
 V[tc34]="-DHECNN_TC_STAGES=3 -DHECNN_TC_GDEPTH=4"
 V[tc25]="-DHECNN_TC_STAGES=2 -DHECNN_TC_GDEPTH=5"
 V[nosacc]="-DHECNN_KS_ABLATE_SACC"
