@@ -154,6 +154,26 @@ __device__ __forceinline__ void tmem_ld_d(uint32_t addr, double (&v)[EL]) {
     for (int k = 0; k < EL; ++k) v[k] = __hiloint2double(static_cast<int>(r[2 * k + 1]), static_cast<int>(r[2 * k]));
 }
 template <int EL>
+__device__ __forceinline__ void tmem_ld_u(uint32_t addr, u64 (&v)[EL]) {
+    static_assert(EL == 4, "4-word units");
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < EL; ++k) v[k] = (static_cast<u64>(r[2 * k + 1]) << 32) | r[2 * k];
+}
+template <int EL>
+__device__ __forceinline__ void tmem_st_u(uint32_t addr, const u64 (&v)[EL]) {
+    static_assert(EL == 4, "4-word units");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
+                 "r"(static_cast<uint32_t>(v[0])), "r"(static_cast<uint32_t>(v[0] >> 32)), "r"(static_cast<uint32_t>(v[1])),
+                 "r"(static_cast<uint32_t>(v[1] >> 32)), "r"(static_cast<uint32_t>(v[2])), "r"(static_cast<uint32_t>(v[2] >> 32)),
+                 "r"(static_cast<uint32_t>(v[3])), "r"(static_cast<uint32_t>(v[3] >> 32))
+                 : "memory");
+}
+template <int EL>
 __device__ __forceinline__ void tmem_st_d(uint32_t addr, const double (&v)[EL]) {
     static_assert(EL == 4, "4-word units");
     uint32_t r[8];
@@ -291,6 +311,10 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     // TM2: c0 in tensor memory too; the registers it frees hold this thread's
     // a_t words, loaded one digit ahead, so the last round reads no evk from L2
     constexpr bool TM2 = TM && HECNN_KS_TMEM >= 2;
+    // TMI: the integer (60-bit limb) path keeps its c1 accumulators in tensor
+    // memory as well (its 16-byte Shoup twiddles leave no shared memory to stage evk)
+    constexpr bool TMI = !FP && PRIV && HECNN_KS_TMEM && EL == 4;
+    constexpr bool USE_TMEM = TM || TMI;
     constexpr int TCW = (TM2 ? 4 : 2) * PL * EL;  // tensor-memory columns per thread
     TW* stw = reinterpret_cast<TW*>(smem + B);
     double* sacc = reinterpret_cast<double*>(smem + 2 * B);  // FP path: c1 accumulators (TM: b_t staging)
@@ -298,13 +322,13 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     constexpr int TNEED = (T / 128) * TCW;
     constexpr int TCOLS = TNEED <= 32 ? 32 : (TNEED <= 64 ? 64 : (TNEED <= 128 ? 128 : (TNEED <= 256 ? 256 : 512)));
     uint32_t tm_lane = 0;
-    if constexpr (TM) {
+    if constexpr (USE_TMEM) {
         __shared__ uint32_t tm_slot;
         if (threadIdx.x < 32) {
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ks_saddr(&tm_slot)), "n"(TCOLS));
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
         }
-        if (threadIdx.x == 0) {
+        if (TM && threadIdx.x == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(bbar)));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
@@ -313,12 +337,13 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int w = threadIdx.x >> 5;
         tm_lane = tm_slot + (static_cast<uint32_t>((w & 3) * 32) << 16) + static_cast<uint32_t>((w >> 2) * TCW);
-        const double z[EL] = {};
+        const u64 z[EL] = {};
 #pragma unroll
-        for (int uu = 0; uu < TCW / (2 * EL); ++uu) tmem_st_d<EL>(tm_lane + uu * 2 * EL, z);
+        for (int uu = 0; uu < TCW / (2 * EL); ++uu) tmem_st_u<EL>(tm_lane + uu * 2 * EL, z);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        if (threadIdx.x == 0)
-            ks_bulk_load(sacc, key.evk_f + key.ioff + blk_off, B * 8, bbar);  // b_0 of this block
+        if constexpr (TM) {
+            if (threadIdx.x == 0) ks_bulk_load(sacc, key.evk_f + key.ioff + blk_off, B * 8, bbar);  // b_0 of this block
+        }
     }
     auto slot = [&](int idx, int uu, int k) -> int {
         if constexpr (PRIV) { (void)idx; return (uu * EL + k) * T + threadIdx.x; }
@@ -333,7 +358,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     }
     __syncthreads();  // table complete before the first round reads it
 
-    V a0[PL * EL], a1[FP ? 1 : PL * EL];  // TM2: a0 holds the a_t words of the last-round units
+    V a0[PL * EL], a1[(FP || TMI) ? 1 : PL * EL];  // TM2: a0 holds the a_t words of the last-round units
 #pragma unroll
     for (int k = 0; k < PL * EL; ++k) a0[k] = V(0);
     // c1 (TM) and c0 (TM2) tensor-memory columns of unit slot uu
@@ -355,7 +380,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     };
     if constexpr (TM2) load_a(0);
 #pragma unroll
-    for (int k = 0; k < (FP ? 1 : PL * EL); ++k) a1[k] = V(0);
+    for (int k = 0; k < ((FP || TMI) ? 1 : PL * EL); ++k) a1[k] = V(0);
 
     u32 pf[PREFETCH ? P0 * E0 * PFW : 1];
     auto prefetch = [&](int t) {
@@ -426,6 +451,8 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                                                                             [&](int kk) -> double& { return sacc[slot(base + kk, uu, kk)]; });
                                                   }
 #endif
+                                              } else if constexpr (TMI) {
+                                                  key.template unit_tm<EL>(t, blk_off + base, stash, a0 + uu * EL, tm_lane + uu * 2 * EL);
                                               } else {
                                                   key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
                                                                         [&](int kk) -> u64& { return a1[uu * EL + kk]; });
@@ -437,7 +464,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                                           // inputs land while this one is transformed
                                           if (t + 1 < D) prefetch(t + 1);
                                       });
-        if constexpr (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if constexpr (USE_TMEM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         __syncthreads();  // the next digit's first round overwrites shared memory
         if constexpr (TM) {
             if (threadIdx.x == 0 && t + 1 < D)
@@ -463,6 +490,8 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         if (UL % T != 0 && u >= UL) break;
         const int base = ntt::fwd_last_base<LOGB, LOGE, T>(uu);
         double c1u[EL], c0u[EL];
+        u64 c1i[EL];
+        if constexpr (TMI) tmem_ld_u<EL>(tm_lane + uu * 2 * EL, c1i);
         if constexpr (TM) tmem_ld_d<EL>(c1col + uu * 2 * EL, c1u);
         if constexpr (TM2) tmem_ld_d<EL>(tm_lane + uu * 2 * EL, c0u);
 #pragma unroll
@@ -478,7 +507,8 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                     else r1[h] = ntt::fcanon(sacc[slot(idx + h, uu, k + h)], ar.q, ar.qinv);
                 } else {
                     r0[h] = reduce_2q(a0[uu * EL + k + h], q);
-                    r1[h] = reduce_2q(a1[uu * EL + k + h], q);
+                    if constexpr (TMI) r1[h] = reduce_2q(c1i[k + h], q);
+                    else r1[h] = reduce_2q(a1[uu * EL + k + h], q);
                 }
             }
             const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(o0 + idx);
@@ -509,7 +539,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
             *reinterpret_cast<ulonglong2*>(o1 + idx) = make_ulonglong2(add_mod(b1[0], r1[0], q), add_mod(b1[1], r1[1], q));
         }
     }
-    if constexpr (TM) {
+    if constexpr (USE_TMEM) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         if (threadIdx.x < 32) {
@@ -622,6 +652,14 @@ struct IntKey {
                 r1 = x1 >= two_q ? x1 - two_q : x1;
             }
         }
+    }
+    // c1 read-modify-written in this thread's tensor-memory columns
+    template <int EL>
+    __device__ __forceinline__ void unit_tm(int t, long long pos, const u64* v, u64* s0, uint32_t tcol) const {
+        u64 c1[EL];
+        tmem_ld_u<EL>(tcol, c1);
+        unit<EL>(t, pos, v, s0, [&](int e) -> u64& { return c1[e]; });
+        tmem_st_u<EL>(tcol, c1);
     }
 };
 
