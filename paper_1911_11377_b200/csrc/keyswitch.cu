@@ -483,7 +483,25 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         if constexpr (FP) return ntt::fcanon(ntt::fmodmul(ntt::to_fp(a), ntt::to_fp(c), ar.q, ar.qinv), ar.q, ar.qinv);
         else return mul_mod(a, c, mc);
     };
-    // each unit's EL words are contiguous: 16-byte loads and stores
+    // each unit's EL words are contiguous: 16-byte loads and stores. With
+    // whole units per thread, every unit's (x0, x1) words are loaded before
+    // the first is used (their HBM latency overlaps instead of serialising)
+#ifndef HECNN_KS_EPI_PF
+#define HECNN_KS_EPI_PF 1
+#endif
+    constexpr bool EPF = HECNN_KS_EPI_PF && PRIV && T <= 512;  // 1024-thread blocks (64 registers) spill with it
+    ulonglong2 xpre[EPF ? PL * EL : 1];
+    if constexpr (EPF) {
+#pragma unroll
+        for (int uu = 0; uu < PL; ++uu) {
+            const int base = ntt::fwd_last_base<LOGB, LOGE, T>(uu);
+#pragma unroll
+            for (int k = 0; k < EL; k += 2) {
+                xpre[uu * EL + k] = *reinterpret_cast<const ulonglong2*>(o0 + base + k);
+                xpre[uu * EL + k + 1] = *reinterpret_cast<const ulonglong2*>(o1 + base + k);
+            }
+        }
+    }
 #pragma unroll
     for (int uu = 0; uu < PL; ++uu) {
         const int u = threadIdx.x + uu * T;
@@ -511,8 +529,8 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                     else r1[h] = reduce_2q(a1[uu * EL + k + h], q);
                 }
             }
-            const ulonglong2 x0 = *reinterpret_cast<const ulonglong2*>(o0 + idx);
-            const ulonglong2 x1 = *reinterpret_cast<const ulonglong2*>(o1 + idx);
+            const ulonglong2 x0 = EPF ? xpre[uu * EL + k] : *reinterpret_cast<const ulonglong2*>(o0 + idx);
+            const ulonglong2 x1 = EPF ? xpre[uu * EL + k + 1] : *reinterpret_cast<const ulonglong2*>(o1 + idx);
             u64 b0[2], b1[2];
             const u64 xa[2] = {x0.x, x0.y}, xb[2] = {x1.x, x1.y};
             if (mode == 0) {  // acc01 already holds (d0, d1)
