@@ -287,8 +287,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_conv_imma(DevRing R, ImmaMac g, 
 // own gathered words through a private cp.async ring and the weight fragments
 // come straight from L2; with 1-8 steps per output there is nothing to
 // amortise CTA-wide staging against.
-#ifndef HECNN_DIRECT_MINB
-#define HECNN_DIRECT_MINB 1
+// occupancy knob for experiments: a minimum-blocks bound changes the register
+// allocation even at 1 (the default leaves it to the compiler: 96-128 registers)
+#ifdef HECNN_DIRECT_MINB
+#define HECNN_DIRECT_LB __launch_bounds__(WARPS * 32, HECNN_DIRECT_MINB)
+#else
+#define HECNN_DIRECT_LB __launch_bounds__(WARPS * 32)
 #endif
 namespace direct {
 constexpr int WARPS = 4;
@@ -380,7 +384,7 @@ __device__ __forceinline__ void byte_planes(const u64 (&w)[4], unsigned (&p)[NA]
 // SHORT: every accumulation chunk has <= 48 steps (three shift classes per
 // exact double in the fold); otherwise classes are folded in pairs.
 template <int MT, bool SHORT>
-__global__ void __launch_bounds__(WARPS * 32, HECNN_DIRECT_MINB) k_conv_imma_direct(DevRing R, ImmaMac g, const u64* __restrict__ x,
+__global__ void HECNN_DIRECT_LB k_conv_imma_direct(DevRing R, ImmaMac g, const u64* __restrict__ x,
                                                          u64* __restrict__ y, int level, int limb0, int nl,
                                                          int groups, int pg) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -492,7 +496,7 @@ __global__ void __launch_bounds__(WARPS * 32, HECNN_DIRECT_MINB) k_conv_imma_dir
 // unsigned bytes; 48 s8 x u8 products per tap in 13 shift classes, each an
 // exact int32 sum (|D_s| <= 6 * 128 * 255 * 6144 < 2^31). The epilogue adds
 // D_s (2^8s mod q) with 64-bit Shoup multiplies.
-__global__ void __launch_bounds__(WARPS * 32, HECNN_DIRECT_MINB) k_conv_imma_wide_direct(DevRing R, ImmaMac g, const u64* __restrict__ x,
+__global__ void HECNN_DIRECT_LB k_conv_imma_wide_direct(DevRing R, ImmaMac g, const u64* __restrict__ x,
                                                               u64* __restrict__ y, int level, int limb0, int nl,
                                                               int groups, int pg) {
     constexpr int NA = 8, NB = 6, NS = NA + NB - 1;
