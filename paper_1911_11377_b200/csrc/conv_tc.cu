@@ -198,33 +198,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
         tc_fence_before();
         mbar_arrive(acc_free);  // the accumulator is ready for the MMAs
 
-        const u64* xcol = x + col_base + r;
+#ifndef HECNN_TC_G16
+#define HECNN_TC_G16 0
+#endif
+        // producer mapping: G16 -> a thread owns two adjacent coefficient rows and
+        // 8 taps (16-byte cp.async per tap), else one row and 16 taps (8-byte copies)
+        constexpr bool G16 = HECNN_TC_G16;
+        constexpr int ROWS = G16 ? 2 : 1, TAPS = G16 ? 8 : 16;
+        const int prow = G16 ? 2 * (tid & 63) : r;         // first row of this thread
+        const int pk0 = G16 ? 8 * (tid >> 6) : 16 * kh;     // first tap of this thread within a step
+        const u64* xcol = x + col_base + prow;
         const uint4* wt = (WIDE ? g.wtc_wide : g.wtc + static_cast<long long>(i) * tiles * ks_n * (S::B_BYTES / 16)) +
                           static_cast<long long>(ot) * ks_n * (S::B_BYTES / 16);
-        // this thread's 16 tap words of step ks, gathered with cp.async into the
+        // this thread's tap words of step ks, gathered with cp.async into the
         // staging ring (padding taps, -1, zero-fill); each thread reads back
         // only its own words, so cp.async.wait_group alone orders the ring.
         // Steps are gathered in order; the tap indices of the next one are
         // loaded one gather ahead so their latency is off the issue path.
-        const int* src_p = g.src + static_cast<long long>(p) * g.kpad + kh * 16;
-        int4 taps[4];
+        const int* src_p = g.src + static_cast<long long>(p) * g.kpad + pk0;
+        int4 taps[TAPS / 4];
         auto load_taps = [&](int ks) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) taps[c] = __ldg(reinterpret_cast<const int4*>(src_p + ks * 32 + 4 * c));
+            for (int c = 0; c < TAPS / 4; ++c) taps[c] = __ldg(reinterpret_cast<const int4*>(src_p + ks * 32 + 4 * c));
         };
         load_taps(0);
         auto gather = [&](int ks) {
-            u64* dst = gstage + (ks % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid;
-            int tt[16];
+            // staging slot: [tap][thread] entries of ROWS words
+            u64* dst = gstage + (ks % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid * ROWS;
+            int tt[TAPS];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tt[4 * c] = taps[c].x, tt[4 * c + 1] = taps[c].y, tt[4 * c + 2] = taps[c].z, tt[4 * c + 3] = taps[c].w;
+            for (int c = 0; c < TAPS / 4; ++c) tt[4 * c] = taps[c].x, tt[4 * c + 1] = taps[c].y, tt[4 * c + 2] = taps[c].z, tt[4 * c + 3] = taps[c].w;
             if (ks + 1 < ks_n) load_taps(ks + 1);
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < TAPS; ++u) {
                 const u64* from = xcol + static_cast<long long>(max(tt[u], 0)) * cell_words;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s_addr(dst + u * TC_PRODUCERS)), "l"(from),
-                             "r"(tt[u] >= 0 ? 8 : 0)
-                             : "memory");
+                if constexpr (G16)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s_addr(dst + u * 2 * TC_PRODUCERS)), "l"(from),
+                                 "r"(tt[u] >= 0 ? 16 : 0)
+                                 : "memory");
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s_addr(dst + u * TC_PRODUCERS)), "l"(from),
+                                 "r"(tt[u] >= 0 ? 8 : 0)
+                                 : "memory");
             }
         };
 #pragma unroll
@@ -234,39 +249,52 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(DevRing R, ImmaMac g,
         }
         for (int ks = 0; ks < ks_n; ++ks) {
             asm volatile("cp.async.wait_group %0;" ::"n"(TC_GDEPTH - 1) : "memory");  // step ks landed
-            u64 cur[16];
+            u64 cur[ROWS][TAPS];
             {
-                const u64* from = gstage + (ks % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid;
+                const u64* from = gstage + (ks % TC_GDEPTH) * (16 * TC_PRODUCERS) + tid * ROWS;
 #pragma unroll
-                for (int u = 0; u < 16; ++u) cur[u] = from[u * TC_PRODUCERS];
+                for (int u = 0; u < TAPS; ++u) {
+                    if constexpr (G16) {
+                        const ulonglong2 v2 = *reinterpret_cast<const ulonglong2*>(from + u * 2 * TC_PRODUCERS);
+                        cur[0][u] = v2.x;
+                        cur[ROWS - 1][u] = v2.y;
+                    } else {
+                        cur[0][u] = from[u * TC_PRODUCERS];
+                    }
+                }
             }
             const int stage = ks % STAGES;
             if (ks >= STAGES) mbar_wait(empty + stage, ((ks / STAGES) - 1) & 1);
             unsigned char* st = smem + stage * S::STAGE_BYTES;
-            // byte planes a < NA of row r, this thread's 16 taps
-            unsigned pl[NA][4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const u64* ww = cur + 4 * c;
-                unsigned p4[4];
-                transpose4(static_cast<unsigned>(ww[0]), static_cast<unsigned>(ww[1]), static_cast<unsigned>(ww[2]),
-                           static_cast<unsigned>(ww[3]), p4);
+            for (int rr = 0; rr < ROWS; ++rr) {
+                // byte planes a < NA of row prow + rr, this thread's taps
+                unsigned pl[NA][TAPS / 4];
 #pragma unroll
-                for (int a = 0; a < 4; ++a) pl[a][c] = p4[a];
-                const unsigned h0 = static_cast<unsigned>(ww[0] >> 32), h1 = static_cast<unsigned>(ww[1] >> 32);
-                const unsigned h2 = static_cast<unsigned>(ww[2] >> 32), h3 = static_cast<unsigned>(ww[3] >> 32);
-                if constexpr (WIDE) {
-                    transpose4(h0, h1, h2, h3, p4);
+                for (int c = 0; c < TAPS / 4; ++c) {
+                    const u64* ww = cur[rr] + 4 * c;
+                    unsigned p4[4];
+                    transpose4(static_cast<unsigned>(ww[0]), static_cast<unsigned>(ww[1]), static_cast<unsigned>(ww[2]),
+                               static_cast<unsigned>(ww[3]), p4);
 #pragma unroll
-                    for (int a = 0; a < 4; ++a) pl[4 + a][c] = p4[a];
-                } else {
-                    pl[4][c] = __byte_perm(__byte_perm(h0, h1, 0x0040), __byte_perm(h2, h3, 0x0040), 0x5410);
+                    for (int a = 0; a < 4; ++a) pl[a][c] = p4[a];
+                    const unsigned h0 = static_cast<unsigned>(ww[0] >> 32), h1 = static_cast<unsigned>(ww[1] >> 32);
+                    const unsigned h2 = static_cast<unsigned>(ww[2] >> 32), h3 = static_cast<unsigned>(ww[3] >> 32);
+                    if constexpr (WIDE) {
+                        transpose4(h0, h1, h2, h3, p4);
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) pl[4 + a][c] = p4[a];
+                    } else {
+                        pl[4][c] = __byte_perm(__byte_perm(h0, h1, 0x0040), __byte_perm(h2, h3, 0x0040), 0x5410);
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < NA; ++a) {
+                    unsigned char* dst = st + a * TC_A_BYTES + core_off(prow + rr, pk0);
+                    if constexpr (G16) *reinterpret_cast<uint2*>(dst) = make_uint2(pl[a][0], pl[a][1]);
+                    else *reinterpret_cast<uint4*>(dst) = make_uint4(pl[a][0], pl[a][1], pl[a][2], pl[a][3]);
                 }
             }
-#pragma unroll
-            for (int a = 0; a < NA; ++a)
-                *reinterpret_cast<uint4*>(st + a * TC_A_BYTES + core_off(r, kh * 16)) =
-                    make_uint4(pl[a][0], pl[a][1], pl[a][2], pl[a][3]);
             // refill the staging slot just read (its words are consumed: the plane stores used them)
             if (ks + TC_GDEPTH < ks_n) gather(ks + TC_GDEPTH);
             asm volatile("cp.async.commit_group;" ::: "memory");
