@@ -88,6 +88,49 @@ def layer_work(hb, spec):
     return out
 
 
+def c3_cryptonets(hb, device, with_reference, stream=None, steps=5):
+    """the CryptoNets-style stack (pad -> conv 5x5/2 -> square
+    -> dense 100 -> square -> dense 10) on 4096 encrypted synthetic 28x28x1
+    images per set (net-n8192-d8), device-timed; with the reference, the same
+    set through oracle/_ref on all host threads, and the output ciphertext
+    words compared (full-config parity)."""
+    import torch
+    p = hb.preset_params("net-n8192-d8")
+    spec = c3_spec(hb)
+    eng = hb.CkksEngine(p, device=device).keygen(1)
+    if stream is not None:
+        eng.set_stream(stream)
+    data = np.random.default_rng(3).uniform(0, 1, size=(p.n // 2, spec.input.positions()))
+    x = eng.encrypt_tensor(data, seed=11, shape=spec.input)
+    model = eng.model(spec)
+    for _ in range(2):
+        y = hb.forward_encrypted(model, x, eng, seed=13)
+    eng.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        y = hb.forward_encrypted(model, x, eng, seed=13)
+    e.record()
+    torch.cuda.synchronize()
+    sec = s.elapsed_time(e) / 1e3 / steps
+    res = {"preset": "net-n8192-d8", "images_per_set": p.n // 2, "ms_per_set": sec * 1e3,
+           "images_per_s": (p.n // 2) / sec}
+    if with_reference:
+        from oracle import ref
+        if ref.available():
+            threads = os.cpu_count() or 1
+            r = ref.RefEngine.from_params(p).keygen(1)
+            rx = r.encrypt_tensor(data, spec.input, seed=11, threads=threads)
+            t0 = time.perf_counter()
+            ry, _ = r.forward_encrypted(spec, rx, seed=13, threads=threads)
+            wall = time.perf_counter() - t0
+            res["reference"] = {"seconds_per_set": wall, "images_per_s": (p.n // 2) / wall, "threads": threads,
+                                "kind": "reference", "sample": "the full C3 set (no extrapolation)"}
+            res["output_words_equal_reference"] = bool(np.array_equal(y.words(), ry.words()))
+    eng.close()
+    return res
+
+
 def crop_extrapolation_check(hb, eng, full_ms, crop=8):
     """Validates the C5 crop method on C4, where the full set also runs: the
     C4 stack on a crop x crop x 3 input, each layer's CUDA-event time scaled
@@ -474,6 +517,8 @@ def run_ours(args):
         c5 = c5_extrapolated(hb, local, stream=stream.cuda_stream) if world == 1 and not args.no_c5 else None
         if c5 is not None:
             c5["method_check_on_c4"] = xcheck
+        c3 = (c3_cryptonets(hb, local, with_reference=not args.no_cpu_baseline, stream=stream.cuda_stream)
+              if world == 1 and not args.no_c5 else None)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             from oracle import ref
@@ -497,7 +542,7 @@ def run_ours(args):
                         "d2h_bytes_per_step": out_words_n * 8},
                 "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "output": {"cells": out_cells, "level": out_level},
-                "microbench_c2": mb, "c5_alexnet_cowc_extrapolated": c5, "kernels": kernels}
+                "microbench_c2": mb, "c3_cryptonets": c3, "c5_alexnet_cowc_extrapolated": c5, "kernels": kernels}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
