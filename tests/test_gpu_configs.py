@@ -32,3 +32,31 @@ def test_full_config_matches_reference(ref, config):
     plain = ref.forward_plain(spec, data[:64])
     dec = eng.decrypt_tensor(y, p.n // 2)[:64]
     assert np.max(np.abs(dec - plain)) < 1e-2
+
+
+def test_c5_ring_slice_matches_reference(ref):
+    """C5's ring (large-n16384-d24, 25 limbs, 8192 slots) on a slice of its
+    stack: conv 11x11 (K = 363: the tcgen05 path for every limb) -> relu-poly2
+    (key switch at N = 2^14, level 23, 49 digits) -> avg_pool 2 -> dense(1),
+    on a 4x4x3 crop with 8 filters (the full AlexNet layers are too slow for
+    the reference)."""
+    p = hb.preset_params("large-n16384-d24")
+    spec = hb.ModelSpec(hb.Shape.spatial(4, 4, 3))
+    spec.activations["relu-poly2"] = hb.relu_default_surrogate()
+    spec.layers = [hb.LayerSpec.conv2d(8, 11, 11), hb.LayerSpec.activation("relu-poly2"), hb.LayerSpec.avg_pool2d(2),
+                   hb.LayerSpec.dense(1)]
+    spec = hb.glorot_weights(spec, 5)
+    threads = os.cpu_count() or 1
+    data = np.random.default_rng(7).uniform(0, 1, size=(p.n // 2, spec.input.positions()))
+    eng = hb.CkksEngine(p).keygen(3)
+    eng.profile_reset()
+    eng.profile(True)
+    y = hb.forward_encrypted(spec, eng.encrypt_tensor(data, seed=21, shape=spec.input), eng, seed=23)
+    eng.synchronize()
+    eng.profile(False)
+    assert "k_conv_tc" in eng.profile_read()
+    r = ref.RefEngine.from_params(p).keygen(3)
+    ry, _ = r.forward_encrypted(spec, r.encrypt_tensor(data, spec.input, seed=21, threads=threads), seed=23,
+                                threads=threads)
+    assert (y.level, y.scale) == ry.info()[1:]
+    assert np.array_equal(y.words(), ry.words())
