@@ -141,6 +141,19 @@ __device__ __forceinline__ void ks_mbar_wait(uint64_t* b, unsigned parity) {
                  "l"(src), "r"(bytes), "r"(ks_saddr(bar))
                  : "memory");
 }
+// ---- CTA-pair (cluster of 2) helpers for the shared column stage ------------
+__device__ __forceinline__ void ks_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ks_mapa(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void ks_st_cluster(uint32_t addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
 // EL doubles of this thread's TMEM lane at column `col` (2 x 32-bit columns each)
 template <int EL>
 __device__ __forceinline__ void tmem_ld_d(uint32_t addr, double (&v)[EL]) {
@@ -294,7 +307,16 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     // FP64 path: the next digit's first-round inputs are loaded into registers
     // while the current digit is transformed; with one column stage (C = 1) the
     // two inputs of each element's column butterfly are prefetched
-    constexpr bool PREFETCH = FP && (C == 0 || (HECNN_KS_PF_COL && C == 1));
+#ifndef HECNN_KS_CLUSTER
+#define HECNN_KS_CLUSTER 0
+#endif
+    // CL: the two block CTAs of a limb polynomial (N = 2^14) run as a cluster;
+    // each computes the column butterfly for half of the positions once and
+    // writes both outputs -- its own into its shared memory, the other block's
+    // into the peer's through distributed shared memory -- instead of every
+    // CTA recomputing the stage for all of its positions
+    constexpr bool CL = FP && C == 1 && HECNN_KS_CLUSTER;
+    constexpr bool PREFETCH = FP && !CL && (C == 0 || (HECNN_KS_PF_COL && C == 1));
     constexpr int PFW = C == 0 ? 1 : 2;  // words per first-round element
     const long long n = 1LL << LOGN;
     const long long blk_off = static_cast<long long>(b) << LOGB;
@@ -405,9 +427,27 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         if constexpr (LIFT) return lift_digit(v, q);
         else return v;
     };
+    const double w_cl = CL ? R.fwd_f[(static_cast<long long>(i) << LOGN) + 1] : 0.0;
+    if constexpr (CL) ks_cluster_sync();  // the peer CTA is running before its shared memory is written
     for (int t = 0; t < D; ++t) {
         const u32* dig = digits + (ct * D + t) * n;
+        if constexpr (CL) {
+            double* sdata = reinterpret_cast<double*>(smem);
+            const uint32_t peer = ks_mapa(ks_saddr(sdata), static_cast<uint32_t>(b ^ 1));
+            for (int r = b * (B / 2) + threadIdx.x; r < (b + 1) * (B / 2); r += T) {
+                const double x0 = ntt::to_fp(lift(__ldg(dig + r))), x1 = ntt::to_fp(lift(__ldg(dig + r + B)));
+                const double v = ntt::fmodmul(x1, w_cl, ar.q, ar.qinv);
+                const int sr = ntt::swz(r);
+                sdata[sr] = b == 0 ? x0 + v : x0 - v;
+                ks_st_cluster(peer + sr * 8, b == 0 ? x0 - v : x0 + v);
+            }
+            ks_cluster_sync();
+        }
         auto first = [&](int r, int uu, int k) -> V {
+            if constexpr (CL) {
+                (void)uu, (void)k;
+                return reinterpret_cast<const double*>(smem)[ntt::swz(r)];
+            } else
             if constexpr (PREFETCH && C == 0) {
                 (void)r;
                 return ntt::to_fp(lift(pf[uu * E0 + k]));
@@ -465,7 +505,8 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                                           if (t + 1 < D) prefetch(t + 1);
                                       });
         if constexpr (USE_TMEM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        __syncthreads();  // the next digit's first round overwrites shared memory
+        if constexpr (CL) ks_cluster_sync();  // the peer writes this CTA's data buffer next
+        else __syncthreads();  // the next digit's first round overwrites shared memory
         if constexpr (TM) {
             if (threadIdx.x == 0 && t + 1 < D)
                 ks_bulk_load(sacc, key.evk_f + (2LL * (t + 1)) * key.key_stride + key.ioff + blk_off, B * 8, bbar);
@@ -779,6 +820,24 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
             2.0 * D * limbs * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
     auto launch = [&](auto kern, cudaStream_t st, int l0, int nsel) {
         const std::size_t ctas = count * static_cast<std::size_t>(nsel) << (LOGN - P::LOGB);
+        if (HECNN_KS_CLUSTER && LOGN - P::LOGB == 1 && (kern == kfp)) {
+            // the two block CTAs of each limb polynomial as a cluster (shared column stage)
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(ctas));
+            cfg.blockDim = dim3(P::T);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            cuda_check(cudaLaunchKernelEx(&cfg, kern, R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel, mode, fy),
+                       "cudaLaunchKernelEx (key-switch cluster)");
+            return;
+        }
         kern<<<static_cast<unsigned>(ctas), P::T, smem, st>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel, mode, fy);
     };
     // The integer-limb kernel (IMAD pipes) runs on the side stream beside the

@@ -28,6 +28,7 @@ V[noepf]="-DHECNN_KS_EPI_PF=0"
 V[kse4]="-DHECNN_KS_LOGE=4"
 V[col512]="-DHECNN_KS_MAXT_COL=512"
 V[g16]="-DHECNN_TC_G16=1"
+V[kscl]="-DHECNN_KS_CLUSTER=1"
 V[tc34]="-DHECNN_TC_STAGES=3 -DHECNN_TC_GDEPTH=4"
 V[tc25]="-DHECNN_TC_STAGES=2 -DHECNN_TC_GDEPTH=5"
 V[nosacc]="-DHECNN_KS_ABLATE_SACC"
