@@ -10,9 +10,10 @@
 //   digit t it lifts digit_t into limb i (v < q_i, else v mod q_i:
 //   ckks.hpp:622), runs the forward NTT in shared memory (same rounds and
 //   swizzle as ntt.cu) and multiply-accumulates against evk_t (b_t, a_t)
-//   with Shoup constants; accumulators stay in registers across all D
-//   digits, so neither the D lifted digit polynomials nor partial sums ever
-//   touch HBM. The epilogue adds (d0, d1) in place. For N > 2^13 a CTA owns
+//   (exact FP64 arithmetic for q < 2^42, Shoup for the 60-bit limb); the
+//   accumulators stay on chip across all D digits (c0 in registers, c1 in
+//   tensor memory), so neither the D lifted digit polynomials nor partial
+//   sums ever touch HBM. The epilogue adds (d0, d1) in place. For N > 2^13 a CTA owns
 //   a 2^13 block and recomputes the C = log2(N) - 13 column stages for its
 //   block directly from the (L2-resident) u32 digits.
 
@@ -275,11 +276,12 @@ __device__ __forceinline__ double column_value_fp(const u32* __restrict__ dig, c
 // once in shared memory as a block-local table TL[2^s + m] =
 // tw[2^(s+C) + b 2^s + m] and reused by all D digit transforms (round code
 // indexes it with b = c = 0).
-// FP64 path (all limbs but the 60-bit q0): the c1 accumulator lives in the
-// shared-memory space the integer path needs for its 16-byte twiddles, in a
-// thread-private [slot][thread] layout (no barriers, no bank conflicts), and
-// the registers this frees hold the next digit's first-round inputs, loaded
-// while the current digit is transformed.
+// FP64 path (all limbs but the 60-bit q0): the c1 accumulator lives in tensor
+// memory (TM below; without it, in a thread-private [slot][thread] shared-
+// memory layout), the shared memory the integer path needs for its 16-byte
+// twiddles holds the digit's b_t slice, and the registers the accumulator
+// frees hold the next digit's first-round inputs, loaded while the current
+// digit is transformed.
 // LIFT: some prime of the chain is <= 2^20, so digits need v mod q_i
 // (ckks.hpp:622); otherwise every digit is already a residue.
 template <int LOGN, int LOGB, int LOGE, int T, bool LIFT, class A, class KeyAt>
