@@ -70,13 +70,20 @@ public:
         return v;
     }
     // read_poly (ckks_serialize.hpp:67-75) into caller storage of `cap`
-    // words; returns (level, rep)
-    std::pair<std::uint16_t, std::uint8_t> poly(u64* dst, std::size_t n, std::size_t cap_words) {
+    // words; returns (level, rep). The level is checked against `cap` before
+    // any word is copied, and every residue against its limb's prime: the
+    // device kernels assume canonical words in [0, q_i) (the FP64 path needs
+    // them below 2^52), so an unreduced blob is an error, not silent garbage.
+    std::pair<std::uint16_t, std::uint8_t> poly(u64* dst, std::size_t n, std::size_t cap_words, const u64* primes) {
         const auto level = le<std::uint16_t>();
         const auto rep = le<std::uint8_t>();
         const std::size_t words = (static_cast<std::size_t>(level) + 1) * n;
-        if (words > cap_words) throw std::invalid_argument("ckks blob: polynomial level exceeds the context's chain");
+        if (words > cap_words) throw std::invalid_argument("ckks blob: polynomial level exceeds the caller's storage");
         raw(dst, words * 8);
+        for (std::size_t i = 0; i <= level; ++i)
+            for (std::size_t j = 0; j < n; ++j)
+                if (dst[i * n + j] >= primes[i])
+                    throw std::invalid_argument("ckks blob: residue not reduced modulo its prime");
         return {level, rep};
     }
     Params header(Kind expected);  // read_header (ckks_serialize.hpp:41-58)

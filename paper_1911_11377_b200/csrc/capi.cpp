@@ -634,7 +634,7 @@ int hecnn_blob_load_key(hecnn_context* ctx, int kind, const uint8_t* data, size_
         blob::Reader r(data, len);
         require_same(r.header(static_cast<blob::Kind>(kind)), c);
         auto top_poly = [&](u64* dst, uint8_t want_rep, const char* what) {
-            const auto [level, rep] = r.poly(dst, n, poly);
+            const auto [level, rep] = r.poly(dst, n, poly, c.ring.primes.data());
             if (level != L || rep != want_rep)
                 throw std::invalid_argument(std::string("ckks blob: ") + what + " must be a top-level " +
                                             (want_rep ? "NTT" : "coefficient") + "-domain polynomial");
@@ -682,7 +682,7 @@ int hecnn_blob_load_ciphertexts(hecnn_context* ctx, const uint8_t* const* blobs,
     return guard([&] {
         Context& c = C(ctx);
         if (!count) throw std::invalid_argument("blob: no ciphertexts");
-        const std::size_t n = c.n(), cap = (c.top() + 1) * n;
+        const std::size_t n = c.n();
         std::vector<u64> host;
         uint32_t level = 0;
         double scale = 0.0;
@@ -701,7 +701,9 @@ int hecnn_blob_load_ciphertexts(hecnn_context* ctx, const uint8_t* const* blobs,
             }
             u64* dst = host.data() + k * 2 * (level + 1) * n;
             for (int comp = 0; comp < 2; ++comp) {
-                const auto [pl, rep] = r.poly(dst + comp * (level + 1) * n, n, cap);
+                // storage for this cell is sized by the header level: a polynomial
+                // declaring a higher level is rejected before any word is copied
+                const auto [pl, rep] = r.poly(dst + comp * (level + 1) * n, n, (level + 1) * n, c.ring.primes.data());
                 if (pl != level || rep != 0)
                     throw std::invalid_argument("ckks blob: ciphertext polynomials must be coefficient-domain at the ciphertext level");
             }

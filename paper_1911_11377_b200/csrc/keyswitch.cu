@@ -345,6 +345,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     uint64_t* bbar = reinterpret_cast<uint64_t*>(smem + 3 * B);
     constexpr int TNEED = (T / 128) * TCW;
     constexpr int TCOLS = TNEED <= 32 ? 32 : (TNEED <= 64 ? 64 : (TNEED <= 128 ? 128 : (TNEED <= 256 ? 256 : 512)));
+    static_assert(!USE_TMEM || TNEED <= 512, "key switch: tensor-memory accumulators exceed the 512 TMEM columns");
     uint32_t tm_lane = 0;
     if constexpr (USE_TMEM) {
         __shared__ uint32_t tm_slot;

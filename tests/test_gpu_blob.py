@@ -78,3 +78,27 @@ def test_blob_rejections(ref):
     lower, ls = r.rescale(ct, p.top_level, p.scale)
     with pytest.raises(ValueError, match="share level and scale"):
         hb.load_ciphertexts(eng, [top, r.save_ciphertext(lower, p.top_level - 1, ls)])
+
+
+def test_blob_rejects_inconsistent_levels_and_unreduced_words(ref):
+    """A header level below the polynomials' level must be rejected before any
+    word is copied (the storage is sized by the header), and residues >= q_i
+    are rejected instead of reaching the kernels unreduced."""
+    p = hb.preset_params("toy-n16")
+    r = ref.RefEngine.from_params(p).keygen(1)
+    eng = hb.CkksEngine(p)
+    ct = r.encrypt(np.linspace(-1, 1, p.n // 2), 5)
+    top = bytearray(r.save_ciphertext(ct, p.top_level, p.scale))
+    hdr = 4 + 2 + 2 + 4 + 2 + 8 * len(p.primes) + 8 + 8 + 1
+    lvl_at = hdr + 8
+    assert int.from_bytes(top[lvl_at:lvl_at + 2], "little") == p.top_level
+    bad = bytearray(top)
+    bad[lvl_at:lvl_at + 2] = (0).to_bytes(2, "little")
+    with pytest.raises(ValueError, match="polynomial level exceeds"):
+        hb.load_ciphertext(eng, bytes(bad))
+    bad = bytearray(top)
+    w0 = lvl_at + 2 + 2 + 1  # c0: level u16, rep u8, then the first residue of limb 0
+    bad[w0:w0 + 8] = (p.primes[0]).to_bytes(8, "little")
+    with pytest.raises(ValueError, match="not reduced"):
+        hb.load_ciphertext(eng, bytes(bad))
+    assert np.array_equal(hb.load_ciphertext(eng, bytes(top)).words()[0], ct[0])
