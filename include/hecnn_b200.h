@@ -259,6 +259,14 @@ int hecnn_model_create(hecnn_context* ctx, const hecnn_model_desc* desc, hecnn_m
 int hecnn_model_destroy(hecnn_model* m);
 /* depth_cost (model.hpp:169-182) */
 int hecnn_model_depth_cost(const hecnn_model* m, size_t* cost);
+/* Execution of the spatial layers when their tensors exceed device memory
+ * (no reference counterpart: the reference materialises every layer tensor,
+ * layers.hpp:299-368). mode 0: row-stream only the layers whose whole
+ * tensors do not fit (default); 1: row-stream every spatial stage; 2: never.
+ * tile: stage-output columns per tile (0: sized to the memory budget);
+ * mem_budget: device bytes a forward pass may plan with (0: free memory).
+ * Results are identical word for word in every mode. */
+int hecnn_model_set_streaming(hecnn_model* m, int mode, size_t tile, size_t mem_budget);
 /* forward_encrypted (layers.hpp:299-368). x must carry the model's input
  * shape (hecnn_tensor_set_shape). layer_seconds (optional) receives one
  * device-timed entry per layer. */

@@ -44,6 +44,7 @@ EXPORTED_SYMBOLS = (
     "hecnn_decrypt_tensor", "hecnn_ct_add", "hecnn_ct_sub", "hecnn_ct_mul", "hecnn_ct_square", "hecnn_ct_rescale",
     "hecnn_ct_mod_switch", "hecnn_ct_mul_const", "hecnn_ct_add_const", "hecnn_eval_activation",
     "hecnn_model_create", "hecnn_model_destroy", "hecnn_model_depth_cost", "hecnn_forward_encrypted",
+    "hecnn_model_set_streaming",
     "hecnn_profile_enable", "hecnn_profile_reset", "hecnn_profile_read", "hecnn_modmul_peak",
     "hecnn_tensor_copy_to_device", "hecnn_host_encode_real", "hecnn_host_decode_real",
     "hecnn_host_encryption_randomness", "hecnn_fp64_modmul_peak", "hecnn_context_trim",
@@ -127,6 +128,7 @@ _SIGNATURES = {
     "hecnn_model_create": [_V, _V, _PV],
     "hecnn_model_destroy": [_V],
     "hecnn_model_depth_cost": [_V, _PSZ],
+    "hecnn_model_set_streaming": [_V, _I, _SZ, _SZ],
     "hecnn_forward_encrypted": [_V, _V, _V, _U64, _PV, _PD],
     "hecnn_blob_params": [_V, _SZ, ctypes.POINTER(ctypes.c_int), _PSZ, _V, _PSZ, _PD, _PD, ctypes.POINTER(ctypes.c_int)],
     "hecnn_blob_save_key": [_V, _I, _V, _SZ, _PSZ],
@@ -601,6 +603,16 @@ class Model:
         c = ctypes.c_size_t()
         _check(lib().hecnn_model_depth_cost(self._h, ctypes.byref(c)))
         return c.value
+
+    STREAM_AUTO, STREAM_ALWAYS, STREAM_NEVER = 0, 1, 2
+
+    def set_streaming(self, mode: int = 0, tile: int = 0, mem_budget: int = 0) -> "Model":
+        """Row-streamed execution of the spatial layers (hecnn_model_set_streaming):
+        mode 0 streams only what does not fit in device memory, 1 always, 2 never;
+        tile = stage-output columns per tile (0: from the budget); mem_budget =
+        device bytes to plan with (0: free memory). Output words do not depend on it."""
+        _check(lib().hecnn_model_set_streaming(self._h, int(mode), ctypes.c_size_t(tile), ctypes.c_size_t(mem_budget)))
+        return self
 
 
 # ---------------------------------------------------------------- engine

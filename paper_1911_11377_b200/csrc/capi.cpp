@@ -539,6 +539,17 @@ int hecnn_model_depth_cost(const hecnn_model* m, size_t* cost) {
     });
 }
 
+int hecnn_model_set_streaming(hecnn_model* m, int mode, size_t tile, size_t mem_budget) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("model: null handle");
+        if (mode < 0 || mode > 2) throw std::invalid_argument("model: streaming mode must be 0, 1 or 2");
+        m->m.stream_mode = mode;
+        m->m.stream_tile = tile;
+        m->m.mem_budget = mem_budget;
+        m->m.plans.clear();
+    });
+}
+
 int hecnn_forward_encrypted(hecnn_context* ctx, const hecnn_model* m, const hecnn_tensor* x, uint64_t seed,
                             hecnn_tensor** out, double* layer_seconds) {
     return guard([&] {

@@ -1,5 +1,6 @@
 // Device-resident CKKS engine (see engine.hpp).
 #include "engine.hpp"
+#include "engine_detail.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -36,8 +37,7 @@ struct Trace {
     }
 };
 
-// Scratch budget per batched scheme op; chunks of ciphertexts are sized to it.
-constexpr std::size_t kScratchBytes = std::size_t(3) << 30;
+using detail::kScratchBytes;
 
 unsigned host_threads() {
     unsigned t = std::thread::hardware_concurrency();
@@ -652,7 +652,7 @@ void Activation::validate() const {
 }
 
 // eval_encrypted (activation.hpp:228-265): power-basis plan over whole tensors.
-static TensorPtr eval_activation_cells(Context& C, const Activation& act, const Tensor& x) {
+static TensorPtr eval_activation_cells(Context& C, const Activation& act, const Tensor& x, u64* dst) {
     Trace tr("eval_activation");
     act.validate();
     const std::size_t d = act.degree(), depth = act.encrypted_depth();
@@ -709,7 +709,14 @@ static TensorPtr eval_activation_cells(Context& C, const Activation& act, const 
                     C.enc->residues_of_rounded(roundl(static_cast<long double>(c) * static_cast<long double>(s0)), lvl));
                 st.c0 = d0.as<u64>();
             }
-            TensorPtr acc = make_tensor(C, x.cells, lvl, s0);
+            TensorPtr acc = dst ? std::make_unique<Tensor>() : make_tensor(C, x.cells, lvl, s0);
+            if (dst) {  // written straight into the caller's storage
+                acc->ctx = &C;
+                acc->cells = x.cells;
+                acc->level = lvl;
+                acc->scale = s0;
+                acc->buf = DevBuf::alias(dst, x.cells * 2 * (lvl + 1) * C.n() * 8);
+            }
             rescale(C.dev, p.data(), acc->data(), static_cast<int>(p.level), 2 * x.cells, C.L(), dc.as<ulonglong2>(),
                     &st);
             acc->shape = x.shape;
@@ -729,6 +736,19 @@ static TensorPtr eval_activation_cells(Context& C, const Activation& act, const 
     if (act.coefficients[0] != 0.0) acc = ct_add_const(C, *acc, act.coefficients[0]);
     acc->shape = x.shape;
     acc->batch = x.batch;
+    if (dst) {
+        cuda_check(cudaMemcpyAsync(dst, acc->data(), x.cells * acc->cell_words() * 8, cudaMemcpyDeviceToDevice, C.stream),
+                   "copy activation");
+        TensorPtr view = std::make_unique<Tensor>();
+        view->ctx = &C;
+        view->cells = acc->cells;
+        view->level = acc->level;
+        view->scale = acc->scale;
+        view->shape = acc->shape;
+        view->batch = acc->batch;
+        view->buf = DevBuf::alias(dst, x.cells * acc->cell_words() * 8);
+        return view;
+    }
     return acc;
 }
 
@@ -748,18 +768,31 @@ static TensorPtr cell_slice(const Tensor& x, std::size_t c0, std::size_t m) {
 // The power plan is identical for every cell, so large tensors are evaluated
 // in cell chunks written straight into the output: peak memory is input +
 // output + one chunk's intermediates instead of every full-size power/term.
-TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x) {
+TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x, u64* dst) {
     const std::size_t per_cell = x.cell_words() * 8;
     const std::size_t chunk = std::max<std::size_t>(1, (std::size_t(6) << 30) / (per_cell * 6));
-    if (x.cells <= chunk) return eval_activation_cells(C, act, x);
+    if (x.cells <= chunk) return eval_activation_cells(C, act, x, dst);
     TensorPtr out;
     for (std::size_t c0 = 0; c0 < x.cells; c0 += chunk) {
         const std::size_t m = std::min(chunk, x.cells - c0);
-        TensorPtr part = eval_activation_cells(C, act, *cell_slice(x, c0, m));
-        if (!out) out = make_tensor(C, x.cells, part->level, part->scale);
-        cuda_check(cudaMemcpyAsync(out->cell(c0), part->data(), m * part->cell_words() * 8, cudaMemcpyDeviceToDevice,
-                                   C.stream),
-                   "copy activation chunk");
+        if (out) {  // later chunks land in place
+            eval_activation_cells(C, act, *cell_slice(x, c0, m), out->cell(c0));
+            continue;
+        }
+        TensorPtr part = eval_activation_cells(C, act, *cell_slice(x, c0, m), dst);
+        if (dst) {
+            out = std::make_unique<Tensor>();
+            out->ctx = &C;
+            out->cells = x.cells;
+            out->level = part->level;
+            out->scale = part->scale;
+            out->buf = DevBuf::alias(dst, x.cells * part->cell_words() * 8);
+        } else {
+            out = make_tensor(C, x.cells, part->level, part->scale);
+            cuda_check(cudaMemcpyAsync(out->cell(c0), part->data(), m * part->cell_words() * 8,
+                                       cudaMemcpyDeviceToDevice, C.stream),
+                       "copy activation chunk");
+        }
     }
     out->shape = x.shape;
     out->batch = x.batch;
@@ -768,7 +801,7 @@ TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x) {
 
 // ---------------------------------------------------------------- encryption
 
-namespace {
+namespace detail {
 
 // Public-key encryptions of `count` messages (or zeros) at limbs 0..level,
 // randomness from make_encryption_randomness(seeds[i]) (ckks.hpp:238-266).
@@ -826,7 +859,9 @@ void encrypt_into(Context& C, std::size_t count, const u64* seeds, const std::ve
     }
 }
 
-}  // namespace
+}  // namespace detail
+
+using detail::encrypt_into;
 
 // encrypt_tensor (tensor.hpp:77-94)
 TensorPtr encrypt_tensor(Context& C, const double* data, std::size_t batch, std::size_t positions, u64 seed) {
@@ -1001,8 +1036,8 @@ void for_limb_runs(const Context& C, std::size_t limbs, F f) {
 // A fragments of mma.m16n8k32 (row-major 16 x 32): lane (g, t) holds
 // reg0 = row g, k 4t..4t+3; reg1 = row g+8, same k; reg2/reg3 = the same rows
 // at k + 16; byte u of a register is k + u. Row = output channel in the tile.
-void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulonglong2>& w, const std::vector<int>& src,
-                      std::size_t rows, std::size_t limbs) {
+void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulonglong2>& w, std::size_t rows,
+                      std::size_t limbs) {
     const std::size_t K = rows, oc = static_cast<std::size_t>(lc.oc), oc_pad = static_cast<std::size_t>(lc.oc_pad);
     const std::size_t ksteps = (K + 31) / 32, kpad = ksteps * 32;
     std::size_t tiles = (oc + 15) / 16;
@@ -1088,17 +1123,13 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
     std::vector<double> sh(limbs * 9);
     for (std::size_t i = 0; i < limbs; ++i)
         for (int s = 0; s < 9; ++s) sh[i * 9 + s] = static_cast<double>(C.ring.mods[i].pow(2, 8 * s));
-    const std::size_t pixels = static_cast<std::size_t>(lc.pixels);
-    std::vector<int> sp(pixels * kpad, -1);
-    for (std::size_t p = 0; p < pixels; ++p)
-        for (std::size_t k = 0; k < K; ++k) sp[p * kpad + k] = src[p * K + k];
     // tcgen05 weight tiles: per (limb, 48-channel tile, 32-tap step) the B
     // operand of conv_tc.cu, rows n = b * 48 + o (weight byte b of channel o),
     // in the UMMA K-major core-matrix layout (8 rows x 16 taps per 128 B)
     const std::size_t TOC = static_cast<std::size_t>(tc_oc_tile(false)), ttiles = (oc + TOC - 1) / TOC;
     const std::size_t tile_bytes = 5 * TOC * 32, wtc_bytes = limbs * ttiles * ksteps * tile_bytes;
     const char* no_tc = std::getenv("HECNN_NO_TCGEN05");
-    if (!(no_tc && *no_tc == '1') && lc.pixels > 1 && ksteps <= 192 && C.n() % 128 == 0 && wtc_bytes <= (std::size_t(1) << 30)) {
+    if (!(no_tc && *no_tc == '1') && lc.conv && ksteps <= 192 && C.n() % 128 == 0 && wtc_bytes <= (std::size_t(1) << 30)) {
         std::vector<std::uint8_t> t(wtc_bytes, 0);
         for (std::size_t i = 0; i < limbs; ++i) {
             if (!imma_limb(C, i)) continue;
@@ -1152,11 +1183,144 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
     }
     lc.wfrag = C.upload_vec(frag);
     lc.shift = C.upload_vec(sh);
-    lc.src_pad = C.upload_vec(sp);
     lc.kpad = static_cast<int>(kpad);
     lc.ksteps = static_cast<int>(ksteps);
     lc.oc_tiles = static_cast<int>(tiles);
 }
+
+}  // namespace
+
+namespace detail {
+
+// Integer weight residues of a conv / dense layer at `level`, with the
+// tensor-core layouts (layers.hpp:185-188 encodes each weight once per layer
+// call; here once per model and level).
+Model::LinearCache& linear_weights(Context& C, Model& M, std::size_t li, std::uint32_t level, std::size_t rows) {
+    const Layer& l = M.layers[li];
+    const bool conv = l.kind == 0;
+    const std::size_t oc = conv ? l.filters : l.units;
+    if (l.w.size() != rows * oc || l.b.size() != oc)
+        throw std::invalid_argument(conv ? "conv2d: weight/bias shape mismatch" : "dense: weight/bias shape mismatch");
+    if (level == 0) throw std::invalid_argument(conv ? "conv2d: no level headroom" : "dense: no level headroom");
+    auto key = std::make_pair(li, level);
+    auto it = M.linear.find(key);
+    if (it != M.linear.end()) return it->second;
+    const std::size_t limbs = level + 1;
+    Model::LinearCache lc;
+    lc.conv = conv;
+    lc.K = static_cast<int>(rows);
+    lc.oc = static_cast<int>(oc);
+    lc.oc_pad = static_cast<int>((oc + 15) / 16 * 16);
+    std::vector<ulonglong2> w(rows * lc.oc_pad * limbs, make_ulonglong2(0, 0));
+    std::vector<uint2> ws(rows * lc.oc_pad * limbs, make_uint2(0, 0));
+    for (std::size_t r = 0; r < rows; ++r)
+        for (std::size_t o = 0; o < oc; ++o) {
+            std::vector<u64> res = C.enc->scalar_residues(l.w[r * oc + o], C.scale, level);
+            for (std::size_t i = 0; i < limbs; ++i) {
+                const std::size_t at = (i * rows + r) * lc.oc_pad + o;  // limb-major: OCT channels contiguous
+                w[at] = make_ulonglong2(res[i], shoup_of(res[i], C.ring.primes[i]));
+                ws[at] = make_uint2(static_cast<unsigned>(res[i] & 0x1FFFFFu), static_cast<unsigned>(res[i] >> 21));
+            }
+        }
+    std::vector<ulonglong2> rc(2 * limbs);
+    for (std::size_t i = 0; i < limbs; ++i) {
+        const HostMod& m = C.ring.mods[i];
+        const u64 a = m.pow(2, 21), b = m.pow(2, 42);
+        rc[2 * i] = make_ulonglong2(a, shoup_of(a, m.q));
+        rc[2 * i + 1] = make_ulonglong2(b, shoup_of(b, m.q));
+    }
+    lc.wsplit = C.upload_vec(ws);
+    lc.recomb = C.upload_vec(rc);
+    lc.weights = C.upload_vec(w);
+    if (imma_enabled(C, rows)) build_imma_cache(C, lc, w, rows, limbs);
+    return M.linear.emplace(key, std::move(lc)).first->second;
+}
+
+Model::Taps make_taps(Context& C, const Model::LinearCache& lc, const std::vector<int>& src) {
+    Model::Taps t;
+    const std::size_t K = static_cast<std::size_t>(lc.K);
+    t.pixels = src.size() / K;
+    t.src = C.upload_vec(src);
+    if (lc.ksteps) {
+        const std::size_t kpad = static_cast<std::size_t>(lc.kpad);
+        std::vector<int> sp(t.pixels * kpad, -1);
+        for (std::size_t p = 0; p < t.pixels; ++p)
+            for (std::size_t k = 0; k < K; ++k) sp[p * kpad + k] = src[p * K + k];
+        t.src_pad = C.upload_vec(sp);
+    }
+    return t;
+}
+
+// ConvGeom (layers.hpp:24-50): same padding offsets of a conv from its input dims
+void conv_offsets(const Layer& l, std::size_t in_h, std::size_t in_w, std::size_t out_h, std::size_t out_w,
+                  long long& pad_top, long long& pad_left) {
+    pad_top = pad_left = 0;
+    if (l.valid) return;
+    const std::size_t need_h = (out_h - 1) * l.stride + l.kh, need_w = (out_w - 1) * l.stride + l.kw;
+    pad_top = need_h > in_h ? static_cast<long long>((need_h - in_h) / 2) : 0;
+    pad_left = need_w > in_w ? static_cast<long long>((need_w - in_w) / 2) : 0;
+}
+
+// bias residues at the accumulator scale (add_scalar_inplace, ckks.hpp:468-472)
+const u64* linear_bias(Context& C, Model& M, std::size_t li, std::uint32_t level, double acc_scale) {
+    const Layer& l = M.layers[li];
+    const std::size_t oc = l.kind == 0 ? l.filters : l.units, limbs = level + 1;
+    auto bkey = std::make_tuple(li, level, acc_scale);
+    auto bit = M.bias.find(bkey);
+    if (bit == M.bias.end()) {
+        std::vector<u64> b(oc * limbs);
+        for (std::size_t o = 0; o < oc; ++o) {
+            std::vector<u64> res = C.enc->scalar_residues(l.b[o], acc_scale, level);
+            std::copy(res.begin(), res.end(), b.begin() + o * limbs);
+        }
+        bit = M.bias.emplace(bkey, C.upload_vec(b)).first;
+    }
+    return bit->second.as<u64>();
+}
+
+// Output cells [m][oc] at `out` (level - 1) for pixels [p0, p0 + m) of a tap
+// table over the input cells at `x`: MAC over the taps (mul_scalar_mac,
+// ckks.hpp:448-465), bias, rescale (ckks.hpp:474-482). Chunked so the
+// pre-rescale scratch stays within kScratchBytes.
+void linear_apply(Context& C, Model::LinearCache& lc, const Model::Taps& taps, const u64* bias, const u64* x,
+                  std::uint32_t level, std::size_t p0, std::size_t m, u64* out) {
+    const std::size_t limbs = level + 1, oc = static_cast<std::size_t>(lc.oc);
+    const std::size_t cw = 2 * limbs * C.n();
+    const std::size_t per_pixel = oc * cw * 8;
+    const std::size_t pix_chunk = std::max<std::size_t>(1, std::min<std::size_t>(m, kScratchBytes / per_pixel));
+    DevBuf pre(&C, pix_chunk * per_pixel);
+    Launch L = C.L();
+    for (std::size_t q0 = 0; q0 < m; q0 += pix_chunk) {
+        const std::size_t mm = std::min(pix_chunk, m - q0), pp = p0 + q0;
+        GatherMac g{taps.src.as<int>() + pp * lc.K, lc.weights.as<ulonglong2>(), bias, lc.wsplit.as<uint2>(),
+                    lc.recomb.as<ulonglong2>(), static_cast<int>(mm), lc.K, lc.oc, lc.oc_pad, lc.oc};
+        if (lc.ksteps) {
+            ImmaMac im{taps.src_pad.as<int>() + pp * lc.kpad, lc.wfrag.as<uint4>(), bias, lc.shift.as<double>(),
+                       static_cast<int>(mm), lc.K, lc.kpad, lc.ksteps, lc.oc, lc.oc_tiles, lc.oc,
+                       lc.wfrag_wide.as<uint4>(), lc.shift_wide.as<ulonglong2>(), lc.wtc.as<uint4>(),
+                       lc.wtc_wide.as<uint4>()};
+            for_limb_runs(C, limbs, [&](std::size_t l0, std::size_t l1, bool tc) {
+                if ((tc || lc.wide_ok) && tc_mac_supported(C.dev, im, !tc))
+                    tc_mac(C.dev, im, x, pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
+                           static_cast<int>(l1), !tc, L);
+                else if (tc || lc.wide_ok)
+                    imma_mac(C.dev, im, x, pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
+                             static_cast<int>(l1), !tc, L);
+                else gather_mac(C.dev, g, x, pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
+                                static_cast<int>(l1), L);
+            });
+        } else {
+            gather_mac(C.dev, g, x, pre.as<u64>(), static_cast<int>(level), 0, static_cast<int>(limbs), L);
+        }
+        rescale(C.dev, pre.as<u64>(), out + q0 * oc * 2 * level * C.n(), static_cast<int>(level), 2 * mm * oc, L);
+    }
+}
+
+}  // namespace detail
+
+namespace {
+
+using detail::linear_weights;
 
 // conv2d / dense as a gather-MAC (layers.hpp:174-211, 269-293)
 TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, const Shape& out_shape) {
@@ -1165,50 +1329,13 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
     const bool conv = l.kind == 0;
     const Shape& in = x.shape;
     const std::size_t rows = conv ? l.kh * l.kw * in.c : in.positions();
-    const std::size_t oc = conv ? l.filters : l.units;
-    if (l.w.size() != rows * oc || l.b.size() != oc)
-        throw std::invalid_argument(conv ? "conv2d: weight/bias shape mismatch" : "dense: weight/bias shape mismatch");
-    if (x.level == 0) throw std::invalid_argument(conv ? "conv2d: no level headroom" : "dense: no level headroom");
     const std::uint32_t level = x.level;
-    const std::size_t limbs = level + 1;
-    const double wscale = C.scale;
-
-    auto key = std::make_pair(li, level);
-    auto it = M.linear.find(key);
-    if (it == M.linear.end()) {
-        Model::LinearCache lc;
-        lc.oc = static_cast<int>(oc);
-        lc.oc_pad = static_cast<int>((oc + 15) / 16 * 16);
-        std::vector<ulonglong2> w(rows * lc.oc_pad * limbs, make_ulonglong2(0, 0));
-        std::vector<uint2> ws(rows * lc.oc_pad * limbs, make_uint2(0, 0));
-        for (std::size_t r = 0; r < rows; ++r)
-            for (std::size_t o = 0; o < oc; ++o) {
-                std::vector<u64> res = C.enc->scalar_residues(l.w[r * oc + o], wscale, level);
-                for (std::size_t i = 0; i < limbs; ++i) {
-                    const std::size_t at = (i * rows + r) * lc.oc_pad + o;  // limb-major: OCT channels contiguous
-                    w[at] = make_ulonglong2(res[i], shoup_of(res[i], C.ring.primes[i]));
-                    ws[at] = make_uint2(static_cast<unsigned>(res[i] & 0x1FFFFFu), static_cast<unsigned>(res[i] >> 21));
-                }
-            }
-        std::vector<ulonglong2> rc(2 * limbs);
-        for (std::size_t i = 0; i < limbs; ++i) {
-            const HostMod& m = C.ring.mods[i];
-            const u64 a = m.pow(2, 21), b = m.pow(2, 42);
-            rc[2 * i] = make_ulonglong2(a, shoup_of(a, m.q));
-            rc[2 * i + 1] = make_ulonglong2(b, shoup_of(b, m.q));
-        }
-        lc.wsplit = C.upload_vec(ws);
-        lc.recomb = C.upload_vec(rc);
+    Model::LinearCache& lc = linear_weights(C, M, li, level, rows);
+    if (!lc.taps.pixels) {
         std::vector<int> src;  // tap k of every pixel uses weight row k (ky, kx, ic order)
         if (conv) {
-            const std::size_t need_h = (out_shape.h - 1) * l.stride + l.kh, need_w = (out_shape.w - 1) * l.stride + l.kw;
             long long pad_top = 0, pad_left = 0;
-            if (!l.valid) {
-                pad_top = need_h > in.h ? static_cast<long long>((need_h - in.h) / 2) : 0;
-                pad_left = need_w > in.w ? static_cast<long long>((need_w - in.w) / 2) : 0;
-            }
-            lc.pixels = static_cast<int>(out_shape.h * out_shape.w);
-            lc.K = static_cast<int>(rows);
+            detail::conv_offsets(l, in.h, in.w, out_shape.h, out_shape.w, pad_top, pad_left);
             for (std::size_t oy = 0; oy < out_shape.h; ++oy)
                 for (std::size_t ox = 0; ox < out_shape.w; ++ox)
                     for (std::size_t ky = 0; ky < l.kh; ++ky)
@@ -1221,62 +1348,16 @@ TensorPtr linear_layer(Context& C, Model& M, std::size_t li, const Tensor& x, co
                                 src.push_back(ok ? static_cast<int>((y * in.w + xx) * in.c + ic) : -1);
                             }
         } else {
-            lc.pixels = 1;
-            lc.K = static_cast<int>(rows);
             for (std::size_t k = 0; k < rows; ++k) src.push_back(static_cast<int>(k));
         }
-        lc.weights = C.upload_vec(w);
-        lc.src = C.upload_vec(src);
-        if (imma_enabled(C, rows)) build_imma_cache(C, lc, w, src, rows, limbs);
-        it = M.linear.emplace(key, std::move(lc)).first;
+        lc.taps = detail::make_taps(C, lc, src);
     }
-    Model::LinearCache& lc = it->second;
-
-    const double acc_scale = x.scale * wscale;
-    auto bkey = std::make_tuple(li, level, acc_scale);
-    auto bit = M.bias.find(bkey);
-    if (bit == M.bias.end()) {
-        std::vector<u64> b(oc * limbs);
-        for (std::size_t o = 0; o < oc; ++o) {
-            std::vector<u64> res = C.enc->scalar_residues(l.b[o], acc_scale, level);
-            std::copy(res.begin(), res.end(), b.begin() + o * limbs);
-        }
-        bit = M.bias.emplace(bkey, C.upload_vec(b)).first;
-    }
-
+    const double acc_scale = x.scale * C.scale;
+    const u64* bias = detail::linear_bias(C, M, li, level, acc_scale);
     TensorPtr out = make_tensor(C, out_shape.positions(), level - 1, acc_scale / static_cast<double>(C.ring.primes[level]));
     out->shape = out_shape;
     out->batch = x.batch;
-    const std::size_t cw = x.cell_words();
-    const std::size_t per_pixel = oc * cw * 8;
-    const std::size_t pix_chunk = std::max<std::size_t>(1, std::min<std::size_t>(lc.pixels, kScratchBytes / per_pixel));
-    DevBuf pre(&C, pix_chunk * per_pixel);
-    Launch L = C.L();
-    for (std::size_t p0 = 0; p0 < static_cast<std::size_t>(lc.pixels); p0 += pix_chunk) {
-        const std::size_t m = std::min(pix_chunk, lc.pixels - p0);
-        GatherMac g{lc.src.as<int>() + p0 * lc.K, lc.weights.as<ulonglong2>(),
-                    bit->second.as<u64>(), lc.wsplit.as<uint2>(), lc.recomb.as<ulonglong2>(),
-                    static_cast<int>(m), lc.K, lc.oc, lc.oc_pad, lc.oc};
-        if (lc.ksteps) {
-            ImmaMac im{lc.src_pad.as<int>() + p0 * lc.kpad, lc.wfrag.as<uint4>(), bit->second.as<u64>(),
-                       lc.shift.as<double>(), static_cast<int>(m), lc.K, lc.kpad, lc.ksteps, lc.oc, lc.oc_tiles, lc.oc,
-                       lc.wfrag_wide.as<uint4>(), lc.shift_wide.as<ulonglong2>(), lc.wtc.as<uint4>(),
-                       lc.wtc_wide.as<uint4>()};
-            for_limb_runs(C, limbs, [&](std::size_t l0, std::size_t l1, bool tc) {
-                if ((tc || lc.wide_ok) && tc_mac_supported(C.dev, im, !tc))
-                    tc_mac(C.dev, im, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
-                           static_cast<int>(l1), !tc, L);
-                else if (tc || lc.wide_ok)
-                    imma_mac(C.dev, im, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
-                             static_cast<int>(l1), !tc, L);
-                else gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), static_cast<int>(l0),
-                                static_cast<int>(l1), L);
-            });
-        } else {
-            gather_mac(C.dev, g, x.data(), pre.as<u64>(), static_cast<int>(level), 0, static_cast<int>(limbs), L);
-        }
-        rescale(C.dev, pre.as<u64>(), out->cell(p0 * oc), static_cast<int>(level), 2 * m * oc, L);
-    }
+    detail::linear_apply(C, lc, lc.taps, bias, x.data(), level, 0, lc.taps.pixels, out->data());
     return out;
 }
 
@@ -1375,7 +1456,21 @@ TensorPtr forward_encrypted(Context& C, Model& M, const Tensor& x, u64 seed, dou
 
     TensorPtr cur;
     auto current = [&]() -> const Tensor& { return cur ? *cur : x; };
+    std::vector<double> stream_ms(M.layers.size(), 0.0);
+    std::vector<bool> streamed(M.layers.size(), false);
     for (std::size_t i = 0; i < M.layers.size(); ++i) {
+        // layers whose tensors do not fit in device memory run row-streamed (stream.cpp)
+        std::size_t end = i;
+        TensorPtr seg = detail::forward_streamed(C, M, current(), i, end, seed, layer_seconds ? &stream_ms : nullptr);
+        if (seg) {
+            cur = std::move(seg);
+            for (std::size_t j = i; j < end; ++j) {
+                streamed[j] = true;
+                if (layer_seconds) cudaEventRecord(ev[j + 1], C.stream);
+            }
+            i = end - 1;
+            continue;
+        }
         const Layer& l = M.layers[i];
         const u64 layer_seed = derive_seed(seed, 0x1a7e + i);
         Shape in_shape = current().shape;
@@ -1413,8 +1508,8 @@ TensorPtr forward_encrypted(Context& C, Model& M, const Tensor& x, u64 seed, dou
         C.sync();
         for (std::size_t i = 0; i < M.layers.size(); ++i) {
             float ms = 0;
-            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-            layer_seconds[i] = ms / 1000.0;
+            if (!streamed[i]) cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            layer_seconds[i] = (streamed[i] ? stream_ms[i] : ms) / 1000.0;
         }
         for (auto& e : ev) cudaEventDestroy(e);
     }

@@ -34,6 +34,11 @@ public:
     // Return segments that are entirely free to the driver; returns bytes freed.
     std::size_t trim();
     std::size_t reserved() const { return reserved_; }
+    std::size_t free_bytes() const {
+        std::size_t b = 0;
+        for (const auto& f : free_) b += f.second.size;
+        return b;
+    }
 
 private:
     struct Block {
@@ -162,7 +167,8 @@ struct Activation {
     std::size_t encrypted_depth() const;
     void validate() const;
 };
-TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x);
+// dst: optional device storage for the result cells (the returned tensor is then a view of it)
+TensorPtr eval_activation(Context& C, const Activation& act, const Tensor& x, u64* dst = nullptr);
 
 // ---- client side
 TensorPtr encrypt_tensor(Context& C, const double* data, std::size_t batch, std::size_t positions, u64 seed);
@@ -181,25 +187,44 @@ struct Layer {
     const char* kind_name() const;
 };
 
+struct StreamPlan;  // stream.cpp
+
 struct Model {
     Shape input;
     std::vector<Layer> layers;
     std::vector<Activation> acts;
     std::vector<Shape> shapes;  // per-layer output shapes (shape_infer)
+    // tap table of a conv / dense layer: the input cell each (pixel, tap) reads,
+    // -1 for a clipped tap; src_pad is the same padded to whole 32-tap steps
+    // (tensor-core paths). Pixels may be listed in any order.
+    struct Taps {
+        DevBuf src, src_pad;
+        std::size_t pixels = 0;
+    };
     // integer-weight caches, keyed by (layer, level) and (layer, level, scale)
     struct LinearCache {
-        DevBuf src, weights, wsplit, recomb;
-        int pixels = 0, K = 0, oc = 0, oc_pad = 0;
+        DevBuf weights, wsplit, recomb;
+        int K = 0, oc = 0, oc_pad = 0;
+        bool conv = false;
         // integer tensor-core path (limbs with q < 2^40): fragment-ordered weight
-        // byte planes, 2^8s mod q table, taps padded to whole 32-tap steps
-        DevBuf wfrag, shift, src_pad, wfrag_wide, shift_wide;
+        // byte planes, 2^8s mod q table
+        DevBuf wfrag, shift, wfrag_wide, shift_wide;
         DevBuf wtc, wtc_wide;  // tcgen05 weight tiles (conv_tc.cu), when the shape qualifies
         int kpad = 0, ksteps = 0, oc_tiles = 0;
         bool wide_ok = false;  // limbs with q >= 2^40 also on the tensor cores (signed weight digits)
+        Taps taps;             // whole-tensor layout (built on first non-streamed use)
     };
     std::map<std::pair<std::size_t, std::uint32_t>, LinearCache> linear;
     std::map<std::tuple<std::size_t, std::uint32_t, double>, DevBuf> bias;
     std::map<std::pair<std::size_t, std::uint32_t>, DevBuf> pool_srcs;
+
+    // Row-streamed execution of the spatial layers (stream.cpp) for tensors
+    // that do not fit in device memory: 0 = only when the whole-tensor pass
+    // does not fit, 1 = always (tests), 2 = never.
+    int stream_mode = 0;
+    std::size_t stream_tile = 0;  // stage-output columns per tile (0: sized to the budget)
+    std::size_t mem_budget = 0;   // device bytes a forward pass may use (0: what is free)
+    std::map<std::string, std::shared_ptr<StreamPlan>> plans;  // by segment, input level / scale, options
 
     void infer_shapes();
     std::size_t depth_cost() const;

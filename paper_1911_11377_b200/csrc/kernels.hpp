@@ -194,9 +194,10 @@ void tc_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level,
             const Launch& L);
 void imma_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level, int limb0, int limb1, bool wide,
               const Launch& L);
-// 2x2-style average pool: out cell p sums srcs[p][0..taps) then multiplies by w (shoup), level kept
+// 2x2-style average pool: out cell p sums srcs[p][0..taps) (plus y[p] when accumulate)
+// then multiplies by w (shoup; w == null: no multiply), level kept
 void pool_sum_scale(const DevRing& R, const u64* x, const int* srcs, int taps, const ulonglong2* w, u64* y,
-                    int level, std::size_t out_cells, const Launch& L);
+                    int level, std::size_t out_cells, const Launch& L, bool accumulate = false);
 // gather whole cells: y[i] = x[idx[i]] for idx >= 0 (ciphertext-sized copies)
 void gather_cells(const u64* x, const int* idx, u64* y, std::size_t cell_words, std::size_t cells, const Launch& L);
 

@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(GM_TPB, HECNN_GM_MINB) k_gather_mac(DevRing R,
 // avg_pool2d_encrypted (layers.hpp:213-239): sum of the window, times
 // round(Delta / area) (one Shoup multiply), rescale done by the caller.
 __global__ void k_pool(DevRing R, const u64* __restrict__ x, const int* __restrict__ srcs, int taps,
-                       const ulonglong2* __restrict__ w, u64* __restrict__ y, int level) {
+                       const ulonglong2* __restrict__ w, u64* __restrict__ y, int level, int accumulate) {
     const int limbs = level + 1;
     const long long poly_words = static_cast<long long>(limbs) * R.n;
     const long long cell_words = 2 * poly_words;
@@ -221,10 +221,13 @@ __global__ void k_pool(DevRing R, const u64* __restrict__ x, const int* __restri
     const int i = static_cast<int>((col / R.n) % limbs);
     const long long cell = blockIdx.y;
     const u64 q = R.mod[i].q;
-    u64 s = 0;
+    u64 s = accumulate ? y[cell * cell_words + col] : 0;
     for (int k = 0; k < taps; ++k) s = add_mod(s, x[srcs[cell * taps + k] * cell_words + col], q);
-    const ulonglong2 c = w[i];
-    y[cell * cell_words + col] = mul_shoup(s, c.x, c.y, q);
+    if (w) {
+        const ulonglong2 c = w[i];
+        s = mul_shoup(s, c.x, c.y, q);
+    }
+    y[cell * cell_words + col] = s;
 }
 
 __global__ void k_gather_cells(const u64* __restrict__ x, const int* __restrict__ idx, u64* __restrict__ y,
@@ -259,14 +262,15 @@ void gather_mac(const DevRing& R, const GatherMac& g, const u64* x, u64* y, int 
 }
 
 void pool_sum_scale(const DevRing& R, const u64* x, const int* srcs, int taps, const ulonglong2* w, u64* y, int level,
-                    std::size_t out_cells, const Launch& L) {
+                    std::size_t out_cells, const Launch& L, bool accumulate) {
     if (!out_cells) return;
     const long long cell_words = 2LL * (level + 1) * R.n;
     for (std::size_t off = 0; off < out_cells; off += 65535) {
         const std::size_t m = std::min<std::size_t>(65535, out_cells - off);
         dim3 grid(static_cast<unsigned>((cell_words + TPB - 1) / TPB), static_cast<unsigned>(m));
         L.begin("k_pool", double(m) * cell_words, 8.0 * cell_words * m * (taps + 1));
-        k_pool<<<grid, TPB, 0, L.stream>>>(R, x, srcs + off * taps, taps, w, y + off * cell_words, level);
+        k_pool<<<grid, TPB, 0, L.stream>>>(R, x, srcs + off * taps, taps, w, y + off * cell_words, level,
+                                             accumulate ? 1 : 0);
         L.count();
     }
     check_launch("pool_sum_scale");
