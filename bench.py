@@ -4,9 +4,13 @@
 Default workload (N=1): SURVEY §8(d) C4 -- the CIFAR-10-shaped CNN with the
 degree-2 polynomial ReLU on encrypted synthetic 32x32x3 images, preset
 net-n8192-d8 (4096 images packed in the slots of one ciphertext set). C5
-(AlexNet-like at 64x64) does not fit one GPU without the streaming executor
-(DESIGN.md §7), so C4 is the largest single-GPU config; C2's NTT and HE-mul
-ops/s are reported alongside in the same line.
+(AlexNet-like COWC at 64x64x3) needs ~266 GiB of layer rings even when
+row-streamed, more than one B200 holds, so C4 is the largest
+BASELINE config that fits one GPU and is the headline. The same line reports,
+measured: C5's AlexNet stack (alexnet32_preset, large-n16384-d24) on one full
+8192-image set at 32x32x3 (row-streamed), with its 64x64 time extrapolated
+from those per-layer times; C3 (CryptoNets-style) on a full set with its
+output words checked against the reference; C2's NTT and HE-mul ops/s.
 
 A step = forward_encrypted over one set (4096 images) with the input
 ciphertexts resident in HBM (`value`); `e2e` repeats it through the public
@@ -131,10 +135,10 @@ def c3_cryptonets(hb, device, with_reference, stream=None, steps=5):
     return res
 
 
-def crop_extrapolation_check(hb, eng, full_ms, crop=8):
-    """Validates the C5 crop method on C4, where the full set also runs: the
-    C4 stack on a crop x crop x 3 input, each layer's CUDA-event time scaled
-    by the same layer_work ratios, against the measured full 32x32 step."""
+def crop_extrapolation_check(hb, eng, full_ms, crop=16):
+    """Validates C5's 32x32 -> 64x64 extrapolation on C4, where both sizes
+    run: the C4 stack on a crop x crop x 3 input, each layer's CUDA-event time
+    scaled by the same layer_work ratios, against the measured 32x32 step."""
     spec = c4_spec(hb, crop)
     model = eng.model(spec)
     x = eng.encrypt_tensor(np.random.default_rng(3).uniform(0, 1, size=(eng.params.n // 2, spec.input.positions())),
@@ -148,33 +152,50 @@ def crop_extrapolation_check(hb, eng, full_ms, crop=8):
             "ratio": est * 1e3 / full_ms}
 
 
-def c5_extrapolated(hb, device, crop=8, stream=None):
-    """C5 (AlexNet-like COWC, alexnet32_preset layers, large-n16384-d24, 8192
-    images per set): the full stack runs on the GPU on a crop x crop x 3 input
-    (every layer type, every level, the real key-switch/NTT shapes); each
-    layer's CUDA-event time is scaled by the exact work ratio to the 64x64
-    (BASELINE's COWC patches) and 32x32 (the preset / paper) inputs. Small
-    crop layers underfill the GPU, so the estimate is conservative."""
+def c5_measured(hb, device, stream=None, image=32, check=8):
+    """C5 (AlexNet-like COWC: alexnet32_preset layers, large-n16384-d24, 8192
+    images per ciphertext set) on one FULL set of encrypted synthetic
+    image x image x 3 inputs, device-timed with CUDA events. The layer tensors
+    (conv1's output alone is 576 GiB at 32x32) run row-streamed (stream.cpp):
+    rings of rows and column tiles sized to the free HBM. The 64x64 COWC
+    patches need ~266 GiB of rings even streamed, more than one
+    B200 holds, so that size is extrapolated from this measured run's
+    per-layer times by exact work ratios (method checked on C4, 16x16 ->
+    32x32, where both run)."""
+    import torch
     p = hb.preset_params("large-n16384-d24")
+    t0 = time.perf_counter()
     eng = hb.CkksEngine(p, device=device).keygen(1)
     if stream is not None:
         eng.set_stream(stream)
-    spec = hb.glorot_weights(hb.alexnet32_preset(image=crop), 1)
-    x = eng.encrypt_tensor(np.random.default_rng(3).uniform(0, 1, size=(p.n // 2, spec.input.positions())),
-                           seed=11, shape=spec.input)
+    spec = hb.glorot_weights(hb.alexnet32_preset(image=image), 1)
+    data = np.random.default_rng(3).uniform(0, 1, size=(p.n // 2, spec.input.positions()))
+    x = eng.encrypt_tensor(data, seed=11, shape=spec.input)
+    eng.synchronize()
+    setup = time.perf_counter() - t0
     model = eng.model(spec)
     secs = []
-    hb.forward_encrypted(model, x, eng, seed=13, layer_seconds=secs)   # warm-up (weight caches)
-    secs = []
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
     y = hb.forward_encrypted(model, x, eng, seed=13, layer_seconds=secs)
-    work_crop = layer_work(hb, spec)
-    res = {"preset": "large-n16384-d24", "images_per_set": p.n // 2, "crop": f"{crop}x{crop}x3",
-           "crop_forward_s": float(sum(secs)), "out_level": y.level,
-           "layer_s_crop": [round(s, 4) for s in secs]}
-    for full in (64, 32):
-        work_full = layer_work(hb, hb.alexnet32_preset(image=full))
-        t = sum(s * (wf / wc if wc else 1.0) for s, wf, wc in zip(secs, work_full, work_crop))
-        res[f"{full}x{full}"] = {"seconds_per_set": t, "images_per_s": (p.n // 2) / t}
+    e.record()
+    torch.cuda.synchronize()
+    sec = s.elapsed_time(e) / 1e3
+    res = {"preset": "large-n16384-d24", "images_per_set": p.n // 2, "input": f"{image}x{image}x3",
+           "seconds_per_set": sec, "images_per_s": (p.n // 2) / sec, "out_level": y.level,
+           "layer_s": [round(v, 4) for v in secs], "client_encrypt_s": setup,
+           "execution": "one full set, row-streamed spatial layers (rings of rows + column tiles), first run "
+                        "(weight caches and stream plans built inside the timed region)"}
+    if check:
+        from oracle import ref
+        if ref.available():
+            plain = ref.forward_plain(spec, data[:check])
+            dec = 1.0 / (1.0 + np.exp(-eng.decrypt_tensor(y, p.n // 2)[:check]))
+            res["max_abs_err_vs_plain"] = float(np.max(np.abs(dec - plain)))
+    w32, w64 = layer_work(hb, spec), layer_work(hb, hb.alexnet32_preset(image=64))
+    t64 = sum(v * (b / a if a else 1.0) for v, a, b in zip(secs, w32, w64))
+    res["64x64_extrapolated"] = {"seconds_per_set": t64, "images_per_s": (p.n // 2) / t64,
+                                 "method": "measured 32x32 per-layer times x exact per-layer work ratios"}
     del y, x, model
     eng.close()
     return res
@@ -510,11 +531,12 @@ def run_ours(args):
                        "gb_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0}
                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
         del x, y, xe, ye
-        xcheck = crop_extrapolation_check(hb, eng, dev_s / args.steps * 1e3) if world == 1 and not args.no_c5 else None
+        xcheck = (crop_extrapolation_check(hb, eng, dev_s / args.steps * 1e3, crop=16)
+                  if world == 1 and not args.no_c5 else None)
         eng.trim()  # hand C4's cached arena back before the larger C2/C5 runs
         # single-GPU reference figures: at N > 1 the other ranks would idle at the final barrier
         mb = microbench(hb, local) if world == 1 and not args.no_micro else None
-        c5 = c5_extrapolated(hb, local, stream=stream.cuda_stream) if world == 1 and not args.no_c5 else None
+        c5 = c5_measured(hb, local, stream=stream.cuda_stream) if world == 1 and not args.no_c5 else None
         if c5 is not None:
             c5["method_check_on_c4"] = xcheck
         c3 = (c3_cryptonets(hb, local, with_reference=not args.no_cpu_baseline, stream=stream.cuda_stream)
@@ -542,7 +564,7 @@ def run_ours(args):
                         "d2h_bytes_per_step": out_words_n * 8},
                 "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "output": {"cells": out_cells, "level": out_level},
-                "microbench_c2": mb, "c3_cryptonets": c3, "c5_alexnet_cowc_extrapolated": c5, "kernels": kernels}
+                "microbench_c2": mb, "c3_cryptonets": c3, "c5_alexnet_cowc": c5, "kernels": kernels}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -557,7 +579,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-micro", action="store_true")
-    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (AlexNet-COWC) crop extrapolation")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (AlexNet-COWC) full-set run and C3")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -1036,16 +1036,17 @@ void for_limb_runs(const Context& C, std::size_t limbs, F f) {
 // A fragments of mma.m16n8k32 (row-major 16 x 32): lane (g, t) holds
 // reg0 = row g, k 4t..4t+3; reg1 = row g+8, same k; reg2/reg3 = the same rows
 // at k + 16; byte u of a register is k + u. Row = output channel in the tile.
-void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulonglong2>& w, std::size_t rows,
+void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<u64>& w, std::size_t rows,
                       std::size_t limbs) {
     const std::size_t K = rows, oc = static_cast<std::size_t>(lc.oc), oc_pad = static_cast<std::size_t>(lc.oc_pad);
     const std::size_t ksteps = (K + 31) / 32, kpad = ksteps * 32;
     std::size_t tiles = (oc + 15) / 16;
     if (tiles >= 2) tiles = (tiles + 1) / 2 * 2;  // the kernel pairs tiles
     std::vector<std::uint32_t> frag(limbs * tiles * ksteps * 5 * 32 * 4, 0u);
-    for (std::size_t i = 0; i < limbs; ++i) {
-        if (!imma_limb(C, i)) continue;
-        for (std::size_t t = 0; t < tiles; ++t)
+    parallel_items(limbs * tiles, [&](std::size_t it) {
+        const std::size_t i = it / tiles, t = it % tiles;
+        if (!imma_limb(C, i)) return;
+        {
             for (std::size_t ks = 0; ks < ksteps; ++ks)
                 for (std::size_t lane = 0; lane < 32; ++lane) {
                     const std::size_t g = lane >> 2, tq = lane & 3;
@@ -1054,7 +1055,7 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
                         const std::size_t k0 = ks * 32 + 4 * tq + ((r & 2) ? 16 : 0);
                         std::uint64_t wv[4] = {0, 0, 0, 0};
                         for (int u = 0; u < 4; ++u)
-                            if (o < oc && k0 + u < K) wv[u] = w[(i * rows + k0 + u) * oc_pad + o].x;
+                            if (o < oc && k0 + u < K) wv[u] = w[(i * rows + k0 + u) * oc_pad + o];
                         for (int b = 0; b < 5; ++b) {
                             std::uint32_t reg = 0;
                             for (int u = 0; u < 4; ++u) reg |= static_cast<std::uint32_t>((wv[u] >> (8 * b)) & 0xFF) << (8 * u);
@@ -1062,7 +1063,8 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
                         }
                     }
                 }
-    }
+        }
+    });
     // signed weight integers W (|W| < 2^47) recovered from the widest limb and
     // checked against every limb's residue; their balanced base-256 digits
     // feed the wide-limb kernel
@@ -1070,23 +1072,25 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
     for (std::size_t i = 1; i < limbs; ++i)
         if (C.ring.primes[i] > C.ring.primes[wl]) wl = i;
     const std::int64_t wmax = 127LL * ((1LL << 48) - 1) / 255;  // 6 balanced digits
-    bool wide_ok = true;
     std::vector<std::int64_t> W(K * oc, 0);
-    for (std::size_t k = 0; k < K && wide_ok; ++k)
-        for (std::size_t o = 0; o < oc && wide_ok; ++o) {
-            const u64 qw = C.ring.primes[wl], r = w[(wl * rows + k) * oc_pad + o].x;
+    std::vector<char> row_ok(K, 1);
+    parallel_items(K, [&](std::size_t k) {
+        for (std::size_t o = 0; o < oc && row_ok[k]; ++o) {
+            const u64 qw = C.ring.primes[wl], r = w[(wl * rows + k) * oc_pad + o];
             const std::int64_t v = r > qw / 2 ? -static_cast<std::int64_t>(qw - r) : static_cast<std::int64_t>(r);
-            if (v > wmax || v < -wmax) wide_ok = false;
-            for (std::size_t i = 0; i < limbs && wide_ok; ++i) {
+            if (v > wmax || v < -wmax) row_ok[k] = 0;
+            for (std::size_t i = 0; i < limbs && row_ok[k]; ++i) {
                 const u64 qi = C.ring.primes[i];
                 const u64 ri = v >= 0 ? static_cast<u64>(v) % qi : (qi - static_cast<u64>(-v) % qi) % qi;
-                if (ri != w[(i * rows + k) * oc_pad + o].x) wide_ok = false;
+                if (ri != w[(i * rows + k) * oc_pad + o]) row_ok[k] = 0;
             }
             W[k * oc + o] = v;
         }
+    });
+    const bool wide_ok = std::all_of(row_ok.begin(), row_ok.end(), [](char c) { return c != 0; });
     if (wide_ok) {
         std::vector<std::uint32_t> fw(tiles * ksteps * 6 * 32 * 4, 0u);
-        for (std::size_t t = 0; t < tiles; ++t)
+        parallel_items(tiles, [&](std::size_t t) {
             for (std::size_t ks = 0; ks < ksteps; ++ks)
                 for (std::size_t lane = 0; lane < 32; ++lane) {
                     const std::size_t g = lane >> 2, tq = lane & 3;
@@ -1110,6 +1114,7 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
                         }
                     }
                 }
+        });
         std::vector<ulonglong2> shw(limbs * 16, make_ulonglong2(0, 0));
         for (std::size_t i = 0; i < limbs; ++i)
             for (int s = 0; s < 13; ++s) {
@@ -1131,9 +1136,10 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
     const char* no_tc = std::getenv("HECNN_NO_TCGEN05");
     if (!(no_tc && *no_tc == '1') && lc.conv && ksteps <= 192 && C.n() % 128 == 0 && wtc_bytes <= (std::size_t(1) << 30)) {
         std::vector<std::uint8_t> t(wtc_bytes, 0);
-        for (std::size_t i = 0; i < limbs; ++i) {
-            if (!imma_limb(C, i)) continue;
-            for (std::size_t ot = 0; ot < ttiles; ++ot)
+        parallel_items(limbs * ttiles, [&](std::size_t it) {
+            const std::size_t i = it / ttiles, ot = it % ttiles;
+            if (!imma_limb(C, i)) return;
+            {
                 for (std::size_t ks = 0; ks < ksteps; ++ks) {
                     std::uint8_t* tile = t.data() + ((i * ttiles + ot) * ksteps + ks) * tile_bytes;
                     for (std::size_t o = 0; o < TOC; ++o) {
@@ -1142,7 +1148,7 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
                         for (std::size_t k = 0; k < 32; ++k) {
                             const std::size_t kk = ks * 32 + k;
                             if (kk >= K) continue;
-                            const u64 v = w[(i * rows + kk) * oc_pad + oo].x;
+                            const u64 v = w[(i * rows + kk) * oc_pad + oo];
                             for (std::size_t b = 0; b < 5; ++b) {
                                 const std::size_t n = b * TOC + o;
                                 tile[(n >> 3) * 256 + (k >> 4) * 128 + (n & 7) * 16 + (k & 15)] =
@@ -1151,7 +1157,8 @@ void build_imma_cache(Context& C, Model::LinearCache& lc, const std::vector<ulon
                         }
                     }
                 }
-        }
+            }
+        });
         lc.wtc = C.upload_vec(t);
         if (wide_ok) {
             // the 60-bit limb: the balanced signed base-256 digits of W (one copy for all
@@ -1211,17 +1218,22 @@ Model::LinearCache& linear_weights(Context& C, Model& M, std::size_t li, std::ui
     lc.K = static_cast<int>(rows);
     lc.oc = static_cast<int>(oc);
     lc.oc_pad = static_cast<int>((oc + 15) / 16 * 16);
-    std::vector<ulonglong2> w(rows * lc.oc_pad * limbs, make_ulonglong2(0, 0));
-    std::vector<uint2> ws(rows * lc.oc_pad * limbs, make_uint2(0, 0));
-    for (std::size_t r = 0; r < rows; ++r)
-        for (std::size_t o = 0; o < oc; ++o) {
-            std::vector<u64> res = C.enc->scalar_residues(l.w[r * oc + o], C.scale, level);
-            for (std::size_t i = 0; i < limbs; ++i) {
-                const std::size_t at = (i * rows + r) * lc.oc_pad + o;  // limb-major: OCT channels contiguous
-                w[at] = make_ulonglong2(res[i], shoup_of(res[i], C.ring.primes[i]));
-                ws[at] = make_uint2(static_cast<unsigned>(res[i] & 0x1FFFFFu), static_cast<unsigned>(res[i] >> 21));
+    // make_scalar_plain per weight (host roundl / fmod), rows in parallel; the
+    // first failing range check is rethrown in row order
+    std::vector<u64> w(rows * lc.oc_pad * limbs, 0);  // [limbs][rows][oc_pad]: OCT channels contiguous
+    std::vector<std::string> errs(rows);
+    parallel_items(rows, [&](std::size_t r) {
+        try {
+            for (std::size_t o = 0; o < oc; ++o) {
+                std::vector<u64> res = C.enc->scalar_residues(l.w[r * oc + o], C.scale, level);
+                for (std::size_t i = 0; i < limbs; ++i) w[(i * rows + r) * lc.oc_pad + o] = res[i];
             }
+        } catch (const std::exception& e) {
+            errs[r] = e.what();
         }
+    });
+    for (const auto& e : errs)
+        if (!e.empty()) throw std::invalid_argument(e);
     std::vector<ulonglong2> rc(2 * limbs);
     for (std::size_t i = 0; i < limbs; ++i) {
         const HostMod& m = C.ring.mods[i];
@@ -1229,10 +1241,22 @@ Model::LinearCache& linear_weights(Context& C, Model& M, std::size_t li, std::ui
         rc[2 * i] = make_ulonglong2(a, shoup_of(a, m.q));
         rc[2 * i + 1] = make_ulonglong2(b, shoup_of(b, m.q));
     }
-    lc.wsplit = C.upload_vec(ws);
     lc.recomb = C.upload_vec(rc);
-    lc.weights = C.upload_vec(w);
     if (imma_enabled(C, rows)) build_imma_cache(C, lc, w, rows, limbs);
+    if (!lc.ksteps || !lc.wide_ok) {
+        // gather-MAC operands (some limb is not on the tensor cores): Shoup pairs
+        // and the 21-bit split of each residue
+        std::vector<ulonglong2> wp(w.size());
+        std::vector<uint2> ws(w.size());
+        parallel_items(limbs, [&](std::size_t i) {
+            for (std::size_t at = i * rows * lc.oc_pad; at < (i + 1) * rows * lc.oc_pad; ++at) {
+                wp[at] = make_ulonglong2(w[at], shoup_of(w[at], C.ring.primes[i]));
+                ws[at] = make_uint2(static_cast<unsigned>(w[at] & 0x1FFFFFu), static_cast<unsigned>(w[at] >> 21));
+            }
+        });
+        lc.weights = C.upload_vec(wp);
+        lc.wsplit = C.upload_vec(ws);
+    }
     return M.linear.emplace(key, std::move(lc)).first->second;
 }
 

@@ -242,9 +242,7 @@ TensorPtr forward_streamed(Context& C, Model& M, const Tensor& x, std::size_t fi
                               M.acts[static_cast<std::size_t>(M.layers[static_cast<std::size_t>(s.act)].act)].encrypted_depth())
             return nullptr;  // the whole-tensor path raises the reference's error
 
-    // ---- memory plan: hand wholly free arena segments back first so the
-    // stores below get contiguous memory
-    if (!M.mem_budget) C.arena.trim();
+    // ---- memory plan
     const std::size_t avail = M.mem_budget ? M.mem_budget : avail_bytes(C);
     if (trace_on()) {
         std::size_t fr = 0, tot = 0;
@@ -281,6 +279,9 @@ TensorPtr forward_streamed(Context& C, Model& M, const Tensor& x, std::size_t fi
     };
     const bool fits_whole = full_peak(first, x.shape, x.level) + margin <= avail;
     if (M.stream_mode == 0 && fits_whole) return nullptr;
+    // streaming: hand wholly free arena segments back so the stores below get
+    // contiguous memory (only here -- cudaFree synchronises the device)
+    if (!M.mem_budget) C.arena.trim();
 
     // rings: store s (s >= 1) keeps the window of rows stage s reads
     const std::size_t S = st.size();
