@@ -28,9 +28,16 @@
 namespace hecnn_b200 {
 namespace ntt {
 
-__device__ __forceinline__ int swz(int i) {
+__host__ __device__ __forceinline__ constexpr int swz(int i) {
     return i ^ static_cast<int>((0x1eb4d278963c5af0ull >> (4 * ((i >> 4) & 15))) & 15);
 }
+// swz is GF(2)-linear (the nibble table is a linear map of bits 4..7 onto
+// bits 0..3), so for a unit's positions base | k * STRIDE (disjoint bit
+// fields) swz(base | k * STRIDE) == swz(base) ^ swz(k * STRIDE): one XOR with
+// a compile-time constant per element instead of the table lookup.
+static_assert(swz(0x50) == (swz(0x10) ^ swz(0x40)) && swz(0xf3) == (swz(0xf0) ^ 3) &&
+                  swz(0xa7) == (swz(0x80) ^ swz(0x20) ^ 7),
+              "swizzle must be GF(2)-linear");
 
 __device__ __forceinline__ void ct_butterfly(u64& a, u64& b, ulonglong2 w, u64 q, u64 two_q) {
     u64 u = a;
@@ -187,11 +194,13 @@ __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __r
         if (UNITS % T != 0 && u >= UNITS) break;
         const int grp = u / STRIDE, col = u % STRIDE;
         const int base = grp * G + col;
+        const int sb = swz(base);
         V x[E];
 #pragma unroll
         for (int k = 0; k < E; ++k) {
             // loads that can use the (unit, element) slot, e.g. prefetched registers
-            if constexpr (std::is_invocable_v<Load, int, int, int>) x[k] = load(base + k * STRIDE, uu, k);
+            if constexpr (std::is_same<Load, SmemLoad<V>>::value) x[k] = load.s[sb ^ swz(k * STRIDE)];
+            else if constexpr (std::is_invocable_v<Load, int, int, int>) x[k] = load(base + k * STRIDE, uu, k);
             else x[k] = load(base + k * STRIDE);
         }
 #pragma unroll
@@ -206,7 +215,10 @@ __device__ __forceinline__ void fwd_round(const A& ar, const typename A::TW* __r
             }
         }
 #pragma unroll
-        for (int k = 0; k < E; ++k) store(base + k * STRIDE, x[k], uu, k);
+        for (int k = 0; k < E; ++k) {
+            if constexpr (std::is_same<Store, SmemStore<V>>::value) store.s[sb ^ swz(k * STRIDE)] = x[k];
+            else store(base + k * STRIDE, x[k], uu, k);
+        }
     }
     }
 }
@@ -311,9 +323,13 @@ __device__ __forceinline__ void inv_round(const A& ar, const typename A::TW* __r
         if (UNITS % T != 0 && u >= UNITS) break;
         const int grp = u / STRIDE, col = u % STRIDE;
         const int base = grp * G + col;
+        const int sb = swz(base);
         V x[E];
 #pragma unroll
-        for (int k = 0; k < E; ++k) x[k] = load(base + k * STRIDE);
+        for (int k = 0; k < E; ++k) {
+            if constexpr (std::is_same<Load, SmemLoad<V>>::value) x[k] = load.s[sb ^ swz(k * STRIDE)];
+            else x[k] = load(base + k * STRIDE);
+        }
 #pragma unroll
         for (int rho = R - 1; rho >= 0; --rho) {
             const int half = E >> (rho + 1);
@@ -328,7 +344,8 @@ __device__ __forceinline__ void inv_round(const A& ar, const typename A::TW* __r
 #pragma unroll
         for (int k = 0; k < E; ++k) {
             ar.round_end_inv(x[k]);
-            store(base + k * STRIDE, x[k], uu, k);
+            if constexpr (std::is_same<Store, SmemStore<V>>::value) store.s[sb ^ swz(k * STRIDE)] = x[k];
+            else store(base + k * STRIDE, x[k], uu, k);
         }
     }
 }
