@@ -319,6 +319,34 @@ Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, doubl
     dev.inv_f = tables.back().as<double>();
     tables.push_back(upload_vec(ring.n_inv_f));
     dev.n_inv_f = tables.back().as<double>();
+    {
+        // key-switch block twiddle tables (DevRing::ks_tw): identical to the
+        // forward tables unless N > 2^13 blocks
+        const std::size_t lb = std::min<std::size_t>(ring.logn, 13), B = std::size_t(1) << lb, C = ring.logn - lb;
+        if (C == 0) {
+            dev.ks_tw = dev.fwd;
+            dev.ks_tw_f = dev.fwd_f;
+        } else {
+            const std::size_t nn = ring.n, NB = nn / B;
+            std::vector<u64> ti(2 * ring.limbs * nn, 0);
+            std::vector<double> tf(ring.limbs * nn, 0.0);
+            for (std::size_t l = 0; l < ring.limbs; ++l)
+                for (std::size_t b = 0; b < NB; ++b)
+                    for (std::size_t j = 1; j < B; ++j) {
+                        std::size_t sh = 0;
+                        while ((std::size_t(2) << sh) <= j) ++sh;
+                        const std::size_t m = j - (std::size_t(1) << sh);
+                        const std::size_t src = (std::size_t(1) << (sh + C)) + (b << sh) + m, dst = b * B + j;
+                        ti[2 * (l * nn + dst)] = ring.fwd[2 * (l * nn + src)];
+                        ti[2 * (l * nn + dst) + 1] = ring.fwd[2 * (l * nn + src) + 1];
+                        tf[l * nn + dst] = ring.fwd_f[l * nn + src];
+                    }
+            tables.push_back(upload_vec(ti));
+            dev.ks_tw = tables.back().as<ulonglong2>();
+            tables.push_back(upload_vec(tf));
+            dev.ks_tw_f = tables.back().as<double>();
+        }
+    }
     dev.n = static_cast<int>(ring.n);
     dev.logn = static_cast<int>(ring.logn);
     dev.limbs = static_cast<int>(ring.limbs);

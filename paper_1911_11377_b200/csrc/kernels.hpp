@@ -31,6 +31,11 @@ struct DevRing {
     const double* fwd_f = nullptr;           // [limbs][n]
     const double* inv_f = nullptr;           // [limbs][n]
     const double* n_inv_f = nullptr;         // [limbs]
+    // key-switch block-local twiddle tables (keyswitch.cu): for blocks of
+    // B = 2^min(logn, 13) words, [limb][block][j] = fwd[2^(s+C) + block 2^s + m]
+    // with j = 2^s + m, C = logn - log2 B (== fwd / fwd_f when N <= 2^13)
+    const ulonglong2* ks_tw = nullptr;       // [limbs][n]
+    const double* ks_tw_f = nullptr;         // [limbs][n]
     unsigned long long int_limbs = 0;        // bit i: q_i >= 2^42 (integer-pipe path), for i < 64
     bool small_primes = false;               // some q_i <= 2^20: key-switch digits need v mod q_i
 };

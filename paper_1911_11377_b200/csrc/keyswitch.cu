@@ -17,10 +17,14 @@
 //   a 2^13 block and recomputes the C = log2(N) - 13 column stages for its
 //   block directly from the (L2-resident) u32 digits.
 
+#include <algorithm>
+#include <cmath>
 #include <stdexcept>
 #include <type_traits>
 
 #include "ntt_core.cuh"
+
+#pragma nv_diag_suppress 177  // KsShape constants unused by some instantiations
 
 namespace hecnn_b200 {
 
@@ -142,19 +146,6 @@ __device__ __forceinline__ void ks_mbar_wait(uint64_t* b, unsigned parity) {
                  "l"(src), "r"(bytes), "r"(ks_saddr(bar))
                  : "memory");
 }
-// ---- CTA-pair (cluster of 2) helpers for the shared column stage ------------
-__device__ __forceinline__ void ks_cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t ks_mapa(uint32_t saddr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void ks_st_cluster(uint32_t addr, double v) {
-    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
-}
-
 // EL doubles of this thread's TMEM lane at column `col` (2 x 32-bit columns each)
 template <int EL>
 __device__ __forceinline__ void tmem_ld_d(uint32_t addr, double (&v)[EL]) {
@@ -272,10 +263,11 @@ __device__ __forceinline__ double column_value_fp(const u32* __restrict__ dig, c
 // every t. The last round's units are EL consecutive words (its stride is 1),
 // so the MAC runs once per unit with 16-byte evk loads (KeyAt::unit) instead
 // of one 8-byte load per word. A = IntArith (u64 Shoup, evk + evk_sh) or
-// FpArith (exact FP64, evk_f = e as doubles). The block's twiddles are staged
-// once in shared memory as a block-local table TL[2^s + m] =
-// tw[2^(s+C) + b 2^s + m] and reused by all D digit transforms (round code
-// indexes it with b = c = 0).
+// FpArith (exact FP64, evk_f = e as doubles). The block's twiddles sit in
+// shared memory as a block-local table TL[2^s + m] = tw[2^(s+C) + b 2^s + m]
+// (precomputed per (limb, block) in DevRing::ks_tw / ks_tw_f and bulk-copied
+// when a CTA moves to another limb or block) and are reused by all D digit
+// transforms (round code indexes it with b = c = 0).
 // FP64 path (all limbs but the 60-bit q0): the c1 accumulator lives in tensor
 // memory (TM below; without it, in a thread-private [slot][thread] shared-
 // memory layout), the shared memory the integer path needs for its 16-byte
@@ -284,130 +276,95 @@ __device__ __forceinline__ double column_value_fp(const u32* __restrict__ dig, c
 // digit is transformed.
 // LIFT: some prime of the chain is <= 2^20, so digits need v mod q_i
 // (ckks.hpp:622); otherwise every digit is already a residue.
-template <int LOGN, int LOGB, int LOGE, int T, bool LIFT, class A, class KeyAt>
-__device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typename A::TW* tw, const u32* digits,
-                                        KeyAt key, u64* acc01, int level, int D, long long ct, int i, int b, u64 q,
-                                        int mode, const u64* fy) {
-    using V = typename A::V;
-    using TW = typename A::TW;
-    constexpr bool FP = std::is_same<V, double>::value;
-    extern __shared__ u64 smem[];
-    constexpr int B = 1 << LOGB, C = LOGN - LOGB;
-    constexpr int SL = ntt::last_round_start(LOGB, LOGE);
-    constexpr int RL = LOGB - SL, EL = 1 << RL, UL = B >> RL, PL = (UL + T - 1) / T;
-    static_assert(EL % 2 == 0, "last round units must hold an even number of words");
+//
+// The kernel is persistent: a CTA keeps its tensor-memory allocation and
+// mbarriers and walks work items (ciphertext, limb, block) with a grid
+// stride, so one item's epilogue overlaps the next item's first round on
+// other warps and the per-CTA setup is paid once.
+template <int LOGN, int LOGB, int LOGE, int T, bool FP>
+struct KsShape {
+    static constexpr int B = 1 << LOGB, C = LOGN - LOGB;
+    static constexpr int SL = ntt::last_round_start(LOGB, LOGE);
+    static constexpr int RL = LOGB - SL, EL = 1 << RL, UL = B >> RL, PL = (UL + T - 1) / T;
     // c1 accumulator slots: thread-private [slot][thread] when every thread
     // owns PL whole units (fits the B-word region), else at swizzled positions
-    constexpr bool PRIV = UL % T == 0;
-    static_assert(!ntt::Split<LOGB, LOGE, T>::on || UL % T == 0, "split blocks own whole last-round units");
-    // first round (S0 = 0): unit u owns positions u + k * STR0, k < E0
-    constexpr int R0 = ntt::round_size(LOGB, LOGE, 0), E0 = 1 << R0, U0 = B >> R0, P0 = (U0 + T - 1) / T;
-    constexpr int STR0 = U0;
-#ifndef HECNN_KS_PF_COL
-#define HECNN_KS_PF_COL 0
-#endif
-    // FP64 path: the next digit's first-round inputs are loaded into registers
-    // while the current digit is transformed; with one column stage (C = 1) the
-    // two inputs of each element's column butterfly are prefetched
-#ifndef HECNN_KS_CLUSTER
-#define HECNN_KS_CLUSTER 0
-#endif
-    // CL: the two block CTAs of a limb polynomial (N = 2^14) run as a cluster;
-    // each computes the column butterfly for half of the positions once and
-    // writes both outputs -- its own into its shared memory, the other block's
-    // into the peer's through distributed shared memory -- instead of every
-    // CTA recomputing the stage for all of its positions
-    constexpr bool CL = FP && C == 1 && HECNN_KS_CLUSTER;
-    constexpr bool PREFETCH = FP && !CL && (C == 0 || (HECNN_KS_PF_COL && C == 1));
-    constexpr int PFW = C == 0 ? 1 : 2;  // words per first-round element
-    const long long n = 1LL << LOGN;
-    const long long blk_off = static_cast<long long>(b) << LOGB;
-    const ulonglong2* itw = R.fwd + (static_cast<long long>(i) << LOGN);  // integer twiddles for the column stages
-
+    static constexpr bool PRIV = UL % T == 0;
 #ifndef HECNN_KS_TMEM
 #define HECNN_KS_TMEM 1
 #endif
     // TM: the c1 accumulators live in tensor memory (thread-private lane
     // columns, tcgen05.ld/st) and the shared-memory region they used holds
     // the digit's b_t slice, bulk-copied in while the previous digit's
-    // transform runs; a_t still streams from L2
-    constexpr bool TM = FP && PRIV && HECNN_KS_TMEM && EL == 4;
-    // TM2: c0 in tensor memory too; the registers it frees hold this thread's
-    // a_t words, loaded one digit ahead, so the last round reads no evk from L2
-    constexpr bool TM2 = TM && HECNN_KS_TMEM >= 2;
+    // transform runs; a_t streams from L2
+    static constexpr bool TM = FP && PRIV && HECNN_KS_TMEM && EL == 4;
     // TMI: the integer (60-bit limb) path keeps its c1 accumulators in tensor
     // memory as well (its 16-byte Shoup twiddles leave no shared memory to stage evk)
-    constexpr bool TMI = !FP && PRIV && HECNN_KS_TMEM && EL == 4;
-    constexpr bool USE_TMEM = TM || TMI;
-    constexpr int TCW = (TM2 ? 4 : 2) * PL * EL;  // tensor-memory columns per thread
+    static constexpr bool TMI = !FP && PRIV && HECNN_KS_TMEM && EL == 4;
+    static constexpr bool USE_TMEM = TM || TMI;
+    static constexpr int TCW = 2 * PL * EL;  // tensor-memory columns per thread
+    static constexpr int TNEED = (T / 128) * TCW;
+    static constexpr int TCOLS = TNEED <= 32 ? 32 : (TNEED <= 64 ? 64 : (TNEED <= 128 ? 128 : (TNEED <= 256 ? 256 : 512)));
+    static_assert(!USE_TMEM || TNEED <= 512, "key switch: tensor-memory accumulators exceed the 512 TMEM columns");
+    static_assert(EL % 2 == 0, "last round units must hold an even number of words");
+    static_assert(!ntt::Split<LOGB, LOGE, T>::on || UL % T == 0, "split blocks own whole last-round units");
+    // first round (S0 = 0): unit u owns positions u + k * STR0, k < E0
+    static constexpr int R0 = ntt::round_size(LOGB, LOGE, 0), E0 = 1 << R0, U0 = B >> R0, P0 = (U0 + T - 1) / T;
+    static constexpr int STR0 = U0;
+    // FP64 path, N <= 2^LOGB: the next digit's first-round inputs are loaded
+    // into registers while the current digit is transformed
+    static constexpr bool PREFETCH = FP && C == 0;
+};
+
+// Shared-memory map (dynamic): data [B] words | twiddle table [B] TW | FP:
+// c1 accumulators or b_t stage [B] doubles | 2 mbarriers (b_t, twiddles).
+template <int LOGN, int LOGB, int LOGE, int T, bool LIFT, class A, class KeyAt>
+__device__ __forceinline__ void ks_item(const DevRing& R, const A& ar, const typename A::TW* tw_block,
+                                        bool load_tw, const u32* digits, KeyAt key, u64* acc01, int level, int D,
+                                        long long ct, int i, int b, u64 q, int mode, const u64* fy, uint32_t tm_lane,
+                                        unsigned& bphase, unsigned& tphase) {
+    using V = typename A::V;
+    using TW = typename A::TW;
+    constexpr bool FP = std::is_same<V, double>::value;
+    using S = KsShape<LOGN, LOGB, LOGE, T, FP>;
+    constexpr int B = S::B, C = S::C, EL = S::EL, PL = S::PL, UL = S::UL, E0 = S::E0, U0 = S::U0, P0 = S::P0;
+    constexpr int STR0 = S::STR0;
+    constexpr bool PRIV = S::PRIV, TM = S::TM, TMI = S::TMI, USE_TMEM = S::USE_TMEM, PREFETCH = S::PREFETCH;
+    extern __shared__ u64 smem[];
+    const long long n = 1LL << LOGN;
+    const long long blk_off = static_cast<long long>(b) << LOGB;
+    const ulonglong2* itw = R.fwd + (static_cast<long long>(i) << LOGN);  // integer twiddles for the column stages
     TW* stw = reinterpret_cast<TW*>(smem + B);
     double* sacc = reinterpret_cast<double*>(smem + 2 * B);  // FP path: c1 accumulators (TM: b_t staging)
     uint64_t* bbar = reinterpret_cast<uint64_t*>(smem + 3 * B);
-    constexpr int TNEED = (T / 128) * TCW;
-    constexpr int TCOLS = TNEED <= 32 ? 32 : (TNEED <= 64 ? 64 : (TNEED <= 128 ? 128 : (TNEED <= 256 ? 256 : 512)));
-    static_assert(!USE_TMEM || TNEED <= 512, "key switch: tensor-memory accumulators exceed the 512 TMEM columns");
-    uint32_t tm_lane = 0;
+    uint64_t* tbar = bbar + 1;
+
+    // the previous item's rounds are over (barrier after its last digit):
+    // shared memory may be refilled
+    if (threadIdx.x == 0) {
+        if (load_tw) ks_bulk_load(stw, tw_block, B * sizeof(TW), tbar);
+        if constexpr (TM) ks_bulk_load(sacc, key.evk_f + key.ioff + blk_off, B * 8, bbar);  // b_0 of this block
+    }
     if constexpr (USE_TMEM) {
-        __shared__ uint32_t tm_slot;
-        if (threadIdx.x < 32) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ks_saddr(&tm_slot)), "n"(TCOLS));
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-        }
-        if (TM && threadIdx.x == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(bbar)));
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int w = threadIdx.x >> 5;
-        tm_lane = tm_slot + (static_cast<uint32_t>((w & 3) * 32) << 16) + static_cast<uint32_t>((w >> 2) * TCW);
         const u64 z[EL] = {};
 #pragma unroll
-        for (int uu = 0; uu < TCW / (2 * EL); ++uu) tmem_st_u<EL>(tm_lane + uu * 2 * EL, z);
+        for (int uu = 0; uu < S::TCW / (2 * EL); ++uu) tmem_st_u<EL>(tm_lane + uu * 2 * EL, z);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        if constexpr (TM) {
-            if (threadIdx.x == 0) ks_bulk_load(sacc, key.evk_f + key.ioff + blk_off, B * 8, bbar);  // b_0 of this block
-        }
     }
     auto slot = [&](int idx, int uu, int k) -> int {
         if constexpr (PRIV) { (void)idx; return (uu * EL + k) * T + threadIdx.x; }
         else { (void)uu; (void)k; return ntt::swz(idx); }
     };
-    for (int j = threadIdx.x + 1; j < B; j += T) {
-        const int s = 31 - __clz(j), m = j - (1 << s);
-        stw[j] = tw[(1 << (s + C)) + (b << s) + m];
-    }
     if constexpr (FP && !TM) {
         for (int j = threadIdx.x; j < B; j += T) sacc[j] = 0.0;
     }
-    __syncthreads();  // table complete before the first round reads it
 
-    V a0[PL * EL], a1[(FP || TMI) ? 1 : PL * EL];  // TM2: a0 holds the a_t words of the last-round units
+    V a0[PL * EL], a1[(FP || TMI) ? 1 : PL * EL];
 #pragma unroll
     for (int k = 0; k < PL * EL; ++k) a0[k] = V(0);
-    // c1 (TM) and c0 (TM2) tensor-memory columns of unit slot uu
-    const uint32_t c1col = tm_lane + (TM2 ? 2 * PL * EL : 0);
-    auto load_a = [&](int t) {
-        if constexpr (TM2) {
-#pragma unroll
-            for (int uu = 0; uu < PL; ++uu) {
-                const double2* ka = reinterpret_cast<const double2*>(key.evk_f + (2LL * t + 1) * key.key_stride + key.ioff + blk_off +
-                                                                     ntt::fwd_last_base<LOGB, LOGE, T>(uu));
-#pragma unroll
-                for (int k = 0; k < EL / 2; ++k) {
-                    const double2 w2 = __ldg(ka + k);
-                    a0[uu * EL + 2 * k] = w2.x;
-                    a0[uu * EL + 2 * k + 1] = w2.y;
-                }
-            }
-        }
-    };
-    if constexpr (TM2) load_a(0);
 #pragma unroll
     for (int k = 0; k < ((FP || TMI) ? 1 : PL * EL); ++k) a1[k] = V(0);
 
-    u32 pf[PREFETCH ? P0 * E0 * PFW : 1];
+    u32 pf[PREFETCH ? P0 * E0 : 1];
     auto prefetch = [&](int t) {
         if constexpr (PREFETCH) {
             const u32* dig = digits + (ct * D + t) * n;
@@ -415,85 +372,49 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
             for (int uu = 0; uu < P0; ++uu) {
                 const int u = threadIdx.x + uu * T;
 #pragma unroll
-                for (int k = 0; k < E0; ++k)
-#pragma unroll
-                    for (int h = 0; h < PFW; ++h)
-                        pf[(uu * E0 + k) * PFW + h] = (U0 % T != 0 && u >= U0) ? 0u : __ldg(dig + u + k * STR0 + h * B);
+                for (int k = 0; k < E0; ++k) pf[uu * E0 + k] = (U0 % T != 0 && u >= U0) ? 0u : __ldg(dig + u + k * STR0);
             }
         }
     };
-    // the column stage's twiddle (stage 0 of the N-point transform) for C = 1
-    const double w_col = (PREFETCH && C == 1) ? R.fwd_f[(static_cast<long long>(i) << LOGN) + 1] : 0.0;
     prefetch(0);
+    if (load_tw) {
+        ks_mbar_wait(tbar, tphase & 1);  // twiddle table landed
+        ++tphase;
+    }
+    if constexpr (!TM) __syncthreads();  // zeroed c1 slots before any thread accumulates
 
     auto lift = [&](u32 v) -> u64 {
         if constexpr (LIFT) return lift_digit(v, q);
         else return v;
     };
-    const double w_cl = CL ? R.fwd_f[(static_cast<long long>(i) << LOGN) + 1] : 0.0;
-    if constexpr (CL) ks_cluster_sync();  // the peer CTA is running before its shared memory is written
     for (int t = 0; t < D; ++t) {
         const u32* dig = digits + (ct * D + t) * n;
-        if constexpr (CL) {
-            double* sdata = reinterpret_cast<double*>(smem);
-            const uint32_t peer = ks_mapa(ks_saddr(sdata), static_cast<uint32_t>(b ^ 1));
-            for (int r = b * (B / 2) + threadIdx.x; r < (b + 1) * (B / 2); r += T) {
-                const double x0 = ntt::to_fp(lift(__ldg(dig + r))), x1 = ntt::to_fp(lift(__ldg(dig + r + B)));
-                const double v = ntt::fmodmul(x1, w_cl, ar.q, ar.qinv);
-                const int sr = ntt::swz(r);
-                sdata[sr] = b == 0 ? x0 + v : x0 - v;
-                ks_st_cluster(peer + sr * 8, b == 0 ? x0 - v : x0 + v);
-            }
-            ks_cluster_sync();
-        }
         auto first = [&](int r, int uu, int k) -> V {
-            if constexpr (CL) {
-                (void)uu, (void)k;
-                return reinterpret_cast<const double*>(smem)[ntt::swz(r)];
-            } else
-            if constexpr (PREFETCH && C == 0) {
+            if constexpr (PREFETCH) {
                 (void)r;
                 return ntt::to_fp(lift(pf[uu * E0 + k]));
-            } else if constexpr (PREFETCH) {
-                (void)r;
-                const double x0 = ntt::to_fp(lift(pf[(uu * E0 + k) * 2])), x1 = ntt::to_fp(lift(pf[(uu * E0 + k) * 2 + 1]));
-                const double v = ntt::fmodmul(x1, w_col, ar.q, ar.qinv);
-                return b == 0 ? x0 + v : x0 - v;
             } else if constexpr (FP) {
+                (void)uu, (void)k;
                 return column_value_fp<LOGN, C, LIFT>(dig, R.fwd_f + (static_cast<long long>(i) << LOGN), q, ar.q, ar.qinv, r, b);
             } else {
+                (void)uu, (void)k;
                 return column_value<LOGN, C>(dig, itw, q, r, b);
             }
         };
         V stash[EL];
+        const unsigned par = bphase & 1;
         ntt::fwd_block<LOGB, LOGE, T>(reinterpret_cast<V*>(smem), ar, stw, 0, 0, first,
                                       [&](int idx, V v, int uu, int k) {
                                           stash[k] = v;
                                           if (k == EL - 1) {
                                               const int base = idx - (EL - 1);
-                                              if constexpr (FP) {
-#if defined(HECNN_KS_ABLATE_MAC)
-                                                  // ablation: NTT only (outputs summed, no key, no c1)
-#pragma unroll
-                                                  for (int kk = 0; kk < EL; ++kk) a0[uu * EL + kk] += stash[kk];
-#elif defined(HECNN_KS_ABLATE_SACC)
-                                                  // ablation: key MAC, c1 folded into the c0 registers
+                                              if constexpr (TM) {
+                                                  ks_mbar_wait(bbar, par);  // b_t landed
+                                                  key.template unit_tm<EL>(t, blk_off + base, stash, a0 + uu * EL,
+                                                                           sacc + base, tm_lane + uu * 2 * EL);
+                                              } else if constexpr (FP) {
                                                   key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
-                                                                        [&](int kk) -> double& { return a0[uu * EL + kk]; });
-#else
-                                                  if constexpr (TM2) {
-                                                      ks_mbar_wait(bbar, t & 1);  // b_t landed
-                                                      key.template unit_tm2<EL>(t, blk_off + base, stash, a0 + uu * EL, sacc + base,
-                                                                                tm_lane + uu * 2 * EL, c1col + uu * 2 * EL, t + 1 < D);
-                                                  } else if constexpr (TM) {
-                                                      ks_mbar_wait(bbar, t & 1);  // b_t landed
-                                                      key.template unit_tm<EL>(t, blk_off + base, stash, a0 + uu * EL,
-                                                                               sacc + base, tm_lane + uu * 2 * EL);
-                                                  } else {
-                                                      key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
-                                                                            [&](int kk) -> double& { return sacc[slot(base + kk, uu, kk)]; });
-                                                  }
-#endif
+                                                                        [&](int kk) -> double& { return sacc[slot(base + kk, uu, kk)]; });
                                               } else if constexpr (TMI) {
                                                   key.template unit_tm<EL>(t, blk_off + base, stash, a0 + uu * EL, tm_lane + uu * 2 * EL);
                                               } else {
@@ -507,9 +428,9 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
                                           // inputs land while this one is transformed
                                           if (t + 1 < D) prefetch(t + 1);
                                       });
+        if constexpr (TM) ++bphase;
         if constexpr (USE_TMEM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        if constexpr (CL) ks_cluster_sync();  // the peer writes this CTA's data buffer next
-        else __syncthreads();  // the next digit's first round overwrites shared memory
+        __syncthreads();  // the next digit's first round overwrites shared memory
         if constexpr (TM) {
             if (threadIdx.x == 0 && t + 1 < D)
                 ks_bulk_load(sacc, key.evk_f + (2LL * (t + 1)) * key.key_stride + key.ioff + blk_off, B * 8, bbar);
@@ -530,10 +451,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
     // each unit's EL words are contiguous: 16-byte loads and stores. With
     // whole units per thread, every unit's (x0, x1) words are loaded before
     // the first is used (their HBM latency overlaps instead of serialising)
-#ifndef HECNN_KS_EPI_PF
-#define HECNN_KS_EPI_PF 1
-#endif
-    constexpr bool EPF = HECNN_KS_EPI_PF && PRIV && T <= 512;  // 1024-thread blocks (64 registers) spill with it
+    constexpr bool EPF = PRIV && T <= 512;  // 1024-thread blocks (64 registers) spill with it
     ulonglong2 xpre[EPF ? PL * EL : 1];
     if constexpr (EPF) {
 #pragma unroll
@@ -551,11 +469,10 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
         const int u = threadIdx.x + uu * T;
         if (UL % T != 0 && u >= UL) break;
         const int base = ntt::fwd_last_base<LOGB, LOGE, T>(uu);
-        double c1u[EL], c0u[EL];
+        double c1u[EL];
         u64 c1i[EL];
         if constexpr (TMI) tmem_ld_u<EL>(tm_lane + uu * 2 * EL, c1i);
-        if constexpr (TM) tmem_ld_d<EL>(c1col + uu * 2 * EL, c1u);
-        if constexpr (TM2) tmem_ld_d<EL>(tm_lane + uu * 2 * EL, c0u);
+        if constexpr (TM) tmem_ld_d<EL>(tm_lane + uu * 2 * EL, c1u);
 #pragma unroll
         for (int k = 0; k < EL; k += 2) {
             const int idx = base + k;
@@ -563,8 +480,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if constexpr (FP) {
-                    if constexpr (TM2) r0[h] = ntt::fcanon(c0u[k + h], ar.q, ar.qinv);
-                    else r0[h] = ntt::fcanon(a0[uu * EL + k + h], ar.q, ar.qinv);
+                    r0[h] = ntt::fcanon(a0[uu * EL + k + h], ar.q, ar.qinv);
                     if constexpr (TM) r1[h] = ntt::fcanon(c1u[k + h], ar.q, ar.qinv);
                     else r1[h] = ntt::fcanon(sacc[slot(idx + h, uu, k + h)], ar.q, ar.qinv);
                 } else {
@@ -601,14 +517,7 @@ __device__ __forceinline__ void ks_body(const DevRing& R, const A& ar, const typ
             *reinterpret_cast<ulonglong2*>(o1 + idx) = make_ulonglong2(add_mod(b1[0], r1[0], q), add_mod(b1[1], r1[1], q));
         }
     }
-    if constexpr (USE_TMEM) {
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_lane), "n"(TCOLS));  // warp 0: the allocated base
-        }
-    }
+    if constexpr (!USE_TMEM && FP) __syncthreads();  // c1 slots are re-zeroed by the next item
 }
 
 // Unit-wise evk MACs: EL consecutive NTT outputs v[] at key positions
@@ -631,35 +540,6 @@ struct FpKey {
             s0[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], wb[k].y, q, qinv);
             s1(2 * k) += ntt::fmodmul(v[2 * k], wa[k].x, q, qinv);
             s1(2 * k + 1) += ntt::fmodmul(v[2 * k + 1], wa[k].y, q, qinv);
-        }
-    }
-    // TM2: b_t from the shared-memory stage, a_t from registers (reloaded
-    // with a_{t+1} for the next digit), c0 and c1 in tensor memory
-    template <int EL>
-    __device__ __forceinline__ void unit_tm2(int t, long long pos, const double* v, double* a, const double* bst,
-                                             uint32_t c0col, uint32_t c1col, bool more) const {
-        double c0[EL], c1[EL];
-        tmem_ld_d<EL>(c0col, c0);
-        tmem_ld_d<EL>(c1col, c1);
-        const double2* kb = reinterpret_cast<const double2*>(bst);
-#pragma unroll
-        for (int k = 0; k < EL / 2; ++k) {
-            const double2 wb = kb[k];
-            c0[2 * k] += ntt::fmodmul(v[2 * k], wb.x, q, qinv);
-            c0[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], wb.y, q, qinv);
-            c1[2 * k] += ntt::fmodmul(v[2 * k], a[2 * k], q, qinv);
-            c1[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], a[2 * k + 1], q, qinv);
-        }
-        tmem_st_d<EL>(c0col, c0);
-        tmem_st_d<EL>(c1col, c1);
-        if (more) {  // this unit's a_{t+1}, in flight until the next digit's last round
-            const double2* ka = reinterpret_cast<const double2*>(evk_f + (2LL * t + 3) * key_stride + ioff + pos);
-#pragma unroll
-            for (int k = 0; k < EL / 2; ++k) {
-                const double2 w2 = __ldg(ka + k);
-                a[2 * k] = w2.x;
-                a[2 * k + 1] = w2.y;
-            }
         }
     }
     // b_t from the shared-memory stage, a_t from L2, c1 read-modify-written in
@@ -725,40 +605,85 @@ struct IntKey {
     }
 };
 
-// blockIdx.x = (ct * nsel + i - limb0) * nblocks + b over limbs [limb0, limb0 + nsel). FPK: this instantiation serves
-// the FP64 limbs (q < 2^42) and skips the others, or the reverse, so each
-// path gets its own register allocation; the host launches both.
+// Persistent: CTA c takes items c, c + gridDim.x, ... of
+// item = (ct * nsel + i - limb0) * nblocks + b over limbs [limb0, limb0 + nsel)
+// (ciphertext-major, so the CTAs running at once share the ciphertexts'
+// digits in L2). FPK: this instantiation serves the FP64 limbs (q < 2^42) and
+// skips the others, or the reverse, so each path gets its own register
+// allocation; the host launches both.
 template <int LOGN, int LOGB, int LOGE, int T, int MINB, bool FPK, bool LIFT>
 __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
                                                  const u64* __restrict__ evk_sh, const double* __restrict__ evk_f,
                                                  u64* __restrict__ acc01, int level, int D, int limb0, int nsel,
-                                                 int mode, const u64* __restrict__ fy) {
-    constexpr int C = LOGN - LOGB;
-    const long long cta = blockIdx.x;
-    const int b = static_cast<int>(cta & ((1 << C) - 1));
-    const long long row = cta >> C;  // ct * nsel + (i - limb0)
-    const long long ct = row / nsel;
-    const int i = limb0 + static_cast<int>(row % nsel);
-    const u64 q = R.mod[i].q;
+                                                 long long items, int mode, const u64* __restrict__ fy) {
+    constexpr int C = LOGN - LOGB, B = 1 << LOGB;
+    using S = KsShape<LOGN, LOGB, LOGE, T, FPK>;
+    extern __shared__ u64 smem[];
+    uint64_t* bbar = reinterpret_cast<uint64_t*>(smem + 3 * B);
+    uint64_t* tbar = bbar + 1;
+    uint32_t tm_lane = 0;
+    __shared__ uint32_t tm_slot;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(bbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(tbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if constexpr (S::USE_TMEM) {
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ks_saddr(&tm_slot)),
+                         "n"(S::TCOLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+    __syncthreads();
+    if constexpr (S::USE_TMEM) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int w = threadIdx.x >> 5;
+        tm_lane = tm_slot + (static_cast<uint32_t>((w & 3) * 32) << 16) + static_cast<uint32_t>((w >> 2) * S::TCW);
+    }
     const long long n = 1LL << LOGN;
     const long long key_stride = static_cast<long long>(R.limbs) * n;  // one evk polynomial
-    const long long ioff = static_cast<long long>(i) * n;
-    if (ntt::fp_limb(q) != FPK) return;
-    if constexpr (FPK) {
-        const ntt::FpArith ar{static_cast<double>(q), R.inv_q[i]};
-        const FpKey key{evk_f, key_stride, ioff, ar.q, ar.qinv};
-        ks_body<LOGN, LOGB, LOGE, T, LIFT>(R, ar, R.fwd_f + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
-    } else {
-        // primes >= 2^42 only: digits < 2^20 < q are residues already
-        const ntt::IntArith ar{q, q << 1};
-        const IntKey key{evk, evk_sh, key_stride, ioff, q, q << 1};
-        ks_body<LOGN, LOGB, LOGE, T, false>(R, ar, R.fwd + ioff, digits, key, acc01, level, D, ct, i, b, q, mode, fy);
+    unsigned bphase = 0, tphase = 0;
+    int tw_key = -1;  // (limb, block) whose twiddle table is in shared memory
+    for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+        const int b = static_cast<int>(item & ((1 << C) - 1));
+        const long long row = item >> C;  // ct * nsel + (i - limb0)
+        const long long ct = row / nsel;
+        const int i = limb0 + static_cast<int>(row % nsel);
+        const u64 q = R.mod[i].q;
+        if (ntt::fp_limb(q) != FPK) continue;
+        const long long ioff = static_cast<long long>(i) * n;
+        const int key_now = (i << C) + b;
+        const bool load_tw = key_now != tw_key;
+        tw_key = key_now;
+        if constexpr (FPK) {
+            const ntt::FpArith ar{static_cast<double>(q), R.inv_q[i]};
+            const FpKey key{evk_f, key_stride, ioff, ar.q, ar.qinv};
+            ks_item<LOGN, LOGB, LOGE, T, LIFT>(R, ar, R.ks_tw_f + ioff + (static_cast<long long>(b) << LOGB), load_tw,
+                                               digits, key, acc01, level, D, ct, i, b, q, mode, fy, tm_lane, bphase,
+                                               tphase);
+        } else {
+            // primes >= 2^42 only: digits < 2^20 < q are residues already
+            const ntt::IntArith ar{q, q << 1};
+            const IntKey key{evk, evk_sh, key_stride, ioff, q, q << 1};
+            ks_item<LOGN, LOGB, LOGE, T, false>(R, ar, R.ks_tw + ioff + (static_cast<long long>(b) << LOGB), load_tw,
+                                                digits, key, acc01, level, D, ct, i, b, q, mode, fy, tm_lane, bphase,
+                                                tphase);
+        }
+    }
+    if constexpr (S::USE_TMEM) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_slot), "n"(S::TCOLS));
+        }
     }
 }
 
-#ifndef HECNN_KS_LOGB
-#define HECNN_KS_LOGB 13
-#endif
+// block size: the block twiddle tables (DevRing::ks_tw) are built for 2^13
+constexpr int HECNN_KS_LOGB = 13;
 #ifndef HECNN_KS_LOGE
 #define HECNN_KS_LOGE 3
 #endif
@@ -799,7 +724,7 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
     auto kint = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false, false>;
     // data + staged twiddles (u64 Shoup pairs on the integer path; double
     // twiddles + c1 accumulators on the FP64 path)
-    const int smem = P::B * (8 + 16) + 64;  // + the b_t stage's mbarrier
+    const int smem = P::B * (8 + 16) + 64;  // + the b_t stage's and twiddle table's mbarriers
     static bool init = (smem > 48 * 1024
                             ? (cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, true>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
@@ -821,43 +746,50 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
     // per (ct, limb, digit): one N-point NTT + 2N MACs; bytes: evk once + digits + acc r/w
     L.begin("k_keyswitch", cl * D * (n / 2 * LOGN + 2 * n),
             2.0 * D * limbs * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
-    auto launch = [&](auto kern, cudaStream_t st, int l0, int nsel) {
-        const std::size_t ctas = count * static_cast<std::size_t>(nsel) << (LOGN - P::LOGB);
-        if (HECNN_KS_CLUSTER && LOGN - P::LOGB == 1 && (kern == kfp)) {
-            // the two block CTAs of each limb polynomial as a cluster (shared column stage)
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(static_cast<unsigned>(ctas));
-            cfg.blockDim = dim3(P::T);
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = st;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = 2;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            cuda_check(cudaLaunchKernelEx(&cfg, kern, R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel, mode, fy),
-                       "cudaLaunchKernelEx (key-switch cluster)");
-            return;
-        }
-        kern<<<static_cast<unsigned>(ctas), P::T, smem, st>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel, mode, fy);
+    // Persistent grids: the capacity (resident CTAs per SM x SMs) is split
+    // between the FP64-limb and integer-limb kernels in proportion to their
+    // work (an integer-limb item costs HECNN_KS_INT_COST FP64 items), so both
+    // finish together when they run side by side.
+    static int sms = 0, occ_fp = 0, occ_int = 0;
+    if (!sms) {
+        int dev = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fp, kfp, P::T, smem), "occupancy");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_int, kint, P::T, smem), "occupancy");
+        occ_fp = std::max(occ_fp, 1);
+        occ_int = std::max(occ_int, 1);
+    }
+#ifndef HECNN_KS_INT_COST
+#define HECNN_KS_INT_COST 2.75
+#endif
+    const long long nb = 1LL << (LOGN - P::LOGB);
+    const long long items_fp = static_cast<long long>(count) * nfp * nb, items_int = static_cast<long long>(count) * nint * nb;
+    const int n_int_limbs = __builtin_popcountll(int_mask);
+    const double w_fp = double(count) * (limbs - n_int_limbs) * nb, w_int = double(count) * n_int_limbs * nb * HECNN_KS_INT_COST;
+    auto launch = [&](auto kern, cudaStream_t st, int l0, int nsel, long long items, long long grid) {
+        grid = std::max(1LL, std::min(grid, items));
+        kern<<<static_cast<unsigned>(grid), P::T, smem, st>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel, items,
+                                                             mode, fy);
     };
     // The integer-limb kernel (IMAD pipes) runs on the side stream beside the
-    // FP64 kernel, filling the SMs the FP64 kernel's last wave leaves idle.
+    // FP64 kernel on its share of the SMs.
     const bool split = nfp && nint && L.aux;
     unsigned long long launched = 0;
     if (split) {
+        const long long cap = static_cast<long long>(sms) * std::min(occ_fp, occ_int);
+        long long g_int = std::llround(double(cap) * w_int / (w_int + w_fp));
+        g_int = std::min(std::max(g_int, 1LL), cap - 1);
         cuda_check(cudaEventRecord(L.fork_ev, L.stream), "cudaEventRecord");
         cuda_check(cudaStreamWaitEvent(L.aux, L.fork_ev, 0), "cudaStreamWaitEvent");
-        launch(kint, L.aux, int0, nint);
-        launch(kfp, L.stream, fp0, nfp);
+        launch(kint, L.aux, int0, nint, items_int, g_int);
+        launch(kfp, L.stream, fp0, nfp, items_fp, cap - g_int);
         cuda_check(cudaEventRecord(L.join_ev, L.aux), "cudaEventRecord");
         cuda_check(cudaStreamWaitEvent(L.stream, L.join_ev, 0), "cudaStreamWaitEvent");
         launched = 2;
     } else {
-        if (nfp) launch(kfp, L.stream, fp0, nfp), ++launched;
-        if (nint) launch(kint, L.stream, int0, nint), ++launched;
+        if (nfp) launch(kfp, L.stream, fp0, nfp, items_fp, static_cast<long long>(sms) * occ_fp), ++launched;
+        if (nint) launch(kint, L.stream, int0, nint, items_int, static_cast<long long>(sms) * occ_int), ++launched;
     }
     L.count(launched);
 }
