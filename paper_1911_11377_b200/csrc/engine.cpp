@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <future>
 #include <stdexcept>
 #include <thread>
 #include <tuple>
@@ -185,6 +186,26 @@ void Arena::release(void* ptr) {
         }
     }
     free_.emplace(p, blk);
+}
+
+void Arena::shrink(void* ptr, std::size_t bytes) {
+    bytes = (bytes + 255) & ~std::size_t(255);
+    auto it = used_.find(static_cast<char*>(ptr));
+    if (it == used_.end() || it->second.size <= bytes) return;
+    const std::size_t rest = it->second.size - bytes;
+    const int seg = it->second.seg;
+    it->second.size = bytes;
+    char* tail = static_cast<char*>(ptr) + bytes;
+    used_.emplace(tail, Block{rest, seg});
+    release(tail);  // coalesces with a free neighbour
+}
+
+DevBuf DevBuf::adopt(Context* ctx, void* ptr, std::size_t bytes) {
+    DevBuf b;
+    b.ctx_ = ctx;
+    b.ptr_ = ptr;
+    b.bytes_ = bytes;
+    return b;
 }
 
 DevBuf::DevBuf(Context* ctx, std::size_t bytes) : ctx_(ctx), bytes_(bytes) {
@@ -856,6 +877,7 @@ void encrypt_into(Context& C, std::size_t count, const u64* seeds, const std::ve
         C.upload(dr.get(), hr.data(), m * n);
         C.upload(de0.get(), he0.data(), m * n);
         C.upload(de1.get(), he1.data(), m * n);
+        // (encrypt_sampled below is the same device sequence for pre-sampled noise)
         const u64* mres = nullptr;
         if (msgs) {
             bool all_small = true;
@@ -885,6 +907,68 @@ void encrypt_into(Context& C, std::size_t count, const u64* seeds, const std::ve
         ntt_inverse(C.dev, o, static_cast<int>(level), 2 * m, L);
         add_noise_msg(C.dev, o, de0.as<signed char>(), de1.as<signed char>(), mres, static_cast<int>(level), m, L);
     }
+}
+
+void encrypt_sampled(Context& C, std::size_t count, const signed char* r, const signed char* e0, const signed char* e1,
+                     std::uint32_t level, u64* out) {
+    if (!C.has_pk) throw std::invalid_argument("encrypt: no public key loaded");
+    const std::size_t n = C.n(), limbs = level + 1, cw = 2 * limbs * n;
+    const std::size_t chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, 1024));
+    Launch L = C.L();
+    DevBuf dr(&C, chunk * n), de0(&C, chunk * n), de1(&C, chunk * n), rr(&C, chunk * limbs * n * 8);
+    for (std::size_t c0 = 0; c0 < count; c0 += chunk) {
+        const std::size_t m = std::min(chunk, count - c0);
+        C.upload(dr.get(), r + c0 * n, m * n);
+        C.upload(de0.get(), e0 + c0 * n, m * n);
+        C.upload(de1.get(), e1 + c0 * n, m * n);
+        small_to_rns(C.dev, dr.as<signed char>(), rr.as<u64>(), static_cast<int>(level), m, L);
+        ntt_forward(C.dev, rr.as<u64>(), static_cast<int>(level), m, L);
+        u64* o = out + c0 * cw;
+        mul_by_key(C.dev, rr.as<u64>(), C.pk.as<u64>(), C.top() + 1, o, static_cast<int>(level), m, L);
+        ntt_inverse(C.dev, o, static_cast<int>(level), 2 * m, L);
+        add_noise_msg(C.dev, o, de0.as<signed char>(), de1.as<signed char>(), nullptr, static_cast<int>(level), m, L);
+    }
+}
+
+PadNoiseMap start_pad_noise(Context& C, const Model& M, u64 seed) {
+    PadNoiseMap out;
+    if (!C.has_pk) return out;  // the pad layer raises the reference's error
+    Shape in = M.input;
+    for (std::size_t i = 0; i < M.layers.size() && i < M.shapes.size(); ++i) {
+        const Layer& l = M.layers[i];
+        const Shape os = M.shapes[i];
+        if (l.kind == 2 && !in.flat && l.pad) {
+            const u64 layer_seed = derive_seed(seed, 0x1a7e + i);
+            const std::size_t pad = l.pad;
+            const Shape is = in;
+            out.emplace(i, std::async(std::launch::async, [&C, os, is, pad, layer_seed]() {
+                                auto P = std::make_shared<PadNoise>();
+                                const std::size_t cells = os.positions(), n = C.n();
+                                P->border.assign(cells, -1);
+                                std::vector<u64> seeds;
+                                for (std::size_t p = 0; p < cells; ++p) {
+                                    const std::size_t xy = p / os.c, y = xy / os.w, xx = xy % os.w;
+                                    const bool inside = y >= pad && y < pad + is.h && xx >= pad && xx < pad + is.w;
+                                    if (!inside) {
+                                        P->border[p] = static_cast<int>(seeds.size());
+                                        seeds.push_back(derive_seed(layer_seed, 0xbad0 + p));
+                                    }
+                                }
+                                P->r.resize(seeds.size() * n);
+                                P->e0.resize(seeds.size() * n);
+                                P->e1.resize(seeds.size() * n);
+                                parallel_items(seeds.size(), [&](std::size_t k) {
+                                    const u64 s = seeds[k];
+                                    to_int8(sample_secretish(C, 0.5, derive_seed(s, 0x0a01)), &P->r[k * n]);
+                                    to_int8(sample_error(C, derive_seed(s, 0x0a02)), &P->e0[k * n]);
+                                    to_int8(sample_error(C, derive_seed(s, 0x0a03)), &P->e1[k * n]);
+                                });
+                                return std::shared_ptr<const PadNoise>(P);
+                            }).share());
+        }
+        in = os;
+    }
+    return out;
 }
 
 }  // namespace detail
@@ -1450,7 +1534,8 @@ TensorPtr pool_layer(Context& C, Model& M, std::size_t li, const Tensor& x, cons
 
 // zero_pad2d_encrypted (layers.hpp:241-267): inner cells copied, border cells
 // are fresh encryptions of zero (host randomness, device arithmetic).
-TensorPtr pad_layer(Context& C, Model& M, std::size_t li, const Tensor& x, const Shape& out_shape, u64 layer_seed) {
+TensorPtr pad_layer(Context& C, Model& M, std::size_t li, const Tensor& x, const Shape& out_shape, u64 layer_seed,
+                    const detail::PadNoiseMap& pads) {
     const Layer& l = M.layers[li];
     const std::size_t cells = out_shape.positions();
     std::vector<int> idx_in(cells, -1), idx_border(cells, -1);
@@ -1475,7 +1560,13 @@ TensorPtr pad_layer(Context& C, Model& M, std::size_t li, const Tensor& x, const
     gather_cells(x.data(), din.as<int>(), out->data(), x.cell_words(), cells, L);
     if (!seeds.empty()) {
         DevBuf fresh(&C, seeds.size() * x.cell_words() * 8);
-        encrypt_into(C, seeds.size(), seeds.data(), nullptr, x.level, fresh.as<u64>());
+        auto it = pads.find(li);
+        if (it != pads.end()) {  // sampled on host threads while earlier layers ran
+            const detail::PadNoise& P = *it->second.get();
+            detail::encrypt_sampled(C, seeds.size(), P.r.data(), P.e0.data(), P.e1.data(), x.level, fresh.as<u64>());
+        } else {
+            encrypt_into(C, seeds.size(), seeds.data(), nullptr, x.level, fresh.as<u64>());
+        }
         DevBuf db = C.upload_vec(idx_border);
         gather_cells(fresh.as<u64>(), db.as<int>(), out->data(), x.cell_words(), cells, L);
     }
@@ -1509,11 +1600,13 @@ TensorPtr forward_encrypted(Context& C, Model& M, const Tensor& x, u64 seed, dou
     TensorPtr cur;
     auto current = [&]() -> const Tensor& { return cur ? *cur : x; };
     std::vector<double> stream_ms(M.layers.size(), 0.0);
+    const detail::PadNoiseMap pads = detail::start_pad_noise(C, M, seed);
     std::vector<bool> streamed(M.layers.size(), false);
     for (std::size_t i = 0; i < M.layers.size(); ++i) {
         // layers whose tensors do not fit in device memory run row-streamed (stream.cpp)
         std::size_t end = i;
-        TensorPtr seg = detail::forward_streamed(C, M, current(), i, end, seed, layer_seconds ? &stream_ms : nullptr);
+        TensorPtr seg =
+            detail::forward_streamed(C, M, current(), i, end, seed, layer_seconds ? &stream_ms : nullptr, pads);
         if (seg) {
             cur = std::move(seg);
             for (std::size_t j = i; j < end; ++j) {
@@ -1540,7 +1633,7 @@ TensorPtr forward_encrypted(Context& C, Model& M, const Tensor& x, u64 seed, dou
             case 0:
             case 3: next = linear_layer(C, M, i, current(), M.shapes[i]); break;
             case 1: next = pool_layer(C, M, i, current(), M.shapes[i]); break;
-            case 2: next = pad_layer(C, M, i, current(), M.shapes[i], layer_seed); break;
+            case 2: next = pad_layer(C, M, i, current(), M.shapes[i], layer_seed, pads); break;
             case 4:
                 next = eval_activation(C, M.acts[static_cast<std::size_t>(l.act)], current());
                 break;

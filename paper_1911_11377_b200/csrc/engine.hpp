@@ -33,6 +33,8 @@ public:
     void release(void* p);
     // Return segments that are entirely free to the driver; returns bytes freed.
     std::size_t trim();
+    // Keep the first `bytes` of the used block at p, free the rest.
+    void shrink(void* p, std::size_t bytes);
     std::size_t reserved() const { return reserved_; }
     std::size_t free_bytes() const {
         std::size_t b = 0;
@@ -63,6 +65,16 @@ public:
     void reset();
     // Non-owning view of memory owned elsewhere (e.g. a slice of a tensor).
     static DevBuf alias(void* ptr, std::size_t bytes);
+    // Take ownership of an arena block allocated by the caller (released on reset).
+    static DevBuf adopt(Context* ctx, void* ptr, std::size_t bytes);
+    // Give up ownership without releasing (the caller keeps the block).
+    void* release_ownership() {
+        void* p = ptr_;
+        ptr_ = nullptr;
+        bytes_ = 0;
+        ctx_ = nullptr;
+        return p;
+    }
     template <class T>
     T* as() const { return static_cast<T*>(ptr_); }
     void* get() const { return ptr_; }

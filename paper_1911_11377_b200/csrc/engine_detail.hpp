@@ -2,6 +2,9 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <future>
+#include <map>
+#include <memory>
 #include <vector>
 
 #include "engine.hpp"
@@ -16,6 +19,22 @@ constexpr std::size_t kScratchBytes = std::size_t(3) << 30;
 // (ckks.hpp:238-266); out: [count][2][level+1][n] device words.
 void encrypt_into(Context& C, std::size_t count, const u64* seeds, const std::vector<EncodedCoeffs>* msgs,
                   std::uint32_t level, u64* out);
+
+// Device part of encrypt_into with host-sampled randomness: r, e0, e1 are
+// [count][n] int8 (ternary / clamped gaussian), messages zero.
+void encrypt_sampled(Context& C, std::size_t count, const signed char* r, const signed char* e0, const signed char* e1,
+                     std::uint32_t level, u64* out);
+
+// zero_pad2d border randomness (layers.hpp:255-262), sampled on host threads
+// while the device runs the layers before the pad: make_encryption_randomness
+// (derive_seed(layer_seed, 0xbad0 + p)) for every border position p.
+struct PadNoise {
+    std::vector<int> border;             // position -> border index (-1: inside)
+    std::vector<signed char> r, e0, e1;  // [borders][n]
+};
+using PadNoiseFuture = std::shared_future<std::shared_ptr<const PadNoise>>;
+using PadNoiseMap = std::map<std::size_t, PadNoiseFuture>;  // by pad layer
+PadNoiseMap start_pad_noise(Context& C, const Model& M, u64 seed);
 
 // Conv / dense weight caches of layer li at `level` (rows = taps x in_c, or in_f).
 Model::LinearCache& linear_weights(Context& C, Model& M, std::size_t li, std::uint32_t level, std::size_t rows);
@@ -37,6 +56,6 @@ void linear_apply(Context& C, Model::LinearCache& lc, const Model::Taps& taps, c
 // `end` is filled with the first layer not covered.
 // layer_ms (optional, one entry per layer): device milliseconds are added per layer.
 TensorPtr forward_streamed(Context& C, Model& M, const Tensor& x, std::size_t first, std::size_t& end, u64 seed,
-                           std::vector<double>* layer_ms);
+                           std::vector<double>* layer_ms, const PadNoiseMap& pads);
 
 }  // namespace hecnn_b200::detail

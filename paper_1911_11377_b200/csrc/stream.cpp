@@ -231,7 +231,7 @@ std::size_t avail_bytes(Context& C) {
 }  // namespace
 
 TensorPtr forward_streamed(Context& C, Model& M, const Tensor& x, std::size_t first, std::size_t& end, u64 seed,
-                           std::vector<double>* layer_ms) {
+                           std::vector<double>* layer_ms, const PadNoiseMap& pads) {
     end = first;
     if (M.stream_mode == 2 || x.shape.flat || first >= M.layers.size()) return nullptr;
     std::vector<Stage> st = parse_stages(M, x, first);
@@ -279,9 +279,8 @@ TensorPtr forward_streamed(Context& C, Model& M, const Tensor& x, std::size_t fi
     };
     const bool fits_whole = full_peak(first, x.shape, x.level) + margin <= avail;
     if (M.stream_mode == 0 && fits_whole) return nullptr;
-    // streaming: hand wholly free arena segments back so the stores below get
-    // contiguous memory (only here -- cudaFree synchronises the device)
-    if (!M.mem_budget) C.arena.trim();
+    // (the stores come from the arena's free blocks; when a store does not fit
+    // one, Arena::alloc hands wholly free segments back and retries)
 
     // rings: store s (s >= 1) keeps the window of rows stage s reads
     const std::size_t S = st.size();
@@ -422,20 +421,33 @@ TensorPtr forward_streamed(Context& C, Model& M, const Tensor& x, std::size_t fi
     st = P.stages;
 
     // ---- stores
-    std::vector<DevBuf> ring(k + 1);
+    // One arena block [segment output | rings]: a single contiguous request
+    // (fragmented free space cannot strand a ring), and after the segment the
+    // ring part is handed back while the output stays.
     std::vector<u64*> base(k + 1);
     std::vector<StoreDims> dims(k + 1);
     base[0] = x.data();
     for (std::size_t s = 0; s <= k; ++s) dims[s] = store_dims(st, s, x);
-    for (std::size_t s = 1; s < k; ++s) {
-        ring[s] = DevBuf(&C, P.ring[s] * dims[s].w * dims[s].c * cell_bytes(C, dims[s].level));
-        base[s] = ring[s].as<u64>();
-    }
     const Stage& lastst = st[k - 1];
-    TensorPtr out = make_tensor(C, lastst.oh * lastst.ow * lastst.oc, lastst.out_level, lastst.out_scale);
+    const std::size_t out_cells = lastst.oh * lastst.ow * lastst.oc;
+    const std::size_t out_bytes = (out_cells * cell_bytes(C, lastst.out_level) + 255) & ~std::size_t(255);
+    std::vector<std::size_t> ring_off(k + 1, 0);
+    std::size_t total = out_bytes;
+    for (std::size_t s = 1; s < k; ++s) {
+        ring_off[s] = total;
+        total += (P.ring[s] * dims[s].w * dims[s].c * cell_bytes(C, dims[s].level) + 255) & ~std::size_t(255);
+    }
+    DevBuf block(&C, total);
+    char* blk = block.as<char>();
+    for (std::size_t s = 1; s < k; ++s) base[s] = reinterpret_cast<u64*>(blk + ring_off[s]);
+    TensorPtr out = std::make_unique<Tensor>();
+    out->ctx = &C;
+    out->cells = out_cells;
+    out->level = lastst.out_level;
+    out->scale = lastst.out_scale;
     out->shape = M.shapes[lastst.last];
     out->batch = x.batch;
-    base[k] = out->data();
+    base[k] = reinterpret_cast<u64*>(blk);
 
     // columns of store s any consumer reads (border encryptions elsewhere are skipped)
     std::vector<std::size_t> used_w(k + 1, 0);
@@ -488,13 +500,19 @@ TensorPtr forward_streamed(Context& C, Model& M, const Tensor& x, std::size_t fi
             C.enc->check_encode(1, 0.0, st[s - 1].out_scale, C.top());
             checked[s] = true;
         }
-        const u64 layer_seed = derive_seed(seed, 0x1a7e + static_cast<u64>(g.pad));
-        std::vector<u64> seeds;
-        seeds.reserve((c1 - c0) * d.c);
-        for (std::size_t col = c0; col < c1; ++col)
-            for (std::size_t c = 0; c < d.c; ++c) seeds.push_back(derive_seed(layer_seed, 0xbad0 + (q * d.w + col) * d.c + c));
         u64* dst = base[s] + ((q % P.ring[s]) * d.w + c0) * d.c * words(d.level);
-        timed(g.pad, [&] { encrypt_into(C, seeds.size(), seeds.data(), nullptr, d.level, dst); });
+        const std::size_t p0 = (q * d.w + c0) * d.c, cnt = (c1 - c0) * d.c;
+        auto it = pads.find(static_cast<std::size_t>(g.pad));
+        if (it != pads.end()) {  // sampled on host threads while earlier rows ran: positions
+            const PadNoise& N = *it->second.get();  // p0.. are consecutive border cells
+            const std::size_t k0 = static_cast<std::size_t>(N.border[p0]), nn = C.n();
+            timed(g.pad, [&] { encrypt_sampled(C, cnt, &N.r[k0 * nn], &N.e0[k0 * nn], &N.e1[k0 * nn], d.level, dst); });
+        } else {
+            const u64 layer_seed = derive_seed(seed, 0x1a7e + static_cast<u64>(g.pad));
+            std::vector<u64> seeds(cnt);
+            for (std::size_t k = 0; k < cnt; ++k) seeds[k] = derive_seed(layer_seed, 0xbad0 + p0 + k);
+            timed(g.pad, [&] { encrypt_into(C, seeds.size(), seeds.data(), nullptr, d.level, dst); });
+        }
     };
 
     // a tensor view over device cells (no ownership)
@@ -605,8 +623,10 @@ TensorPtr forward_streamed(Context& C, Model& M, const Tensor& x, std::size_t fi
         std::fprintf(stderr, "[hecnn] stream layers [%zu, %zu): %zu stages, transient %.1f GiB\n", first, end, k,
                      P.transient / double(GiB));
     for (std::size_t y = 0; y < st[k - 1].oh; ++y) compute_row(k - 1, y);
-    if (out->level != lastst.out_level || out->scale != lastst.out_scale)
-        throw std::logic_error("forward_encrypted: streamed ledger mismatch");
+    // rings done (later work on the stream is ordered after their last use):
+    // keep the output part of the block
+    C.arena.shrink(block.get(), out_bytes);
+    out->buf = DevBuf::adopt(&C, block.release_ownership(), out_bytes);
     if (layer_ms) {
         C.sync();
         for (const Mark& m : marks) {
