@@ -110,7 +110,13 @@ __global__ void __launch_bounds__(128) k_crt_digits(DevRing R, const u64* __rest
             }
         }
     }
-    u32* out = digits + ct * D * R.n + j;
+    // digit layout for the key switch: [ct][D][B][E] with E = N / B column
+    // partners (positions r + k B, k < E) adjacent, B = 2^min(logn, 13), so the
+    // column stage of a block loads one vector per element (plain [D][N] when
+    // N <= 2^13)
+    const int lb = R.logn < 13 ? R.logn : 13, le = R.logn - lb;
+    const int jj = ((j & ((1 << lb) - 1)) << le) | (j >> lb);
+    u32* out = digits + ct * D * R.n + jj;
     // every digit position is a compile-time (word, shift) pair, so acc[]
     // stays in registers (a runtime word index sends it to local memory)
     constexpr int DMAX = (64 * W + 19) / 20;
@@ -194,17 +200,40 @@ __device__ __forceinline__ void tmem_st_d(uint32_t addr, const double (&v)[EL]) 
 
 // Value at block-local position r after the C column stages (block b): only
 // the butterflies on the path to output b are evaluated (2^C - 1 products).
+// E column partners of block position r, adjacent in the digit layout
+// (k_crt_digits): one 4 / 8 / 16-byte load
+template <int E>
+__device__ __forceinline__ void load_partners(const u32* __restrict__ dig, int r, u32 (&v)[E]) {
+    if constexpr (E == 1) {
+        v[0] = __ldg(dig + r);
+    } else if constexpr (E == 2) {
+        const uint2 w = __ldg(reinterpret_cast<const uint2*>(dig) + r);
+        v[0] = w.x, v[1] = w.y;
+    } else if constexpr (E == 4) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(dig) + r);
+        v[0] = w.x, v[1] = w.y, v[2] = w.z, v[3] = w.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < E; k += 4) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(dig + r * E + k));
+            v[k] = w.x, v[k + 1] = w.y, v[k + 2] = w.z, v[k + 3] = w.w;
+        }
+    }
+}
+
 template <int LOGN, int C>
 __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const ulonglong2* __restrict__ tw, u64 q, int r,
                                             int b) {
     if constexpr (C == 0) {
         return lift_digit(dig[r], q);
     } else {
-        constexpr int E = 1 << C, B = 1 << (LOGN - C);
+        constexpr int E = 1 << C;
         const u64 two_q = q << 1;
         u64 x[E];
+        u32 raw[E];
+        load_partners<E>(dig, r, raw);
 #pragma unroll
-        for (int k = 0; k < E; ++k) x[k] = lift_digit(dig[r + k * B], q);
+        for (int k = 0; k < E; ++k) x[k] = lift_digit(raw[k], q);
 #pragma unroll
         for (int rho = 0; rho < C; ++rho) {
             const int half = E >> (rho + 1);
@@ -229,10 +258,12 @@ __device__ __forceinline__ u64 column_value(const u32* __restrict__ dig, const u
 template <int LOGN, int C, bool LIFT>
 __device__ __forceinline__ double column_value_fp(const u32* __restrict__ dig, const double* __restrict__ tw, u64 q,
                                                   double qd, double qinv, int r, int b) {
-    constexpr int E = 1 << C, B = 1 << (LOGN - C);
+    constexpr int E = 1 << C;
     double x[E];
+    u32 raw[E];
+    load_partners<E>(dig, r, raw);
 #pragma unroll
-    for (int k = 0; k < E; ++k) x[k] = ntt::to_fp(LIFT ? lift_digit(dig[r + k * B], q) : dig[r + k * B]);
+    for (int k = 0; k < E; ++k) x[k] = ntt::to_fp(LIFT ? lift_digit(raw[k], q) : raw[k]);
 #pragma unroll
     for (int rho = 0; rho < C; ++rho) {
         const int half = E >> (rho + 1);
