@@ -152,7 +152,61 @@ def crop_extrapolation_check(hb, eng, full_ms, crop=16):
             "ratio": est * 1e3 / full_ms}
 
 
-def c5_measured(hb, device, stream=None, image=32, check=8):
+def layer_levels(hb, spec, top):
+    """Input level of every layer (depth_cost ledger, model.hpp:169-182)."""
+    out, lv = [], top
+    for l in spec.layers:
+        out.append(lv)
+        if l.kind in (hb.CONV2D, hb.AVG_POOL2D, hb.DENSE):
+            lv -= 1
+        elif l.kind == hb.ACTIVATION:
+            lv -= 2  # degree-2 surrogates: ceil(log2 2) + 1
+    return out
+
+
+def reference_per_op_estimate(hb, spec, p, threads, r=None, cache=None):
+    """The reference's own forward_encrypted time for one set of `spec`,
+    estimated per op (C5 cannot run on the CPU): each layer's op
+    count x the reference's measured per-op throughput at that layer's level
+    on all host threads through its parallel_for (oracle/_ref
+    ref_time_layer_op): conv / dense = outputs x (zero + bias + rescale) +
+    scalar MACs (layer_work); activation = cells x eval_encrypted;
+    avg_pool = outputs x (4 MAC-equivalents + rescale); zero_pad = border cells
+    x encrypt + mod_switch."""
+    from oracle import ref
+    if r is None:
+        r = ref.RefEngine.from_params(p).keygen(1)
+    levels, shapes, work = layer_levels(hb, spec, len(p.primes) - 1), spec.shapes(), layer_work(hb, spec)
+    cache = {} if cache is None else cache
+
+    def rate(op, lv, inner):
+        key = (op, lv, inner)
+        if key not in cache:
+            count = threads if op == 0 else 2 * threads
+            # twice: the first pass pays the allocator's first-touch page faults
+            t = min(r.time_layer_op(op, lv, count, inner, threads) for _ in range(2))
+            cache[key] = count / t  # items per second
+        return cache[key]
+
+    per_layer, t_ops = [], time.perf_counter()
+    for l, lv, shp, w in zip(spec.layers, levels, shapes, work):
+        if l.kind in (hb.CONV2D, hb.DENSE):
+            outs = shp.positions()
+            base, full = 1.0 / rate(1, lv, 0), 1.0 / rate(1, lv, 64)
+            per_layer.append(outs * base + w * (full - base) / 64)
+        elif l.kind == hb.ACTIVATION:
+            per_layer.append(shp.positions() / rate(0, lv, 0))
+        elif l.kind == hb.AVG_POOL2D:
+            per_layer.append(shp.positions() / rate(1, lv, 4))
+        elif l.kind == hb.ZERO_PAD2D:
+            per_layer.append(w / rate(2, lv, 0) if w else 0.0)
+        else:
+            per_layer.append(0.0)
+    return {"seconds_per_set": float(sum(per_layer)), "layer_s": [round(v, 3) for v in per_layer],
+            "threads": threads, "probe_wall_s": time.perf_counter() - t_ops}
+
+
+def c5_measured(hb, device, stream=None, image=32, check=8, with_reference=True):
     """C5 (AlexNet-like COWC: alexnet32_preset layers, large-n16384-d24, 8192
     images per ciphertext set) on one FULL set of encrypted synthetic
     image x image x 3 inputs, device-timed with CUDA events. The layer tensors
@@ -198,6 +252,35 @@ def c5_measured(hb, device, stream=None, image=32, check=8):
                                  "method": "measured 32x32 per-layer times x exact per-layer work ratios"}
     del y, x, model
     eng.close()
+    if with_reference:
+        from oracle import ref
+        if ref.available():
+            threads = os.cpu_count() or 1
+            rl, cache = ref.RefEngine.from_params(p).keygen(1), {}
+            est = reference_per_op_estimate(hb, spec, p, threads, rl, cache)
+            spec64 = hb.glorot_weights(hb.alexnet32_preset(image=64), 1)
+            est64 = reference_per_op_estimate(hb, spec64, p, threads, rl, cache)
+            # method check: the same estimator on C3, whose full set the reference runs
+            pc = hb.preset_params("net-n8192-d8")
+            c3 = c3_spec(hb)
+            rc = ref.RefEngine.from_params(pc).keygen(1)
+            c3_est = reference_per_op_estimate(hb, c3, pc, threads, rc)
+            data3 = np.random.default_rng(3).uniform(0, 1, size=(pc.n // 2, c3.input.positions()))
+            rx = rc.encrypt_tensor(data3, c3.input, seed=11, threads=threads)
+            t0 = time.perf_counter()
+            rc.forward_encrypted(c3, rx, seed=13, threads=threads)
+            c3_wall = time.perf_counter() - t0
+            res["reference_estimate"] = {
+                "kind": "reference", "cores": threads,
+                "sample": "per-op throughputs of the reference's layer ops (oracle/_ref) at every layer level on all "
+                          "host threads x the stack's op counts (SURVEY 8(d): C5 does not run on the CPU)",
+                "32x32": {"seconds_per_set": est["seconds_per_set"],
+                          "images_per_s": (p.n // 2) / est["seconds_per_set"], "layer_s": est["layer_s"]},
+                "64x64": {"seconds_per_set": est64["seconds_per_set"],
+                          "images_per_s": (p.n // 2) / est64["seconds_per_set"]},
+                "method_check_on_c3": {"estimated_s": c3_est["seconds_per_set"], "measured_s": c3_wall,
+                                       "ratio": c3_est["seconds_per_set"] / c3_wall},
+                "probe_wall_s": est["probe_wall_s"] + est64["probe_wall_s"]}
     return res
 
 
@@ -536,7 +619,8 @@ def run_ours(args):
         eng.trim()  # hand C4's cached arena back before the larger C2/C5 runs
         # single-GPU reference figures: at N > 1 the other ranks would idle at the final barrier
         mb = microbench(hb, local) if world == 1 and not args.no_micro else None
-        c5 = c5_measured(hb, local, stream=stream.cuda_stream) if world == 1 and not args.no_c5 else None
+        c5 = (c5_measured(hb, local, stream=stream.cuda_stream, with_reference=not args.no_cpu_baseline)
+              if world == 1 and not args.no_c5 else None)
         if c5 is not None:
             c5["method_check_on_c4"] = xcheck
         c3 = (c3_cryptonets(hb, local, with_reference=not args.no_cpu_baseline, stream=stream.cuda_stream)

@@ -293,6 +293,15 @@ class RefEngine:
                                   ctypes.byref(s)))
         return s.value
 
+    def time_layer_op(self, op: int, level: int, count: int, inner: int, threads: int) -> float:
+        """Seconds for `count` independent items of a reference layer op over its
+        parallel_for (0: relu-poly2 eval_encrypted, 1: one conv/dense output with
+        `inner` scalar MACs + bias + rescale, 2: one zero-pad border encryption)."""
+        s = ctypes.c_double()
+        _check(lib().ref_time_layer_op(self.h, self.keys, int(op), ctypes.c_size_t(level), ctypes.c_size_t(count),
+                                       ctypes.c_size_t(inner), ctypes.c_uint(threads), ctypes.byref(s)))
+        return s.value
+
     def time_mul(self, level: int, count: int, threads: int) -> float:
         s = ctypes.c_double()
         _check(lib().ref_time_mul(self.h, self.keys, ctypes.c_size_t(level), ctypes.c_size_t(count),

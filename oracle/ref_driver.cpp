@@ -491,6 +491,50 @@ int ref_time_mul(void* e, void* k, size_t level, size_t count, unsigned threads,
     });
 }
 
+// Per-op costs of the reference's layer kernels (layers.hpp:174-293,
+// activation.hpp:228-265), `count` independent items over its parallel_for;
+// returns seconds. op 0: eval_encrypted(relu_default_surrogate) at `level`;
+// op 1: make_zero_ciphertext + `inner` mul_scalar_mac + add_scalar_inplace +
+// rescale (one conv / dense output with `inner` taps); op 2: a zero-pad border
+// cell (encode_const(0) at the top, encrypt with a seed, mod_switch to `level`).
+int ref_time_layer_op(void* e, void* k, int op, size_t level, size_t count, size_t inner, unsigned threads,
+                      double* secs) {
+    return guard([&] {
+        const CkksEngine& eng = static_cast<RefEngine*>(e)->eng;
+        const RingContext& ctx = eng.ring();
+        const KeySet* ks = static_cast<KeySet*>(k);
+        const double sc = eng.params().scale;
+        std::vector<Ciphertext> xs(op == 2 ? 0 : count);
+        for (size_t i = 0; i < xs.size(); ++i) {
+            xs[i].c0 = sample_poly(ctx, SampleKind::Uniform, {.level = level}, 2000 + 2 * i);
+            xs[i].c1 = sample_poly(ctx, SampleKind::Uniform, {.level = level}, 2001 + 2 * i);
+            xs[i].level = static_cast<u32>(level);
+            xs[i].scale = sc;
+        }
+        const PolyActivation act = relu_default_surrogate();
+        const CkksEngine::ScalarPlain sp = eng.make_scalar_plain(0.125, sc, level);
+        std::vector<Ciphertext> out(count);
+        auto t0 = std::chrono::steady_clock::now();
+        parallel_for(count, threads, [&](std::size_t b, std::size_t en) {
+            for (std::size_t i = b; i < en; ++i) {
+                if (op == 0) {
+                    out[i] = eval_encrypted(act, xs[i], eng, ks->eval);
+                } else if (op == 1) {
+                    Ciphertext acc = eng.make_zero_ciphertext(level, sc * sp.scale);
+                    for (size_t m = 0; m < inner; ++m) eng.mul_scalar_mac(acc, xs[i], sp);
+                    eng.add_scalar_inplace(acc, 0.25);
+                    out[i] = eng.rescale(acc);
+                } else {
+                    EncodedPlaintext zero = eng.encode_const(0.0, sc, eng.top_level());
+                    Ciphertext ct = eng.encrypt(ks->public_key, zero, CkksEngine::derive_seed(77, 0xbad0 + i));
+                    out[i] = eng.mod_switch(ct, level);
+                }
+            }
+        });
+        *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
 // ---- ckks_serialize.hpp (blob v1): the reference's own save_* / load_*
 // Writes the blob into `buf` (cap bytes); *len = blob size (buf may be null
 // to query it).
