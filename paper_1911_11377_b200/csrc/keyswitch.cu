@@ -482,7 +482,7 @@ __device__ __forceinline__ void ks_item(const DevRing& R, const A& ar, const typ
     // each unit's EL words are contiguous: 16-byte loads and stores. With
     // whole units per thread, every unit's (x0, x1) words are loaded before
     // the first is used (their HBM latency overlaps instead of serialising)
-    constexpr bool EPF = PRIV && T <= 512;  // 1024-thread blocks (64 registers) spill with it
+    constexpr bool EPF = FP && PRIV && T <= 512;  // 1024-thread blocks (64 registers) and the integer path spill with it
     ulonglong2 xpre[EPF ? PL * EL : 1];
     if constexpr (EPF) {
 #pragma unroll
@@ -636,48 +636,23 @@ struct IntKey {
     }
 };
 
-// Persistent: CTA c takes items c, c + gridDim.x, ... of
-// item = (ct * nsel + i - limb0) * nblocks + b over limbs [limb0, limb0 + nsel)
-// (ciphertext-major, so the CTAs running at once share the ciphertexts'
-// digits in L2). FPK: this instantiation serves the FP64 limbs (q < 2^42) and
-// skips the others, or the reverse, so each path gets its own register
-// allocation; the host launches both.
-template <int LOGN, int LOGB, int LOGE, int T, int MINB, bool FPK, bool LIFT>
-__global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
-                                                 const u64* __restrict__ evk_sh, const double* __restrict__ evk_f,
-                                                 u64* __restrict__ acc01, int level, int D, int limb0, int nsel,
-                                                 long long items, int mode, const u64* __restrict__ fy) {
-    constexpr int C = LOGN - LOGB, B = 1 << LOGB;
-    using S = KsShape<LOGN, LOGB, LOGE, T, FPK>;
-    extern __shared__ u64 smem[];
-    uint64_t* bbar = reinterpret_cast<uint64_t*>(smem + 3 * B);
-    uint64_t* tbar = bbar + 1;
-    uint32_t tm_lane = 0;
-    __shared__ uint32_t tm_slot;
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(bbar)));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(tbar)));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if constexpr (S::USE_TMEM) {
-        if (threadIdx.x < 32) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ks_saddr(&tm_slot)),
-                         "n"(S::TCOLS));
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    }
-    __syncthreads();
-    if constexpr (S::USE_TMEM) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int w = threadIdx.x >> 5;
-        tm_lane = tm_slot + (static_cast<uint32_t>((w & 3) * 32) << 16) + static_cast<uint32_t>((w >> 2) * S::TCW);
-    }
+// Persistent, one launch for both limb kinds: CTAs [0, g_int) walk the
+// integer-limb items (60-bit primes, IMAD pipes), CTAs [g_int, grid) the
+// FP64-limb items, each group with its own grid stride over
+// item = (ct * nsel + i - limb0) * nblocks + b for its limb range
+// (ciphertext-major, so the CTAs in flight share the ciphertexts' digits in
+// L2). A limb range may cover limbs of the other kind (mixed chains); those
+// items are skipped.
+template <int LOGN, int LOGB, int LOGE, int T, bool FPK, bool LIFT>
+__device__ __forceinline__ void ks_walk(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh,
+                                        const double* evk_f, u64* acc01, int level, int D, int limb0, int nsel,
+                                        long long items, long long first, long long stride, int mode, const u64* fy,
+                                        uint32_t tm_lane, unsigned& bphase, unsigned& tphase) {
+    constexpr int C = LOGN - LOGB;
     const long long n = 1LL << LOGN;
     const long long key_stride = static_cast<long long>(R.limbs) * n;  // one evk polynomial
-    unsigned bphase = 0, tphase = 0;
     int tw_key = -1;  // (limb, block) whose twiddle table is in shared memory
-    for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+    for (long long item = first; item < items; item += stride) {
         const int b = static_cast<int>(item & ((1 << C) - 1));
         const long long row = item >> C;  // ct * nsel + (i - limb0)
         const long long ct = row / nsel;
@@ -703,12 +678,56 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
                                                 tphase);
         }
     }
-    if constexpr (S::USE_TMEM) {
+}
+
+template <int LOGN, int LOGB, int LOGE, int T, int MINB, bool LIFT>
+__global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
+                                                 const u64* __restrict__ evk_sh, const double* __restrict__ evk_f,
+                                                 u64* __restrict__ acc01, int level, int D, int fp0, int nfp,
+                                                 long long items_fp, int int0, int nint, long long items_int, int g_int,
+                                                 int mode, const u64* __restrict__ fy) {
+    constexpr int B = 1 << LOGB;
+    using SF = KsShape<LOGN, LOGB, LOGE, T, true>;
+    using SI = KsShape<LOGN, LOGB, LOGE, T, false>;
+    static_assert(SF::USE_TMEM == SI::USE_TMEM && SF::TCW == SI::TCW, "both limb kinds share the TMEM layout");
+    extern __shared__ u64 smem[];
+    uint64_t* bbar = reinterpret_cast<uint64_t*>(smem + 3 * B);
+    uint64_t* tbar = bbar + 1;
+    uint32_t tm_lane = 0;
+    __shared__ uint32_t tm_slot;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(bbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(tbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if constexpr (SF::USE_TMEM) {
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ks_saddr(&tm_slot)),
+                         "n"(SF::TCOLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+    __syncthreads();
+    if constexpr (SF::USE_TMEM) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int w = threadIdx.x >> 5;
+        tm_lane = tm_slot + (static_cast<uint32_t>((w & 3) * 32) << 16) + static_cast<uint32_t>((w >> 2) * SF::TCW);
+    }
+    unsigned bphase = 0, tphase = 0;
+    if (static_cast<int>(blockIdx.x) < g_int)
+        ks_walk<LOGN, LOGB, LOGE, T, false, false>(R, digits, evk, evk_sh, evk_f, acc01, level, D, int0, nint, items_int,
+                                                   blockIdx.x, g_int, mode, fy, tm_lane, bphase, tphase);
+    else
+        ks_walk<LOGN, LOGB, LOGE, T, true, LIFT>(R, digits, evk, evk_sh, evk_f, acc01, level, D, fp0, nfp, items_fp,
+                                                 blockIdx.x - g_int, gridDim.x - g_int, mode, fy, tm_lane, bphase,
+                                                 tphase);
+    if constexpr (SF::USE_TMEM) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         if (threadIdx.x < 32) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_slot), "n"(S::TCOLS));
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_slot), "n"(SF::TCOLS));
         }
     }
 }
@@ -750,25 +769,24 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
 #else
     const bool lift = R.small_primes;
 #endif
-    auto kfp = lift ? k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, true>
-                              : k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, false>;
-    auto kint = k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false, false>;
+    auto kern = lift ? k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true>
+                     : k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false>;
     // data + staged twiddles (u64 Shoup pairs on the integer path; double
-    // twiddles + c1 accumulators on the FP64 path)
-    const int smem = P::B * (8 + 16) + 64;  // + the b_t stage's and twiddle table's mbarriers
+    // twiddles + the b_t stage or c1 accumulators on the FP64 path) + mbarriers
+    const int smem = P::B * (8 + 16) + 64;
     static bool init = (smem > 48 * 1024
-                            ? (cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, true>,
+                            ? (cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                               cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, false>,
+                               cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false>,
                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                               cudaFuncSetAttribute(kint, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true)
+                               true)
                             : true);
     (void)init;
     const int limbs = level + 1;
     const unsigned long long lmask = limbs >= 64 ? ~0ull : (1ull << limbs) - 1;
     const unsigned long long int_mask = R.int_limbs & lmask;
     // exact limb ranges when only q0 is an integer limb (the presets); otherwise
-    // both kernels cover every limb and skip the other kind's rows
+    // both CTA groups cover every limb and skip the other kind's items
     int fp0 = 0, nfp = limbs, int0 = 0, nint = limbs;
     if (int_mask == 0) nint = 0;
     else if (int_mask == lmask) nfp = 0;
@@ -777,19 +795,16 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
     // per (ct, limb, digit): one N-point NTT + 2N MACs; bytes: evk once + digits + acc r/w
     L.begin("k_keyswitch", cl * D * (n / 2 * LOGN + 2 * n),
             2.0 * D * limbs * n * 8 + double(count) * D * n * 4 + cl * 2 * n * 8 * 2);
-    // Persistent grids: the capacity (resident CTAs per SM x SMs) is split
-    // between the FP64-limb and integer-limb kernels in proportion to their
-    // work (an integer-limb item costs HECNN_KS_INT_COST FP64 items), so both
-    // finish together when they run side by side.
-    static int sms = 0, occ_fp = 0, occ_int = 0;
+    // Persistent grid = resident CTAs per SM x SMs, split between the two CTA
+    // groups in proportion to their work (an integer-limb item costs
+    // HECNN_KS_INT_COST FP64 items), so both groups finish together.
+    static int sms = 0, occ = 0;
     if (!sms) {
         int dev = 0;
         cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
         cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fp, kfp, P::T, smem), "occupancy");
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_int, kint, P::T, smem), "occupancy");
-        occ_fp = std::max(occ_fp, 1);
-        occ_int = std::max(occ_int, 1);
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, P::T, smem), "occupancy");
+        occ = std::max(occ, 1);
     }
 #ifndef HECNN_KS_INT_COST
 #define HECNN_KS_INT_COST 2.75
@@ -798,30 +813,23 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
     const long long items_fp = static_cast<long long>(count) * nfp * nb, items_int = static_cast<long long>(count) * nint * nb;
     const int n_int_limbs = __builtin_popcountll(int_mask);
     const double w_fp = double(count) * (limbs - n_int_limbs) * nb, w_int = double(count) * n_int_limbs * nb * HECNN_KS_INT_COST;
-    auto launch = [&](auto kern, cudaStream_t st, int l0, int nsel, long long items, long long grid) {
-        grid = std::max(1LL, std::min(grid, items));
-        kern<<<static_cast<unsigned>(grid), P::T, smem, st>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, l0, nsel, items,
-                                                             mode, fy);
-    };
-    // The integer-limb kernel (IMAD pipes) runs on the side stream beside the
-    // FP64 kernel on its share of the SMs.
-    const bool split = nfp && nint && L.aux;
-    unsigned long long launched = 0;
-    if (split) {
-        const long long cap = static_cast<long long>(sms) * std::min(occ_fp, occ_int);
-        long long g_int = std::llround(double(cap) * w_int / (w_int + w_fp));
-        g_int = std::min(std::max(g_int, 1LL), cap - 1);
-        cuda_check(cudaEventRecord(L.fork_ev, L.stream), "cudaEventRecord");
-        cuda_check(cudaStreamWaitEvent(L.aux, L.fork_ev, 0), "cudaStreamWaitEvent");
-        launch(kint, L.aux, int0, nint, items_int, g_int);
-        launch(kfp, L.stream, fp0, nfp, items_fp, cap - g_int);
-        cuda_check(cudaEventRecord(L.join_ev, L.aux), "cudaEventRecord");
-        cuda_check(cudaStreamWaitEvent(L.stream, L.join_ev, 0), "cudaStreamWaitEvent");
-        launched = 2;
+    const long long cap = static_cast<long long>(sms) * occ;
+    long long g_int = 0, g_fp = 0;
+    if (!items_int) {
+        g_fp = std::min(cap, items_fp);
+    } else if (!items_fp) {
+        g_int = std::min(cap, items_int);
     } else {
-        if (nfp) launch(kfp, L.stream, fp0, nfp, items_fp, static_cast<long long>(sms) * occ_fp), ++launched;
-        if (nint) launch(kint, L.stream, int0, nint, items_int, static_cast<long long>(sms) * occ_int), ++launched;
+        g_int = std::llround(double(cap) * w_int / (w_int + w_fp));
+        g_int = std::min(std::max(g_int, 1LL), cap - 1);
+        g_fp = cap - g_int;
+        g_int = std::min(g_int, items_int);
+        g_fp = std::min(g_fp, items_fp);
     }
+    kern<<<static_cast<unsigned>(g_int + g_fp), P::T, smem, L.stream>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, fp0,
+                                                                       nfp, items_fp, int0, nint, items_int,
+                                                                       static_cast<int>(g_int), mode, fy);
+    const unsigned long long launched = 1;
     L.count(launched);
 }
 

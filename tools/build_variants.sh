@@ -4,10 +4,7 @@ set -e
 cd "$(dirname "$0")/.."
 declare -A V
 V[na]=""
-V[ic20]="-DHECNN_KS_INT_COST=2.0"
-V[ic25]="-DHECNN_KS_INT_COST=2.5"
-V[ic32]="-DHECNN_KS_INT_COST=3.25"
-V[ic40]="-DHECNN_KS_INT_COST=4.0"
+V[col512]="-DHECNN_KS_MAXT_COL=512"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
