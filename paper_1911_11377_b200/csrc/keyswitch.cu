@@ -133,25 +133,7 @@ __global__ void __launch_bounds__(128) k_crt_digits(DevRing R, const u64* __rest
 
 __device__ __forceinline__ u64 lift_digit(u32 v, u64 q) { return v < q ? v : v % q; }
 
-// ---- tensor memory / bulk-copy helpers (FP64 path with HECNN_KS_TMEM) -------
-__device__ __forceinline__ uint32_t ks_saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void ks_mbar_wait(uint64_t* b, unsigned parity) {
-    asm volatile(
-        "{.reg .pred P1;\n"
-        "WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;}" ::"r"(ks_saddr(b)),
-        "r"(parity)
-        : "memory");
-}
-// one bulk copy of `bytes` from global into shared memory, completing on `bar`
-[[maybe_unused]] __device__ __forceinline__ void ks_bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of dst before the async write
-    asm volatile("{.reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;}" ::"r"(ks_saddr(bar)), "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(ks_saddr(dst)),
-                 "l"(src), "r"(bytes), "r"(ks_saddr(bar))
-                 : "memory");
-}
+// ---- tensor memory / bulk-copy helpers: ks_saddr / ks_mbar_wait / ks_bulk_load (ntt_core.cuh)
 // EL doubles of this thread's TMEM lane at column `col` (2 x 32-bit columns each)
 template <int EL>
 __device__ __forceinline__ void tmem_ld_d(uint32_t addr, double (&v)[EL]) {
@@ -372,8 +354,8 @@ __device__ __forceinline__ void ks_item(const DevRing& R, const A& ar, const typ
     // the previous item's rounds are over (barrier after its last digit):
     // shared memory may be refilled
     if (threadIdx.x == 0) {
-        if (load_tw) ks_bulk_load(stw, tw_block, B * sizeof(TW), tbar);
-        if constexpr (TM) ks_bulk_load(sacc, key.evk_f + key.ioff + blk_off, B * 8, bbar);  // b_0 of this block
+        if (load_tw) ntt::bulk_load(stw, tw_block, B * sizeof(TW), tbar);
+        if constexpr (TM) ntt::bulk_load(sacc, key.evk_f + key.ioff + blk_off, B * 8, bbar);  // b_0 of this block
     }
     if constexpr (USE_TMEM) {
         const u64 z[EL] = {};
@@ -409,7 +391,7 @@ __device__ __forceinline__ void ks_item(const DevRing& R, const A& ar, const typ
     };
     prefetch(0);
     if (load_tw) {
-        ks_mbar_wait(tbar, tphase & 1);  // twiddle table landed
+        ntt::mbar_wait(tbar, tphase & 1);  // twiddle table landed
         ++tphase;
     }
     if constexpr (!TM) __syncthreads();  // zeroed c1 slots before any thread accumulates
@@ -440,7 +422,7 @@ __device__ __forceinline__ void ks_item(const DevRing& R, const A& ar, const typ
                                           if (k == EL - 1) {
                                               const int base = idx - (EL - 1);
                                               if constexpr (TM) {
-                                                  ks_mbar_wait(bbar, par);  // b_t landed
+                                                  ntt::mbar_wait(bbar, par);  // b_t landed
                                                   key.template unit_tm<EL>(t, blk_off + base, stash, a0 + uu * EL,
                                                                            sacc + base, tm_lane + uu * 2 * EL);
                                               } else if constexpr (FP) {
@@ -464,7 +446,7 @@ __device__ __forceinline__ void ks_item(const DevRing& R, const A& ar, const typ
         __syncthreads();  // the next digit's first round overwrites shared memory
         if constexpr (TM) {
             if (threadIdx.x == 0 && t + 1 < D)
-                ks_bulk_load(sacc, key.evk_f + (2LL * (t + 1)) * key.key_stride + key.ioff + blk_off, B * 8, bbar);
+                ntt::bulk_load(sacc, key.evk_f + (2LL * (t + 1)) * key.key_stride + key.ioff + blk_off, B * 8, bbar);
         }
     }
     const int limbs = level + 1;
@@ -696,13 +678,13 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
     uint32_t tm_lane = 0;
     __shared__ uint32_t tm_slot;
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(bbar)));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ks_saddr(tbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ntt::smem_addr(bbar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ntt::smem_addr(tbar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if constexpr (SF::USE_TMEM) {
         if (threadIdx.x < 32) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ks_saddr(&tm_slot)),
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ntt::smem_addr(&tm_slot)),
                          "n"(SF::TCOLS));
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
         }

@@ -20,6 +20,7 @@
 // Values stay lazily reduced ([0,4q) forward, [0,2q) inverse) and are made
 // canonical at the end, so results are word-identical to the CPU reference.
 
+#include <algorithm>
 #include <stdexcept>
 
 #include "ntt_core.cuh"

@@ -21,6 +21,7 @@
 //               runs it 2.7x faster than integer Shoup (tools/modmul_probe.cu).
 // Both produce the same residues; the caller's epilogue makes them canonical.
 #pragma once
+#include <cstdint>
 #include <type_traits>
 
 #include "kernels.hpp"
@@ -271,9 +272,9 @@ __device__ __forceinline__ void fwd_rest(typename A::V* s, const A& ar, const ty
 // stores with `last`, the rest go through shared memory `s`. `after_first`
 // runs once the first round's inputs are consumed (e.g. to start loading the
 // next transform's inputs into the same registers).
-template <int LOGB, int LOGE, int T, class A, class First, class Last, class Hook = NoHook>
+template <int LOGB, int LOGE, int T, class A, class First, class Last, class Hook = NoHook, class Hook2 = NoHook>
 __device__ __forceinline__ void fwd_block(typename A::V* s, const A& ar, const typename A::TW* tw, int b, int c,
-                                          First first, Last last, Hook after_first = Hook{}) {
+                                          First first, Last last, Hook after_first = Hook{}, Hook2 after_sync = Hook2{}) {
     using V = typename A::V;
     constexpr int R0 = round_size(LOGB, LOGE, 0);
     if constexpr (R0 >= LOGB) {
@@ -283,6 +284,7 @@ __device__ __forceinline__ void fwd_block(typename A::V* s, const A& ar, const t
         fwd_round<LOGB, R0, 0, T>(ar, tw, b, c, first, SmemStore<V>{s}, threadIdx.x);
         after_first();
         __syncthreads();
+        after_sync();  // every thread is past the first round (its inputs are consumed)
         using SP = Split<LOGB, LOGE, T>;
         if constexpr (SP::on) {
             const int g = threadIdx.x / SP::TG, lt = threadIdx.x % SP::TG;
@@ -396,6 +398,31 @@ __device__ __forceinline__ void inv_block(typename A::V* s, const A& ar, const t
     } else {
         inv_rest<LOGB, LOGE, T, A, 0>(s, ar, tw, b, c, first, last, [] { __syncthreads(); }, threadIdx.x);
     }
+}
+
+// ---- mbarrier / bulk-copy helpers (cp.async.bulk into shared memory)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{.reg .pred P1;\n"
+        "WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;}" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+// one bulk copy of `bytes` (multiple of 16) from global into shared memory,
+// completing on `bar`; the caller has ordered earlier generic accesses to dst
+// (barrier) -- the proxy fence makes them visible to the async proxy
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("{.reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;}" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
 }
 
 // Limbs whose prime fits the FP64 path.
