@@ -8,6 +8,8 @@
 #include <stdexcept>
 #include <string>
 
+#include <type_traits>
+
 #include "ntt_core.cuh"
 
 namespace hecnn_b200 {
@@ -54,56 +56,82 @@ __global__ void k_elementwise(DevRing R, int op, const u64* __restrict__ a, cons
 #ifndef HECNN_RESCALE_MINB
 #define HECNN_RESCALE_MINB 8  // 32 registers: full occupancy for this latency-bound stream (measured 37 -> 32 ms per C4 step)
 #endif
+#ifndef HECNN_RESCALE_VEC
+#define HECNN_RESCALE_VEC 2  // coefficients per thread (16-byte loads / stores when 2)
+#endif
 template <bool SCALED, bool ADD>
 __global__ void __launch_bounds__(TPB, HECNN_RESCALE_MINB) k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level,
                           const ulonglong2* __restrict__ c, SumTerms t) {
-    const int j = blockIdx.y * TPB + threadIdx.x;
+    constexpr int VW = HECNN_RESCALE_VEC;
+    const int j = (blockIdx.y * TPB + threadIdx.x) * VW;
     if (j >= R.n) return;
     const long long poly = blockIdx.x;
     const u64* src = in + poly * (level + 1) * R.n;
     u64* dst = out + poly * level * R.n;
     const u64 p = R.mod[level].q;
-    u64 v = src[static_cast<long long>(level) * R.n + j];
-    if constexpr (SCALED) v = mul_shoup(v, c[level].x, c[level].y, p);
-    const bool upper = v > (p >> 1);
-    // FP64 limbs (q_i < 2^42) when the dropped residue is an exact double:
-    // centre(v) mod q_i = fcentre(v) - [upper] (p mod q_i), any representative
-    // (the result is canonicalised once at the end)
-    const bool v_fp = v < (1ull << 51);
-    const double vf = v_fp ? ntt::to_fp(v) : 0.0;
+    auto ld = [](const u64* ptr, u64 (&v)[VW]) {
+        if constexpr (VW == 2) {
+            const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(ptr));
+            v[0] = w.x, v[1] = w.y;
+        } else {
+            v[0] = __ldg(ptr);
+        }
+    };
+    u64 v[VW];
+    ld(src + static_cast<long long>(level) * R.n + j, v);
+    bool upper[VW], v_fp = true;
+    double vf[VW];
+#pragma unroll
+    for (int h = 0; h < VW; ++h) {
+        if constexpr (SCALED) v[h] = mul_shoup(v[h], c[level].x, c[level].y, p);
+        upper[h] = v[h] > (p >> 1);
+        // FP64 limbs (q_i < 2^42) when the dropped residue is an exact double:
+        // centre(v) mod q_i = fcentre(v) - [upper] (p mod q_i), any representative
+        // (the result is canonicalised once at the end)
+        v_fp = v_fp && v[h] < (1ull << 51);
+        vf[h] = ntt::to_fp(v[h] & ((1ull << 51) - 1));
+    }
     for (int i = 0; i < level; ++i) {
         const ModConst m = R.mod[i];
         const ulonglong2 inv = R.inv_dropped[level * R.limbs + i];
-        const u64 a = src[static_cast<long long>(i) * R.n + j];
-        u64 r;
+        u64 a[VW], r[VW];
+        ld(src + static_cast<long long>(i) * R.n + j, a);
         if (v_fp && ntt::fp_limb(m.q)) {
             const double q = static_cast<double>(m.q), qinv = R.inv_q[i];
-            double cen = ntt::fcentre(vf, q, qinv);
-            if (upper) cen -= ntt::to_fp(R.p_mod[level * R.limbs + i]);
-            double x = ntt::to_fp(a);
-            if constexpr (SCALED) x = ntt::fmodmul(x, ntt::to_fp(c[i].x), q, qinv);
-            double y = ntt::fmodmul(x - cen, ntt::to_fp(inv.x), q, qinv);
-            if constexpr (ADD) {
+            const double pm = ntt::to_fp(R.p_mod[level * R.limbs + i]), invf = ntt::to_fp(inv.x);
 #pragma unroll
-                for (int k = 0; k < kMaxTerms; ++k)
-                    if (k < t.count) y += ntt::to_fp(__ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j));
-                if (t.c0 && j == 0 && (poly & 1) == 0) y += ntt::to_fp(t.c0[i]);
+            for (int h = 0; h < VW; ++h) {
+                double cen = ntt::fcentre(vf[h], q, qinv);
+                if (upper[h]) cen -= pm;
+                double x = ntt::to_fp(a[h]);
+                if constexpr (SCALED) x = ntt::fmodmul(x, ntt::to_fp(c[i].x), q, qinv);
+                double y = ntt::fmodmul(x - cen, invf, q, qinv);
+                if constexpr (ADD) {
+#pragma unroll
+                    for (int k = 0; k < kMaxTerms; ++k)
+                        if (k < t.count) y += ntt::to_fp(__ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j + h));
+                    if (t.c0 && j + h == 0 && (poly & 1) == 0) y += ntt::to_fp(t.c0[i]);
+                }
+                r[h] = ntt::fcanon(y, q, qinv);
             }
-            r = ntt::fcanon(y, q, qinv);
         } else {
-            u64 centred = reduce_near(v, m);
-            if (upper) centred = sub_mod(centred, R.p_mod[level * R.limbs + i], m.q);
-            u64 x = a;
-            if constexpr (SCALED) x = mul_shoup(x, c[i].x, c[i].y, m.q);
-            r = mul_shoup(sub_mod(x, centred, m.q), inv.x, inv.y, m.q);
-            if constexpr (ADD) {
 #pragma unroll
-                for (int k = 0; k < kMaxTerms; ++k)
-                    if (k < t.count) r = add_mod(r, __ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j), m.q);
-                if (t.c0 && j == 0 && (poly & 1) == 0) r = add_mod(r, t.c0[i], m.q);
+            for (int h = 0; h < VW; ++h) {
+                u64 centred = reduce_near(v[h], m);
+                if (upper[h]) centred = sub_mod(centred, R.p_mod[level * R.limbs + i], m.q);
+                u64 x = a[h];
+                if constexpr (SCALED) x = mul_shoup(x, c[i].x, c[i].y, m.q);
+                r[h] = mul_shoup(sub_mod(x, centred, m.q), inv.x, inv.y, m.q);
+                if constexpr (ADD) {
+#pragma unroll
+                    for (int k = 0; k < kMaxTerms; ++k)
+                        if (k < t.count) r[h] = add_mod(r[h], __ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j + h), m.q);
+                    if (t.c0 && j + h == 0 && (poly & 1) == 0) r[h] = add_mod(r[h], t.c0[i], m.q);
+                }
             }
         }
-        dst[static_cast<long long>(i) * R.n + j] = r;
+        if constexpr (VW == 2) *reinterpret_cast<ulonglong2*>(dst + static_cast<long long>(i) * R.n + j) = make_ulonglong2(r[0], r[1]);
+        else dst[static_cast<long long>(i) * R.n + j] = r[0];
     }
 }
 
@@ -367,7 +395,7 @@ void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t c
     const double extra = add ? add->count : 0;
     L.begin("k_rescale", double(count) * level * R.n * (scale_by ? 2 : 1),
             8.0 * count * R.n * (2 * level + 1 + extra * level));
-    const dim3 grid = rows_grid(count, R.n);
+    const dim3 grid = rows_grid(count, R.n / HECNN_RESCALE_VEC);
     if (add) k_rescale<true, true><<<grid, TPB, 0, L.stream>>>(R, in, out, level, scale_by, *add);
     else if (scale_by) k_rescale<true, false><<<grid, TPB, 0, L.stream>>>(R, in, out, level, scale_by, none);
     else k_rescale<false, false><<<grid, TPB, 0, L.stream>>>(R, in, out, level, nullptr, none);

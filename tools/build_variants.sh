@@ -4,7 +4,8 @@ set -e
 cd "$(dirname "$0")/.."
 declare -A V
 V[na]=""
-V[col512]="-DHECNN_KS_MAXT_COL=512"
+V[pfm6]="-DHECNN_RESCALE_MINB=6"
+V[pfm4]="-DHECNN_RESCALE_MINB=4"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
