@@ -4,8 +4,7 @@ set -e
 cd "$(dirname "$0")/.."
 declare -A V
 V[na]=""
-V[pfm6]="-DHECNN_RESCALE_MINB=6"
-V[pfm4]="-DHECNN_RESCALE_MINB=4"
+V[ks2]="-DHECNN_KS_2CTA=1"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
