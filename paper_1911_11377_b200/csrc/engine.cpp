@@ -855,48 +855,53 @@ namespace detail {
 // Public-key encryptions of `count` messages (or zeros) at limbs 0..level,
 // randomness from make_encryption_randomness(seeds[i]) (ckks.hpp:238-266).
 // out: [count][2][level+1][n] device.
-void encrypt_into(Context& C, std::size_t count, const u64* seeds, const std::vector<EncodedCoeffs>* msgs,
-                  std::uint32_t level, u64* out) {
+// One chunk of host-side encryption inputs: randomness (int8) and the
+// message as i64 coefficients (small) or full residues.
+struct HostChunk {
+    std::vector<signed char> r, e0, e1;
+    std::vector<long long> mi;
+    std::vector<u64> mres;
+    bool small = true;
+};
+using ChunkFn = std::function<void(std::size_t c0, std::size_t m, HostChunk&)>;
+
+// Public-key encryptions of `count` cells at limbs 0..level into out, in
+// chunks: the host work of chunk k + 1 (sampling, and the encode for
+// encrypt_tensor) runs on a host thread while chunk k's uploads and device
+// arithmetic (NTT, key products, INTT, noise + message) are issued -- pageable
+// uploads return once staged, so two host buffers alternate.
+void encrypt_pipelined(Context& C, std::size_t count, std::uint32_t level, u64* out, bool with_msgs,
+                       const ChunkFn& produce) {
     if (!C.has_pk) throw std::invalid_argument("encrypt: no public key loaded");
     const std::size_t n = C.n(), limbs = level + 1, cw = 2 * limbs * n;
-    const std::size_t chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, 1024));
+    const std::size_t chunk = std::max<std::size_t>(1, std::min<std::size_t>(count, 512));
     Launch L = C.L();
-    std::vector<signed char> hr(chunk * n), he0(chunk * n), he1(chunk * n);
-    std::vector<long long> hm;
-    std::vector<u64> hres;
     DevBuf dr(&C, chunk * n), de0(&C, chunk * n), de1(&C, chunk * n), rr(&C, chunk * limbs * n * 8);
-    DevBuf dm(&C, msgs ? chunk * limbs * n * 8 : 0), dmi(&C, msgs ? chunk * n * 8 : 0);
-    for (std::size_t c0 = 0; c0 < count; c0 += chunk) {
+    DevBuf dm(&C, with_msgs ? chunk * limbs * n * 8 : 0), dmi(&C, with_msgs ? chunk * n * 8 : 0);
+    HostChunk host[2];
+    auto make = [&](std::size_t c0, HostChunk& h) {
         const std::size_t m = std::min(chunk, count - c0);
-        parallel_items(m, [&](std::size_t k) {
-            const u64 s = seeds[c0 + k];
-            to_int8(sample_secretish(C, 0.5, derive_seed(s, 0x0a01)), &hr[k * n]);
-            to_int8(sample_error(C, derive_seed(s, 0x0a02)), &he0[k * n]);
-            to_int8(sample_error(C, derive_seed(s, 0x0a03)), &he1[k * n]);
-        });
-        C.upload(dr.get(), hr.data(), m * n);
-        C.upload(de0.get(), he0.data(), m * n);
-        C.upload(de1.get(), he1.data(), m * n);
-        // (encrypt_sampled below is the same device sequence for pre-sampled noise)
+        h.r.resize(m * n);
+        h.e0.resize(m * n);
+        h.e1.resize(m * n);
+        produce(c0, m, h);
+    };
+    std::future<void> next = std::async(std::launch::async, make, 0, std::ref(host[0]));
+    for (std::size_t c0 = 0, k = 0; c0 < count; c0 += chunk, ++k) {
+        const std::size_t m = std::min(chunk, count - c0);
+        next.get();  // rethrows the producer's exception (e.g. encode range checks)
+        HostChunk& h = host[k & 1];
+        if (c0 + chunk < count) next = std::async(std::launch::async, make, c0 + chunk, std::ref(host[(k + 1) & 1]));
+        C.upload(dr.get(), h.r.data(), m * n);
+        C.upload(de0.get(), h.e0.data(), m * n);
+        C.upload(de1.get(), h.e1.data(), m * n);
         const u64* mres = nullptr;
-        if (msgs) {
-            bool all_small = true;
-            for (std::size_t k = 0; k < m; ++k) all_small = all_small && (*msgs)[c0 + k].small;
-            if (all_small) {
-                hm.resize(m * n);
-                for (std::size_t k = 0; k < m; ++k) std::memcpy(&hm[k * n], (*msgs)[c0 + k].coeffs.data(), n * 8);
-                C.upload(dmi.get(), hm.data(), m * n * 8);
+        if (with_msgs) {
+            if (h.small) {
+                C.upload(dmi.get(), h.mi.data(), m * n * 8);
                 i64_to_rns(C.dev, dmi.as<long long>(), dm.as<u64>(), static_cast<int>(level), m, L);
             } else {
-                hres.assign(m * limbs * n, 0);
-                for (std::size_t k = 0; k < m; ++k) {
-                    const EncodedCoeffs& e = (*msgs)[c0 + k];
-                    for (std::size_t i = 0; i < limbs; ++i)
-                        for (std::size_t j = 0; j < n; ++j)
-                            hres[(k * limbs + i) * n + j] =
-                                e.small ? C.ring.mods[i].from_signed(e.coeffs[j]) : e.residues[i * n + j];
-                }
-                C.upload(dm.get(), hres.data(), hres.size() * 8);
+                C.upload(dm.get(), h.mres.data(), m * limbs * n * 8);
             }
             mres = dm.as<u64>();
         }
@@ -907,6 +912,41 @@ void encrypt_into(Context& C, std::size_t count, const u64* seeds, const std::ve
         ntt_inverse(C.dev, o, static_cast<int>(level), 2 * m, L);
         add_noise_msg(C.dev, o, de0.as<signed char>(), de1.as<signed char>(), mres, static_cast<int>(level), m, L);
     }
+}
+
+// make_encryption_randomness(seed) (ckks.hpp:238-244) as int8 rows
+void sample_randomness(Context& C, u64 s, signed char* r, signed char* e0, signed char* e1) {
+    to_int8(sample_secretish(C, 0.5, derive_seed(s, 0x0a01)), r);
+    to_int8(sample_error(C, derive_seed(s, 0x0a02)), e0);
+    to_int8(sample_error(C, derive_seed(s, 0x0a03)), e1);
+}
+
+// the message rows of chunk cells from encoded messages
+void fill_messages(Context& C, const EncodedCoeffs* msgs, std::size_t m, std::uint32_t level, HostChunk& h) {
+    const std::size_t n = C.n(), limbs = level + 1;
+    h.small = true;
+    for (std::size_t k = 0; k < m; ++k) h.small = h.small && msgs[k].small;
+    if (h.small) {
+        h.mi.resize(m * n);
+        for (std::size_t k = 0; k < m; ++k) std::memcpy(&h.mi[k * n], msgs[k].coeffs.data(), n * 8);
+    } else {
+        h.mres.assign(m * limbs * n, 0);
+        for (std::size_t k = 0; k < m; ++k) {
+            const EncodedCoeffs& e = msgs[k];
+            for (std::size_t i = 0; i < limbs; ++i)
+                for (std::size_t j = 0; j < n; ++j)
+                    h.mres[(k * limbs + i) * n + j] = e.small ? C.ring.mods[i].from_signed(e.coeffs[j]) : e.residues[i * n + j];
+        }
+    }
+}
+
+void encrypt_into(Context& C, std::size_t count, const u64* seeds, const std::vector<EncodedCoeffs>* msgs,
+                  std::uint32_t level, u64* out) {
+    const std::size_t n = C.n();
+    encrypt_pipelined(C, count, level, out, msgs != nullptr, [&](std::size_t c0, std::size_t m, HostChunk& h) {
+        parallel_items(m, [&](std::size_t k) { sample_randomness(C, seeds[c0 + k], &h.r[k * n], &h.e0[k * n], &h.e1[k * n]); });
+        if (msgs) fill_messages(C, msgs->data() + c0, m, level, h);
+    });
 }
 
 void encrypt_sampled(Context& C, std::size_t count, const signed char* r, const signed char* e0, const signed char* e1,
@@ -975,21 +1015,35 @@ PadNoiseMap start_pad_noise(Context& C, const Model& M, u64 seed) {
 
 using detail::encrypt_into;
 
-// encrypt_tensor (tensor.hpp:77-94)
+// encrypt_tensor (tensor.hpp:77-94): the host encode (long-double FFT) and the
+// randomness of cell chunk k + 1 run on host threads while chunk k encrypts
+// on the device.
 TensorPtr encrypt_tensor(Context& C, const double* data, std::size_t batch, std::size_t positions, u64 seed) {
     if (batch > C.n() / 2) throw std::invalid_argument("encrypt_tensor: batch exceeds slot count");
-    const std::size_t top = C.top();
-    std::vector<EncodedCoeffs> msgs(positions);
-    std::vector<u64> seeds(positions);
-    parallel_items(positions, [&](std::size_t pos) {
-        std::vector<double> slots(batch);
-        for (std::size_t i = 0; i < batch; ++i) slots[i] = data[i * positions + pos];
-        C.enc->encode_real(slots.data(), batch, C.scale, top, msgs[pos]);
-        seeds[pos] = derive_seed(seed, 0xce11 + pos);
-    });
+    const std::size_t top = C.top(), n = C.n();
     TensorPtr out = make_tensor(C, positions, static_cast<std::uint32_t>(top), C.scale);
     out->batch = batch;
-    encrypt_into(C, positions, seeds.data(), &msgs, static_cast<std::uint32_t>(top), out->data());
+    detail::encrypt_pipelined(C, positions, static_cast<std::uint32_t>(top), out->data(), true,
+                              [&](std::size_t c0, std::size_t m, detail::HostChunk& h) {
+                                  std::vector<EncodedCoeffs> part(m);
+                                  std::vector<std::string> errs(m);
+                                  parallel_items(m, [&](std::size_t k) {
+                                      const std::size_t pos = c0 + k;
+                                      try {
+                                          std::vector<double> slots(batch);
+                                          for (std::size_t i = 0; i < batch; ++i) slots[i] = data[i * positions + pos];
+                                          C.enc->encode_real(slots.data(), batch, C.scale, top, part[k]);
+                                      } catch (const std::exception& e) {
+                                          errs[k] = e.what();
+                                          return;
+                                      }
+                                      detail::sample_randomness(C, derive_seed(seed, 0xce11 + pos), &h.r[k * n],
+                                                                &h.e0[k * n], &h.e1[k * n]);
+                                  });
+                                  for (const auto& e : errs)
+                                      if (!e.empty()) throw std::invalid_argument(e);
+                                  detail::fill_messages(C, part.data(), m, static_cast<std::uint32_t>(top), h);
+                              });
     return out;
 }
 

@@ -4,7 +4,8 @@ set -e
 cd "$(dirname "$0")/.."
 declare -A V
 V[na]=""
-V[ks2]="-DHECNN_KS_2CTA=1"
+V[kse4]="-DHECNN_KS_LOGE=4"
+V[nosplit]="-DHECNN_NTT_SPLIT=0"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
