@@ -341,6 +341,23 @@ def forward_plain(model_spec, data: np.ndarray) -> np.ndarray:
     return out
 
 
+def save_model(model_spec, base: str):
+    """The reference's save_model (model_io.hpp:61-103) of a model spec."""
+    desc, keep = model_spec.to_desc()
+    _check(lib().ref_save_model(ctypes.byref(desc), base.encode()))
+
+
+def save_dataset(count: int, image: int, channels: int, seed: int, path: str):
+    """The reference's gen_synthetic + save_dataset (an HDTS file)."""
+    _check(lib().ref_save_dataset(ctypes.c_size_t(count), ctypes.c_size_t(image), ctypes.c_size_t(channels),
+                                  ctypes.c_uint64(seed), path.encode()))
+
+
+def load_model_check(base: str):
+    """Runs the reference's load_model on `base`; raises its error if rejected."""
+    _check(lib().ref_load_model_weights(base.encode(), None, None, ctypes.c_size_t(0)))
+
+
 def rng_uniform(seed: int, count: int) -> np.ndarray:
     out = np.empty(count, dtype=np.float64)
     _check(lib().ref_rng_uniform(ctypes.c_uint64(seed), ctypes.c_size_t(count), _p(out, ctypes.c_double)))

@@ -427,6 +427,33 @@ int ref_init_random_weights(const hecnn_model_desc* desc, uint64_t seed, double*
     });
 }
 
+// save_model (model_io.hpp:61-103): manifest + weight blob at `base`
+int ref_save_model(const hecnn_model_desc* desc, const char* base) {
+    return guard([&] { save_model(base, model_from(desc)); });
+}
+
+// load_model (model_io.hpp:105-181) round trip: loads `base` and writes its
+// weights / biases into the caller's buffers (sized by shape inference); the
+// reference's errors for a malformed file come back as the status + message
+int ref_load_model_weights(const char* base, double* const* weights, double* const* biases, size_t n_layers) {
+    return guard([&] {
+        ModelSpec m = load_model(base);
+        if (!n_layers) return;  // validation only
+        if (m.layers.size() != n_layers) throw std::invalid_argument("ref: layer count differs");
+        for (size_t i = 0; i < n_layers; ++i) {
+            if (weights[i]) std::memcpy(weights[i], m.weights[i].data(), m.weights[i].size() * sizeof(double));
+            if (biases[i]) std::memcpy(biases[i], m.biases[i].data(), m.biases[i].size() * sizeof(double));
+        }
+    });
+}
+
+// gen_synthetic + save_dataset (synthetic.hpp:24-99): an HDTS file
+int ref_save_dataset(size_t count, size_t image, size_t channels, uint64_t seed, const char* path) {
+    return guard([&] {
+        save_dataset(path, gen_synthetic({.count = count, .image = image, .channels = channels, .seed = seed}));
+    });
+}
+
 // Rng::uniform01 stream (common.hpp:173-179): `count` draws from Rng(seed)
 int ref_rng_uniform(uint64_t seed, size_t count, double* out) {
     return guard([&] {

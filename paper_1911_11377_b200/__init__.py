@@ -365,6 +365,21 @@ class Shape:
 
 CONV2D, AVG_POOL2D, ZERO_PAD2D, DENSE, ACTIVATION, SIGMOID = range(6)
 
+_M64 = (1 << 64) - 1
+
+
+def splitmix64(x: int) -> int:
+    """splitmix64 (common.hpp:164-169)"""
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def derive_seed(seed: int, domain: int) -> int:
+    """CkksEngine::derive_seed (ckks.hpp:507): splitmix64(seed ^ splitmix64(domain))"""
+    return splitmix64((seed & _M64) ^ splitmix64(domain & _M64))
+
 
 @dataclass
 class LayerSpec:
