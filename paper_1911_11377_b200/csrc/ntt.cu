@@ -263,7 +263,10 @@ void set_smem(K kernel, int bytes) {
 
 template <int LOGN>
 struct NttPlan {
-    static constexpr int LOGB = LOGN <= 14 ? LOGN : 13;
+#ifndef HECNN_NTT_MAXLOGB
+#define HECNN_NTT_MAXLOGB 14
+#endif
+    static constexpr int LOGB = LOGN <= HECNN_NTT_MAXLOGB ? LOGN : 13;
     static constexpr int C = LOGN - LOGB;
     static constexpr int LOGE = LOGB >= 8 ? HECNN_NTT_LOGE : 3;
     static constexpr int UNITS = (1 << LOGB) >> LOGE;

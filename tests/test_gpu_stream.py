@@ -90,3 +90,21 @@ def test_streamed_alexnet_crop_matches_whole_tensor_pass():
     streamed = hb.forward_encrypted(eng.model(spec).set_streaming(hb.Model.STREAM_ALWAYS, tile=1), x, eng, seed=13)
     assert (streamed.level, streamed.scale) == (whole.level, whole.scale)
     assert np.array_equal(streamed.words(), whole.words())
+
+
+def test_streamed_cryptonets_matches_reference(ref):
+    """C3 forced through the streaming executor: the leading pad
+    runs whole, then a stride-2 valid conv + square stage is row-streamed with
+    ragged two-column tiles; every output word equals the reference's."""
+    p = hb.preset_params("net-n8192-d8")
+    spec = bench.c3_spec(hb)
+    threads = os.cpu_count() or 1
+    data = np.random.default_rng(3).uniform(0, 1, size=(p.n // 2, spec.input.positions()))
+    eng = hb.CkksEngine(p).keygen(1)
+    x = eng.encrypt_tensor(data, seed=11, shape=spec.input)
+    y = hb.forward_encrypted(eng.model(spec).set_streaming(hb.Model.STREAM_ALWAYS, tile=2), x, eng, seed=13)
+    r = ref.RefEngine.from_params(p).keygen(1)
+    ry, _ = r.forward_encrypted(spec, r.encrypt_tensor(data, spec.input, seed=11, threads=threads), seed=13,
+                                threads=threads)
+    assert (y.level, y.scale) == ry.info()[1:]
+    assert np.array_equal(y.words(), ry.words())
