@@ -4,7 +4,7 @@ set -e
 cd "$(dirname "$0")/.."
 declare -A V
 V[na]=""
-V[b13]="-DHECNN_NTT_MAXLOGB=13"
+V[p512]="-DHECNN_TC_PROD=512"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
