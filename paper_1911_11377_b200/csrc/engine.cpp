@@ -368,6 +368,25 @@ Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, doubl
             dev.ks_tw_f = tables.back().as<double>();
         }
     }
+    // limb 0 via limbs 1..3 (keyswitch.cu "aux"): the 60-bit q0 alone on the
+    // integer pipes, q1..q3 on the FP64 pipe
+    if (ring.limbs >= 4 && ring.primes[0] >= (1ull << 42) && ring.primes[1] < (1ull << 42) &&
+        ring.primes[2] < (1ull << 42) && ring.primes[3] < (1ull << 42)) {
+        using u128 = unsigned __int128;
+        const u128 Pq = static_cast<u128>(ring.primes[1]) * ring.primes[2] * ring.primes[3];
+        for (int a = 0; a < 3; ++a) {
+            const u64 qa = ring.primes[1 + a];
+            const u128 Ma = Pq / qa;
+            dev.aux_M[a][0] = static_cast<u64>(Ma), dev.aux_M[a][1] = static_cast<u64>(Ma >> 64);
+            const u64 inv = ring.mods[1 + a].inv(static_cast<u64>(Ma % qa));
+            dev.aux_inv[a] = make_ulonglong2(inv, shoup_of(inv, qa));
+        }
+        dev.aux_P[0] = static_cast<u64>(Pq), dev.aux_P[1] = static_cast<u64>(Pq >> 64);
+        const u128 Ph = Pq >> 1;
+        dev.aux_Ph[0] = static_cast<u64>(Ph), dev.aux_Ph[1] = static_cast<u64>(Ph >> 64);
+        dev.aux_log2P = std::log2(static_cast<double>(ring.primes[1])) + std::log2(static_cast<double>(ring.primes[2])) +
+                        std::log2(static_cast<double>(ring.primes[3]));
+    }
     dev.n = static_cast<int>(ring.n);
     dev.logn = static_cast<int>(ring.logn);
     dev.limbs = static_cast<int>(ring.limbs);
@@ -387,6 +406,7 @@ Context::~Context() {
     for (cudaEvent_t e : prof.pool) cudaEventDestroy(e);
     s_ntt.reset();
     pk.reset();
+    aux_tab.reset();
     evk.reset();
     evk_sh.reset();
     evk_f.reset();
@@ -514,7 +534,21 @@ void keygen(Context& C, u64 seed) {
     fp_table(C.dev, C.evk.as<u64>(), C.evk_f.as<double>(), static_cast<int>(limbs), 2 * D, L);
     C.evk_digits = D;
     C.has_secret = C.has_pk = true;
+    C.build_aux_tables();
     C.sync();
+}
+
+void Context::build_aux_tables() {
+    aux_tab.reset();
+    dev.aux_tab = nullptr;
+    if (dev.aux_log2P <= 0.0 || !evk_digits || ring.logn < 10 || ring.logn > 14) return;
+    const std::size_t nn = n(), rows = 2 * evk_digits;
+    aux_tab = DevBuf(this, rows * 4 * nn * sizeof(double));
+    DevBuf tmp(this, rows * 5 * nn * sizeof(u64));
+    keyswitch_aux_tables(dev, evk.as<u64>(), top() + 1, static_cast<int>(evk_digits), aux_tab.as<double>(),
+                         tmp.as<u64>(), L());
+    dev.aux_tab = aux_tab.as<double>();
+    sync();
 }
 
 void import_keys(Context& C, const u64* secret, const u64* pk_b, const u64* pk_a, const u64* evk, std::size_t digits) {
@@ -540,6 +574,7 @@ void import_keys(Context& C, const u64* secret, const u64* pk_b, const u64* pk_a
         C.evk_f = DevBuf(&C, digits * 2 * poly * sizeof(double));
         fp_table(C.dev, C.evk.as<u64>(), C.evk_f.as<double>(), static_cast<int>(C.top() + 1), 2 * digits, L);
         C.evk_digits = digits;
+        C.build_aux_tables();
     }
     C.sync();
 }
@@ -571,8 +606,9 @@ void key_switch_raw(Context& C, const u64* d2, u64* out, std::size_t level, std:
     cuda_check(cudaMemcpyAsync(tmp.get(), d2, count * limbs * n * sizeof(u64), cudaMemcpyDeviceToDevice, C.stream), "copy");
     crt_digits(C.dev, tmp.as<u64>(), dig.as<u32>(), static_cast<int>(level), static_cast<int>(D), count, L);
     cuda_check(cudaMemsetAsync(out, 0, count * 2 * limbs * n * sizeof(u64), C.stream), "memset");
+    DevBuf aux(&C, keyswitch_aux_ok(C.dev, static_cast<int>(level), static_cast<int>(D)) ? count * 10 * n * 8 : 0);
     keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), C.evk_f.as<double>(), out,
-                  static_cast<int>(level), static_cast<int>(D), count, L);
+                  static_cast<int>(level), static_cast<int>(D), count, L, 0, nullptr, aux.as<u64>());
 }
 
 // mul / square (ckks.hpp:315-369): tensor -> INTT(d2) -> key switch -> INTT -> rescale.
@@ -596,10 +632,12 @@ static TensorPtr relin_product(Context& C, const Tensor& x, const Tensor* y) {
     out->shape = x.shape;
     out->batch = x.batch;
     const std::size_t cw = 2 * limbs * n;
-    const std::size_t per_ct = (sq ? 1 : 2) * cw * 8 + limbs * n * 8 + D * n * 4;
+    const bool aux = keyswitch_aux_ok(C.dev, static_cast<int>(l), static_cast<int>(D));
+    const std::size_t aux_words = aux ? 10 * n : 0;  // limb 0 via limbs 1..3: [2][4][n] + [2][n]
+    const std::size_t per_ct = (sq ? 1 : 2) * cw * 8 + limbs * n * 8 + D * n * 4 + aux_words * 8;
     const std::size_t chunk = std::max<std::size_t>(1, std::min(x.cells, kScratchBytes / per_ct));
     DevBuf d01(&C, chunk * cw * 8), fy(&C, sq ? 0 : chunk * cw * 8), d2(&C, chunk * limbs * n * 8),
-        dig(&C, chunk * D * n * 4);
+        dig(&C, chunk * D * n * 4), auxs(&C, chunk * aux_words * 8);
     Launch L = C.L();
     const int lv = static_cast<int>(l);
     for (std::size_t c0 = 0; c0 < x.cells; c0 += chunk) {
@@ -612,7 +650,8 @@ static TensorPtr relin_product(Context& C, const Tensor& x, const Tensor* y) {
         ntt_inverse_product(C.dev, d01.as<u64>(), fyp, d2.as<u64>(), lv, m, L);
         crt_digits(C.dev, d2.as<u64>(), dig.as<u32>(), lv, static_cast<int>(D), m, L);
         keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), C.evk_f.as<double>(),
-                      d01.as<u64>(), lv, static_cast<int>(D), m, L, sq ? 1 : 2, sq ? nullptr : fy.as<u64>());
+                      d01.as<u64>(), lv, static_cast<int>(D), m, L, sq ? 1 : 2, sq ? nullptr : fy.as<u64>(),
+                      aux ? auxs.as<u64>() : nullptr);
         if (!ntt_inverse_rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L)) {
             ntt_inverse(C.dev, d01.as<u64>(), lv, 2 * m, L);
             rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L);

@@ -99,6 +99,8 @@ struct Context {
     // keys (device resident; the secret also kept on the host for export)
     std::vector<u64> secret_host;  // [(L+1)][n] coefficient domain
     DevBuf s_ntt, pk, evk, evk_sh, evk_f;
+    DevBuf aux_tab;  // limb 0's key switch through limbs 1..3 (keyswitch.cu), when the chain allows it
+    void build_aux_tables();
     std::size_t evk_digits = 0;
     bool has_secret = false, has_pk = false;
     unsigned long long launches = 0;

@@ -37,6 +37,14 @@ struct DevRing {
     const ulonglong2* ks_tw = nullptr;       // [limbs][n]
     const double* ks_tw_f = nullptr;         // [limbs][n]
     unsigned long long int_limbs = 0;        // bit i: q_i >= 2^42 (integer-pipe path), for i < 64
+    // Key switch of the 60-bit limb 0 through limbs 1..3 (keyswitch.cu, "aux"):
+    // aux_tab [Dtop][2][4][n] = NTT_{q_s}(INTT_{q0}(evk[t][c][0]) mod q_s) as
+    // doubles in slots s = 1..3; CRT constants of P = q1 q2 q3.
+    const double* aux_tab = nullptr;
+    u64 aux_M[3][2] = {};                    // P / q_s, 128-bit (lo, hi)
+    ulonglong2 aux_inv[3] = {};              // ((P / q_s) mod q_s)^-1 mod q_s, Shoup
+    u64 aux_P[2] = {}, aux_Ph[2] = {};       // P and floor(P / 2)
+    double aux_log2P = 0.0;
     bool small_primes = false;               // some q_i <= 2^20: key-switch digits need v mod q_i
 };
 
@@ -96,6 +104,10 @@ void ntt_inverse(const DevRing& R, u64* polys, int level, std::size_t count, con
 // out = rescale(INTT(d)) for `groups` polys of level+1 limbs (d is overwritten); false (nothing
 // launched) when the ring needs a column pass (N > 2^14): call ntt_inverse + rescale instead
 bool ntt_inverse_rescale(const DevRing& R, u64* d, u64* out, int level, std::size_t groups, const Launch& L);
+// in-place inverse NTT (with n^-1, canonical) of limbs [limb0, limb0 + nsel) of
+// `groups` groups of `limbs` polys [groups][limbs][n] (N <= 2^14)
+void ntt_inverse_limbs(const DevRing& R, u64* data, int limbs, int limb0, int nsel, std::size_t groups, const Launch& L,
+                       const char* name = nullptr);
 // d2 = INTT(x1 * y1): x, y forward-transformed ciphertexts [count][2][level+1][n] (y may equal
 // x), the product formed in the first butterfly round; d2 [count][level+1][n] coefficients
 void ntt_inverse_product(const DevRing& R, const u64* x, const u64* y, u64* d2, int level, std::size_t count,
@@ -150,9 +162,18 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
 //   evk_f: FP64-path copy (used for limbs with q < 2^42)
 //   mode 0: acc01 holds (d0, d1); mode 1: acc01 holds NTT(x) and d0 = x0^2, d1 = 2 x0 x1 are
 //   formed in the epilogue; mode 2: likewise d0 = x0 y0, d1 = x0 y1 + x1 y0 with fy = NTT(y)
+// aux_scratch: optional [count][(2 x 4 + 2) n] words; when given and the
+// chain allows it, limb 0's key switch runs through limbs 1..3 (exact CRT)
+// instead of on the integer pipes
 void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
                    u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode = 0,
-                   const u64* fy = nullptr);
+                   const u64* fy = nullptr, u64* aux_scratch = nullptr);
+// the limb-0-through-limbs-1..3 key switch is usable at this level / digit count
+bool keyswitch_aux_ok(const DevRing& R, int level, int D);
+// aux_tab of DevRing from the evaluation key (one-time, at keygen / key import):
+// out [Dtop][2][4][n] doubles; tmp scratch [2 Dtop][5 n] words
+void keyswitch_aux_tables(const DevRing& R, const u64* evk, std::size_t evk_limbs, int Dtop, double* out, u64* tmp,
+                          const Launch& L);
 
 // Integer-pipe peak probe: chained Shoup modmuls (the NTT butterfly's
 // multiply), `iters` per thread over the whole GPU; returns modmuls issued.

@@ -294,7 +294,7 @@ __device__ __forceinline__ double column_value_fp(const u32* __restrict__ dig, c
 // mbarriers and walks work items (ciphertext, limb, block) with a grid
 // stride, so one item's epilogue overlaps the next item's first round on
 // other warps and the per-CTA setup is paid once.
-template <int LOGN, int LOGB, int LOGE, int T, bool FP>
+template <int LOGN, int LOGB, int LOGE, int T, bool FP, bool AUXK = false>
 struct KsShape {
     static constexpr int B = 1 << LOGB, C = LOGN - LOGB;
     static constexpr int SL = ntt::last_round_start(LOGB, LOGE);
@@ -314,7 +314,9 @@ struct KsShape {
     // memory as well (its 16-byte Shoup twiddles leave no shared memory to stage evk)
     static constexpr bool TMI = !FP && PRIV && HECNN_KS_TMEM && EL == 4;
     static constexpr bool USE_TMEM = TM || TMI;
-    static constexpr int TCW = 2 * PL * EL;  // tensor-memory columns per thread
+    // tensor-memory columns per thread: c1, plus (AUXK) limb 0's two
+    // accumulators mod q_s in the aux limbs 1..3
+    static constexpr int TCW = (AUXK ? 6 : 2) * PL * EL;
     static constexpr int TNEED = (T / 128) * TCW;
     static constexpr int TCOLS = TNEED <= 32 ? 32 : (TNEED <= 64 ? 64 : (TNEED <= 128 ? 128 : (TNEED <= 256 ? 256 : 512)));
     static_assert(!USE_TMEM || TNEED <= 512, "key switch: tensor-memory accumulators exceed the 512 TMEM columns");
@@ -330,15 +332,16 @@ struct KsShape {
 
 // Shared-memory map (dynamic): data [B] words | twiddle table [B] TW | FP:
 // c1 accumulators or b_t stage [B] doubles | 2 mbarriers (b_t, twiddles).
-template <int LOGN, int LOGB, int LOGE, int T, bool LIFT, class A, class KeyAt>
+template <int LOGN, int LOGB, int LOGE, int T, bool LIFT, bool AUXK, class A, class KeyAt>
 __device__ __forceinline__ void ks_item(const DevRing& R, const A& ar, const typename A::TW* tw_block,
                                         bool load_tw, const u32* digits, KeyAt key, u64* acc01, int level, int D,
                                         long long ct, int i, int b, u64 q, int mode, const u64* fy, uint32_t tm_lane,
-                                        unsigned& bphase, unsigned& tphase) {
+                                        unsigned& bphase, unsigned& tphase, int aux_slot, const double* aux_tab,
+                                        u64* aux_out) {
     using V = typename A::V;
     using TW = typename A::TW;
     constexpr bool FP = std::is_same<V, double>::value;
-    using S = KsShape<LOGN, LOGB, LOGE, T, FP>;
+    using S = KsShape<LOGN, LOGB, LOGE, T, FP, AUXK>;
     constexpr int B = S::B, C = S::C, EL = S::EL, PL = S::PL, UL = S::UL, E0 = S::E0, U0 = S::U0, P0 = S::P0;
     constexpr int STR0 = S::STR0;
     constexpr bool PRIV = S::PRIV, TM = S::TM, TMI = S::TMI, USE_TMEM = S::USE_TMEM, PREFETCH = S::PREFETCH;
@@ -423,8 +426,15 @@ __device__ __forceinline__ void ks_item(const DevRing& R, const A& ar, const typ
                                               const int base = idx - (EL - 1);
                                               if constexpr (TM) {
                                                   ntt::mbar_wait(bbar, par);  // b_t landed
-                                                  key.template unit_tm<EL>(t, blk_off + base, stash, a0 + uu * EL,
-                                                                           sacc + base, tm_lane + uu * 2 * EL);
+                                                  if (AUXK && aux_slot >= 0)
+                                                      key.template unit_tm_aux<EL>(
+                                                          t, blk_off + base, stash, a0 + uu * EL, sacc + base,
+                                                          tm_lane + uu * 2 * EL, tm_lane + (2 * PL + 4 * uu) * EL,
+                                                          aux_tab + (8LL * t + aux_slot) * n,       // [t][b][slot]
+                                                          aux_tab + (8LL * t + 4 + aux_slot) * n);  // [t][a][slot]
+                                                  else
+                                                      key.template unit_tm<EL>(t, blk_off + base, stash, a0 + uu * EL,
+                                                                               sacc + base, tm_lane + uu * 2 * EL);
                                               } else if constexpr (FP) {
                                                   key.template unit<EL>(t, blk_off + base, stash, a0 + uu * EL,
                                                                         [&](int kk) -> double& { return sacc[slot(base + kk, uu, kk)]; });
@@ -530,6 +540,54 @@ __device__ __forceinline__ void ks_item(const DevRing& R, const A& ar, const typ
             *reinterpret_cast<ulonglong2*>(o1 + idx) = make_ulonglong2(add_mod(b1[0], r1[0], q), add_mod(b1[1], r1[1], q));
         }
     }
+    if constexpr (AUXK && TM && C == 0) {
+        if (aux_slot >= 0) {
+            // limb 0's accumulators mod q_s, inverse-transformed in this CTA (the
+            // whole polynomial is its block): coefficients of E mod q_s straight to
+            // aux_out [ct][comp][4][n] slot s
+            double* sd = reinterpret_cast<double*>(smem);
+            const double ni = R.n_inv_f[i];
+            for (int comp = 0; comp < 2; ++comp) {
+                __syncthreads();  // the data region is free (digit loop / previous transform done)
+#pragma unroll
+                for (int uu = 0; uu < PL; ++uu) {
+                    const int base = ntt::fwd_last_base<LOGB, LOGE, T>(uu);
+                    double e[EL];
+                    tmem_ld_d<EL>(tm_lane + (2 * PL + 4 * uu + 2 * comp) * EL, e);
+#pragma unroll
+                    for (int k = 0; k < EL; ++k) sd[ntt::swz(base + k)] = ntt::fcentre(e[k], ar.q, ar.qinv);
+                }
+                __syncthreads();
+                u64* z = aux_out + ((ct * 2 + comp) * 4 + aux_slot) * n;
+                const ntt::FpArith far{ar.q, ar.qinv};
+                ntt::inv_block<LOGB, LOGE, T>(
+                    sd, far, R.inv_f + (static_cast<long long>(i) << LOGN), 0, 0,
+                    [=](int idx) { return sd[ntt::swz(idx)]; },
+                    [=](int idx, double v, int, int) { z[idx] = ntt::fcanon(ntt::fmodmul(v, ni, far.q, far.qinv), far.q, far.qinv); });
+            }
+        }
+    } else if constexpr (AUXK && TM) {
+        if (aux_slot >= 0) {
+            // limb 0's accumulators mod q_s (NTT domain of limb s) -> aux_out
+            // [ct][comp][4][n] slot s; ntt_inverse_limbs + k_aux_crt take them from there
+#pragma unroll
+            for (int uu = 0; uu < PL; ++uu) {
+                const int base = ntt::fwd_last_base<LOGB, LOGE, T>(uu);
+                double e0[EL], e1[EL];
+                tmem_ld_d<EL>(tm_lane + (2 * PL + 4 * uu) * EL, e0);
+                tmem_ld_d<EL>(tm_lane + (2 * PL + 4 * uu + 2) * EL, e1);
+                u64* z0 = aux_out + ((ct * 2) * 4 + aux_slot) * n + blk_off + base;
+                u64* z1 = aux_out + ((ct * 2 + 1) * 4 + aux_slot) * n + blk_off + base;
+#pragma unroll
+                for (int k = 0; k < EL; k += 2) {
+                    *reinterpret_cast<ulonglong2*>(z0 + k) =
+                        make_ulonglong2(ntt::fcanon(e0[k], ar.q, ar.qinv), ntt::fcanon(e0[k + 1], ar.q, ar.qinv));
+                    *reinterpret_cast<ulonglong2*>(z1 + k) =
+                        make_ulonglong2(ntt::fcanon(e1[k], ar.q, ar.qinv), ntt::fcanon(e1[k + 1], ar.q, ar.qinv));
+                }
+            }
+        }
+    }
     if constexpr (!USE_TMEM && FP) __syncthreads();  // c1 slots are re-zeroed by the next item
 }
 
@@ -554,6 +612,32 @@ struct FpKey {
             s1(2 * k) += ntt::fmodmul(v[2 * k], wa[k].x, q, qinv);
             s1(2 * k + 1) += ntt::fmodmul(v[2 * k + 1], wa[k].y, q, qinv);
         }
+    }
+    // unit_tm plus limb 0's key switch mod q_s (aux): e0 += v * Tb, e1 += v * Ta
+    // with Tb / Ta = NTT_{q_s}(INTT_{q0}(b_t / a_t of limb 0)), in two more
+    // tensor-memory column groups
+    template <int EL>
+    __device__ __forceinline__ void unit_tm_aux(int t, long long pos, const double* v, double* s0, const double* bst,
+                                                uint32_t tcol, uint32_t acol, const double* aux_b,
+                                                const double* aux_a) const {
+        unit_tm<EL>(t, pos, v, s0, bst, tcol);
+        const double2* xb = reinterpret_cast<const double2*>(aux_b + pos);
+        const double2* xa = reinterpret_cast<const double2*>(aux_a + pos);
+        double2 wb[EL / 2], wa[EL / 2];
+#pragma unroll
+        for (int k = 0; k < EL / 2; ++k) wb[k] = __ldg(xb + k), wa[k] = __ldg(xa + k);
+        double e0[EL], e1[EL];
+        tmem_ld_d<EL>(acol, e0);
+        tmem_ld_d<EL>(acol + 2 * EL, e1);
+#pragma unroll
+        for (int k = 0; k < EL / 2; ++k) {
+            e0[2 * k] += ntt::fmodmul(v[2 * k], wb[k].x, q, qinv);
+            e0[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], wb[k].y, q, qinv);
+            e1[2 * k] += ntt::fmodmul(v[2 * k], wa[k].x, q, qinv);
+            e1[2 * k + 1] += ntt::fmodmul(v[2 * k + 1], wa[k].y, q, qinv);
+        }
+        tmem_st_d<EL>(acol, e0);
+        tmem_st_d<EL>(acol + 2 * EL, e1);
     }
     // b_t from the shared-memory stage, a_t from L2, c1 read-modify-written in
     // this thread's tensor-memory columns
@@ -625,11 +709,11 @@ struct IntKey {
 // (ciphertext-major, so the CTAs in flight share the ciphertexts' digits in
 // L2). A limb range may cover limbs of the other kind (mixed chains); those
 // items are skipped.
-template <int LOGN, int LOGB, int LOGE, int T, bool FPK, bool LIFT>
+template <int LOGN, int LOGB, int LOGE, int T, bool FPK, bool LIFT, bool AUXK>
 __device__ __forceinline__ void ks_walk(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh,
                                         const double* evk_f, u64* acc01, int level, int D, int limb0, int nsel,
                                         long long items, long long first, long long stride, int mode, const u64* fy,
-                                        uint32_t tm_lane, unsigned& bphase, unsigned& tphase) {
+                                        uint32_t tm_lane, unsigned& bphase, unsigned& tphase, u64* aux_out) {
     constexpr int C = LOGN - LOGB;
     const long long n = 1LL << LOGN;
     const long long key_stride = static_cast<long long>(R.limbs) * n;  // one evk polynomial
@@ -648,29 +732,30 @@ __device__ __forceinline__ void ks_walk(const DevRing& R, const u32* digits, con
         if constexpr (FPK) {
             const ntt::FpArith ar{static_cast<double>(q), R.inv_q[i]};
             const FpKey key{evk_f, key_stride, ioff, ar.q, ar.qinv};
-            ks_item<LOGN, LOGB, LOGE, T, LIFT>(R, ar, R.ks_tw_f + ioff + (static_cast<long long>(b) << LOGB), load_tw,
-                                               digits, key, acc01, level, D, ct, i, b, q, mode, fy, tm_lane, bphase,
-                                               tphase);
+            const int aux_slot = AUXK && aux_out && i >= 1 && i <= 3 ? i : -1;
+            ks_item<LOGN, LOGB, LOGE, T, LIFT, AUXK>(R, ar, R.ks_tw_f + ioff + (static_cast<long long>(b) << LOGB),
+                                                     load_tw, digits, key, acc01, level, D, ct, i, b, q, mode, fy,
+                                                     tm_lane, bphase, tphase, aux_slot, R.aux_tab, aux_out);
         } else {
             // primes >= 2^42 only: digits < 2^20 < q are residues already
             const ntt::IntArith ar{q, q << 1};
             const IntKey key{evk, evk_sh, key_stride, ioff, q, q << 1};
-            ks_item<LOGN, LOGB, LOGE, T, false>(R, ar, R.ks_tw + ioff + (static_cast<long long>(b) << LOGB), load_tw,
-                                                digits, key, acc01, level, D, ct, i, b, q, mode, fy, tm_lane, bphase,
-                                                tphase);
+            ks_item<LOGN, LOGB, LOGE, T, false, AUXK>(R, ar, R.ks_tw + ioff + (static_cast<long long>(b) << LOGB),
+                                                      load_tw, digits, key, acc01, level, D, ct, i, b, q, mode, fy,
+                                                      tm_lane, bphase, tphase, -1, nullptr, nullptr);
         }
     }
 }
 
-template <int LOGN, int LOGB, int LOGE, int T, int MINB, bool LIFT>
+template <int LOGN, int LOGB, int LOGE, int T, int MINB, bool LIFT, bool AUXK>
 __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __restrict__ digits, const u64* __restrict__ evk,
                                                  const u64* __restrict__ evk_sh, const double* __restrict__ evk_f,
                                                  u64* __restrict__ acc01, int level, int D, int fp0, int nfp,
                                                  long long items_fp, int int0, int nint, long long items_int, int g_int,
-                                                 int mode, const u64* __restrict__ fy) {
+                                                 int mode, const u64* __restrict__ fy, u64* __restrict__ aux_out) {
     constexpr int B = 1 << LOGB;
-    using SF = KsShape<LOGN, LOGB, LOGE, T, true>;
-    using SI = KsShape<LOGN, LOGB, LOGE, T, false>;
+    using SF = KsShape<LOGN, LOGB, LOGE, T, true, AUXK>;
+    using SI = KsShape<LOGN, LOGB, LOGE, T, false, AUXK>;
     static_assert(SF::USE_TMEM == SI::USE_TMEM && SF::TCW == SI::TCW, "both limb kinds share the TMEM layout");
     extern __shared__ u64 smem[];
     uint64_t* bbar = reinterpret_cast<uint64_t*>(smem + 3 * B);
@@ -698,12 +783,13 @@ __global__ void __launch_bounds__(T, MINB) k_keyswitch(DevRing R, const u32* __r
     }
     unsigned bphase = 0, tphase = 0;
     if (static_cast<int>(blockIdx.x) < g_int)
-        ks_walk<LOGN, LOGB, LOGE, T, false, false>(R, digits, evk, evk_sh, evk_f, acc01, level, D, int0, nint, items_int,
-                                                   blockIdx.x, g_int, mode, fy, tm_lane, bphase, tphase);
+        ks_walk<LOGN, LOGB, LOGE, T, false, false, AUXK>(R, digits, evk, evk_sh, evk_f, acc01, level, D, int0, nint,
+                                                         items_int, blockIdx.x, g_int, mode, fy, tm_lane, bphase, tphase,
+                                                         nullptr);
     else
-        ks_walk<LOGN, LOGB, LOGE, T, true, LIFT>(R, digits, evk, evk_sh, evk_f, acc01, level, D, fp0, nfp, items_fp,
-                                                 blockIdx.x - g_int, gridDim.x - g_int, mode, fy, tm_lane, bphase,
-                                                 tphase);
+        ks_walk<LOGN, LOGB, LOGE, T, true, LIFT, AUXK>(R, digits, evk, evk_sh, evk_f, acc01, level, D, fp0, nfp,
+                                                       items_fp, blockIdx.x - g_int, gridDim.x - g_int, mode, fy,
+                                                       tm_lane, bphase, tphase, aux_out);
     if constexpr (SF::USE_TMEM) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
@@ -742,25 +828,139 @@ struct KsPlan {
     static constexpr int MINB = T >= 256 ? HECNN_KS_MINB : 1;
 };
 
+// ---- limb 0 through limbs 1..3 ("aux") --------------------------------------
+// The reference's limb-0 accumulators are sum_t NTT_q0(d_t) (.) b_{t,0} =
+// NTT_q0(E mod q0) with E = sum_t d_t (*) B_t the exact negacyclic integer
+// convolution of the digits with B_t = INTT_q0(b_{t,0}) in [0, q0) (likewise
+// for a). |E| < D N 2^20 q0 < P/2 for P = q1 q2 q3, so E is recovered exactly
+// from E mod q_s, s = 1..3 -- which the FP64 items of limbs 1..3 accumulate
+// beside their own key switch from the digit transforms they already compute
+// (Tb / Ta = NTT_{q_s}(B_t mod q_s), DevRing::aux_tab) -- by an inverse NTT in
+// each limb, a 3-prime CRT and a forward NTT mod q0. The 60-bit limb's D
+// integer-pipe digit NTTs disappear; every word stays the reference's.
+
+// E mod q_s (s = 1..3, canonical) -> centred E mod q0
+__device__ __forceinline__ u64 aux_crt_value(const DevRing& R, const u64 (&res)[3]) {
+    u64 lo = 0, hi = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const ModConst m = R.mod[1 + a];
+        const u64 r = res[a];
+        const u64 y = mul_shoup(r, R.aux_inv[a].x, R.aux_inv[a].y, m.q);  // < q_s < 2^42
+        // += y * M_a (M_a < 2^84): 128-bit multiply-add
+        const u64 p_lo = y * R.aux_M[a][0], p_hi = mulhi(y, R.aux_M[a][0]) + y * R.aux_M[a][1];
+        const u64 s = lo + p_lo;
+        hi += p_hi + (s < lo ? 1 : 0);
+        lo = s;
+    }
+    // X < 3P: reduce to [0, P)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const bool ge = hi > R.aux_P[1] || (hi == R.aux_P[1] && lo >= R.aux_P[0]);
+        if (ge) {
+            const u64 nlo = lo - R.aux_P[0];
+            hi = hi - R.aux_P[1] - (lo < R.aux_P[0] ? 1 : 0);
+            lo = nlo;
+        }
+    }
+    const ModConst m0 = R.mod[0];
+    if (hi < R.aux_Ph[1] || (hi == R.aux_Ph[1] && lo <= R.aux_Ph[0])) return reduce128(lo, hi, m0);  // E = X >= 0
+    // E = X - P < 0: -(P - X) mod q0
+    const u64 dlo = R.aux_P[0] - lo, dhi = R.aux_P[1] - hi - (R.aux_P[0] < lo ? 1 : 0);
+    const u64 v = reduce128(dlo, dhi, m0);
+    return v ? m0.q - v : 0;
+}
+
+// CRT of each coefficient fused into the first round of the forward NTT mod
+// q0: e0 [ct * 2 + comp][n] = NTT_q0(E mod q0); one CTA per polynomial (N <= 2^14)
+template <int LOGN, int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_aux_crt_ntt(DevRing R, const u64* __restrict__ aux_out, u64* __restrict__ e0) {
+    extern __shared__ u64 smem[];
+    const long long row = blockIdx.x;  // ct * 2 + comp
+    const long long n = 1LL << LOGN;
+    const u64* a1 = aux_out + (row * 4 + 1) * n;
+    u64* g = e0 + row * n;
+    const u64 q = R.mod[0].q;
+    const ntt::IntArith ar{q, q << 1};
+    ntt::fwd_block<LOGN, 3, T>(
+        smem, ar, R.fwd, 0, 0,
+        [=](int i) {
+            const u64 res[3] = {a1[i], a1[n + i], a1[2 * n + i]};
+            return aux_crt_value(R, res);
+        },
+        [=](int i, u64 v, int, int) { g[i] = reduce_4q(v, q); });
+}
+
+// limb 0 of acc01 (NTT domain): the tensor product's (d0, d1) (mode as in
+// keyswitch_mac) plus NTT_q0(E) of each component
+__global__ void k_limb0_combine(DevRing R, u64* __restrict__ acc01, const u64* __restrict__ e0, const u64* __restrict__ fy,
+                                int limbs, int mode, long long count) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= count * R.n) return;
+    const long long ct = t / R.n;
+    const int j = static_cast<int>(t % R.n);
+    const ModConst m = R.mod[0];
+    u64* o0 = acc01 + (ct * 2) * limbs * R.n + j;
+    u64* o1 = o0 + static_cast<long long>(limbs) * R.n;
+    const u64 xa = *o0, xb = *o1;
+    u64 b0, b1;
+    if (mode == 0) {
+        b0 = xa, b1 = xb;
+    } else if (mode == 1) {
+        b0 = mul_mod(xa, xa, m);
+        const u64 c = mul_mod(xa, xb, m);
+        b1 = add_mod(c, c, m.q);
+    } else {
+        const u64* y0 = fy + (ct * 2) * limbs * R.n + j;
+        const u64 va = y0[0], vb = y0[static_cast<long long>(limbs) * R.n];
+        b0 = mul_mod(xa, va, m);
+        b1 = add_mod(mul_mod(xa, vb, m), mul_mod(xb, va, m), m.q);
+    }
+    *o0 = add_mod(b0, e0[(ct * 2) * R.n + j], m.q);
+    *o1 = add_mod(b1, e0[(ct * 2 + 1) * R.n + j], m.q);
+}
+
+// aux_tab build: rows of B (coefficients mod q0) -> slot s of [rows][4][n] = B mod q_s
+__global__ void k_aux_rows(DevRing R, const u64* __restrict__ b, u64* __restrict__ w, long long rows) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= rows * R.n) return;
+    const long long row = t / R.n;
+    const int j = static_cast<int>(t % R.n);
+    const u64 v = b[row * R.n + j];
+    w[(row * 4) * R.n + j] = 0;
+#pragma unroll
+    for (int s = 1; s <= 3; ++s) w[(row * 4 + s) * R.n + j] = reduce128(v, 0, R.mod[s]);
+}
+
 template <int LOGN>
 void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
-                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy) {
+                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy,
+                   u64* aux_scratch) {
     using P = KsPlan<LOGN>;
 #ifdef HECNN_KS_FORCE_LIFT
     const bool lift = true;
 #else
     const bool lift = R.small_primes;
 #endif
-    auto kern = lift ? k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true>
-                     : k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false>;
+    const bool aux = aux_scratch && keyswitch_aux_ok(R, level, D);
+    auto pick = [&](bool lf, bool ax) {
+        if constexpr (LOGN >= 10 && LOGN <= 14 && KsShape<LOGN, P::LOGB, P::LOGE, P::T, true, true>::TM) {
+            if (ax)
+                return lf ? k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, true>
+                          : k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false, true>;
+        }
+        return lf ? k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true, false>
+                  : k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false, false>;
+    };
+    auto kern = pick(lift, aux);
     // data + staged twiddles (u64 Shoup pairs on the integer path; double
     // twiddles + the b_t stage or c1 accumulators on the FP64 path) + mbarriers
     const int smem = P::B * (8 + 16) + 64;
     static bool init = (smem > 48 * 1024
-                            ? (cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, true>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                               cudaFuncSetAttribute(k_keyswitch<LOGN, P::LOGB, P::LOGE, P::T, P::MINB, false>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                            ? (cudaFuncSetAttribute(pick(true, false), cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                               cudaFuncSetAttribute(pick(false, false), cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                               cudaFuncSetAttribute(pick(true, true), cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                               cudaFuncSetAttribute(pick(false, true), cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                                true)
                             : true);
     (void)init;
@@ -773,6 +973,7 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
     if (int_mask == 0) nint = 0;
     else if (int_mask == lmask) nfp = 0;
     else if (int_mask == 1) { fp0 = 1; nfp = limbs - 1; nint = 1; }
+    if (aux) nint = 0;  // limb 0 rides on limbs 1..3
     const double n = double(1 << LOGN), cl = double(count) * limbs;
     // per (ct, limb, digit): one N-point NTT + 2N MACs; bytes: evk once + digits + acc r/w
     L.begin("k_keyswitch", cl * D * (n / 2 * LOGN + 2 * n),
@@ -793,7 +994,7 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
 #endif
     const long long nb = 1LL << (LOGN - P::LOGB);
     const long long items_fp = static_cast<long long>(count) * nfp * nb, items_int = static_cast<long long>(count) * nint * nb;
-    const int n_int_limbs = __builtin_popcountll(int_mask);
+    const int n_int_limbs = nint ? __builtin_popcountll(int_mask) : 0;
     const double w_fp = double(count) * (limbs - n_int_limbs) * nb, w_int = double(count) * n_int_limbs * nb * HECNN_KS_INT_COST;
     const long long cap = static_cast<long long>(sms) * occ;
     long long g_int = 0, g_fp = 0;
@@ -808,11 +1009,36 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
         g_int = std::min(g_int, items_int);
         g_fp = std::min(g_fp, items_fp);
     }
+    u64* aux_out = aux ? aux_scratch : nullptr;
     kern<<<static_cast<unsigned>(g_int + g_fp), P::T, smem, L.stream>>>(R, digits, evk, evk_sh, evk_f, acc01, level, D, fp0,
                                                                        nfp, items_fp, int0, nint, items_int,
-                                                                       static_cast<int>(g_int), mode, fy);
-    const unsigned long long launched = 1;
-    L.count(launched);
+                                                                       static_cast<int>(g_int), mode, fy, aux_out);
+    L.count(1);
+    if (aux) {
+        // E mod q_s -> coefficients (limbs 1..3 of [ct][comp][4][n]), CRT -> E mod q0,
+        // NTT_q0, then limb 0 = d + NTT_q0(E)
+        u64* e0 = aux_scratch + count * 2 * 4 * (1ull << LOGN);
+        if constexpr (LOGN > P::LOGB) ntt_inverse_limbs(R, aux_scratch, 4, 1, 3, count * 2, L, "k_ks_aux_intt");
+        // (N <= 2^13: the key-switch CTAs of limbs 1..3 wrote coefficients already)
+        constexpr int TN = (1 << LOGN) / 8 >= 512 ? 512 : ((1 << LOGN) / 8 >= 32 ? (1 << LOGN) / 8 : 32);
+        constexpr int MB = LOGN <= 13 ? 2 : 1;
+        auto kc = k_aux_crt_ntt<LOGN, TN, MB>;
+        const int csm = (1 << LOGN) * 8;
+        static const bool cinit = [&] {
+            if (csm > 48 * 1024) cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, csm);
+            return true;
+        }();
+        (void)cinit;
+        const double cells = double(count) * 2 * (1 << LOGN);
+        L.begin("k_ks_aux_crt_ntt", cells * (LOGN / 2.0 + 6), 8.0 * cells * 4);
+        kc<<<static_cast<unsigned>(count * 2), TN, csm, L.stream>>>(R, aux_scratch, e0);
+        L.count();
+        const long long pos = static_cast<long long>(count) << LOGN;
+        L.begin("k_ks_aux_combine", double(pos) * 4, 8.0 * pos * 6);
+        k_limb0_combine<<<static_cast<unsigned>((pos + 255) / 256), 256, 0, L.stream>>>(R, acc01, e0, fy, limbs, mode,
+                                                                                      static_cast<long long>(count));
+        L.count();
+    }
 }
 
 }  // namespace
@@ -836,12 +1062,62 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
     check_launch("crt_digits");
 }
 
+namespace {
+// the FP64 key-switch items keep c1 in tensor memory at this ring degree (the
+// aux accumulators live beside it)
+template <int LOGN>
+constexpr bool aux_shape() {
+    using P = KsPlan<LOGN>;
+    return KsShape<LOGN, P::LOGB, P::LOGE, P::T, true, true>::TM;
+}
+bool aux_shape_ok(int logn) {
+    switch (logn) {
+        case 10: return aux_shape<10>();
+        case 11: return aux_shape<11>();
+        case 12: return aux_shape<12>();
+        case 13: return aux_shape<13>();
+        case 14: return aux_shape<14>();
+        default: return false;
+    }
+}
+}  // namespace
+
+bool keyswitch_aux_ok(const DevRing& R, int level, int D) {
+#ifndef HECNN_KS_AUX
+#define HECNN_KS_AUX 1
+#endif
+    if (!HECNN_KS_AUX || !R.aux_tab || level < 3 || !aux_shape_ok(R.logn)) return false;
+    const unsigned long long lmask = level + 1 >= 64 ? ~0ull : (1ull << (level + 1)) - 1;
+    if ((R.int_limbs & lmask) != 1) return false;  // the 60-bit limb 0 alone on the integer path
+    // |E| < D N 2^20 q0 must stay below P / 2 (one bit of margin)
+    const double bits = std::log2(double(D)) + R.logn + 20.0 + 61.0 + 2.0;
+    return bits < R.aux_log2P;
+}
+
+void keyswitch_aux_tables(const DevRing& R, const u64* evk, std::size_t evk_limbs, int Dtop, double* out, u64* tmp,
+                          const Launch& L) {
+    const std::size_t n = static_cast<std::size_t>(R.n), rows = 2 * static_cast<std::size_t>(Dtop);
+    // limb 0 of every evk polynomial, back to coefficients (INTT mod q0)
+    cuda_check(cudaMemcpy2DAsync(tmp, n * 8, evk, evk_limbs * n * 8, n * 8, rows, cudaMemcpyDeviceToDevice, L.stream),
+               "copy evk limb 0");
+    ntt_inverse(R, tmp, 0, rows, L);
+    // slots 1..3: B mod q_s, then NTT in each slot's limb, as exact doubles
+    u64* w = tmp + rows * n;
+    const long long cells = static_cast<long long>(rows * n);
+    k_aux_rows<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, L.stream>>>(R, tmp, w, static_cast<long long>(rows));
+    L.count();
+    ntt_forward(R, w, 3, rows, L);
+    fp_table(R, w, out, 4, rows, L);
+    check_launch("keyswitch_aux_tables");
+}
+
 void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
-                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy) {
+                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy,
+                   u64* aux_scratch) {
     if (!count) return;
     if (mode == 2 && !fy) throw std::invalid_argument("keyswitch_mac: product mode needs the second operand");
 #define HECNN_KS_CASE(LG) \
-    case LG: run_keyswitch<LG>(R, digits, evk, evk_sh, evk_f, acc01, level, D, count, L, mode, fy); break;
+    case LG: run_keyswitch<LG>(R, digits, evk, evk_sh, evk_f, acc01, level, D, count, L, mode, fy, aux_scratch); break;
     switch (R.logn) {
         HECNN_KS_CASE(3) HECNN_KS_CASE(4) HECNN_KS_CASE(5) HECNN_KS_CASE(6) HECNN_KS_CASE(7) HECNN_KS_CASE(8)
         HECNN_KS_CASE(9) HECNN_KS_CASE(10) HECNN_KS_CASE(11) HECNN_KS_CASE(12) HECNN_KS_CASE(13)

@@ -401,6 +401,41 @@ bool run_inverse_rescale(const DevRing& R, u64* d, u64* out, int limbs, std::siz
 }
 }  // namespace
 
+namespace {
+template <int LOGN>
+void run_inverse_limbs(const DevRing& R, u64* data, int limbs, int limb0, int nsel, std::size_t groups, const Launch& L,
+                       const char* name) {
+    using P = NttPlan<LOGN>;
+    if constexpr (P::C > 0) {
+        throw std::invalid_argument("ntt_inverse_limbs: ring degree above one block");
+    } else {
+        auto kern = k_ntt_inv_sel<LOGN, P::LOGE, P::THREADS, P::MINB, false>;
+        const int smem = (1 << LOGN) * 8;
+        static bool init = (set_smem(kern, smem), true);
+        (void)init;
+        const std::size_t polys = groups * static_cast<std::size_t>(nsel);
+        L.begin(name ? name : "k_ntt_inv_block", double(polys) * (1 << (LOGN - 1)) * LOGN, 16.0 * polys * (1 << LOGN));
+        kern<<<static_cast<unsigned>(polys), P::THREADS, smem, L.stream>>>(R, data, data, limbs, limb0, nsel);
+        L.count();
+    }
+}
+}  // namespace
+
+void ntt_inverse_limbs(const DevRing& R, u64* data, int limbs, int limb0, int nsel, std::size_t groups, const Launch& L,
+                       const char* name) {
+    if (!groups || nsel <= 0) return;
+#define HECNN_NTT_CASE(LG) \
+    case LG: run_inverse_limbs<LG>(R, data, limbs, limb0, nsel, groups, L, name); break;
+    switch (R.logn) {
+        HECNN_NTT_CASE(3) HECNN_NTT_CASE(4) HECNN_NTT_CASE(5) HECNN_NTT_CASE(6) HECNN_NTT_CASE(7)
+        HECNN_NTT_CASE(8) HECNN_NTT_CASE(9) HECNN_NTT_CASE(10) HECNN_NTT_CASE(11) HECNN_NTT_CASE(12)
+        HECNN_NTT_CASE(13) HECNN_NTT_CASE(14) HECNN_NTT_CASE(15) HECNN_NTT_CASE(16)
+        default: throw std::invalid_argument("ntt: ring degree outside 2^3..2^16 is not supported on the device");
+    }
+#undef HECNN_NTT_CASE
+    check_launch("ntt_inverse_limbs");
+}
+
 bool ntt_inverse_rescale(const DevRing& R, u64* d, u64* out, int level, std::size_t groups, const Launch& L) {
     if (level < 1 || !groups) return false;
     bool done = false;
