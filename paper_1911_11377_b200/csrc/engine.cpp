@@ -649,11 +649,13 @@ static TensorPtr relin_product(Context& C, const Tensor& x, const Tensor* y) {
         const u64* fyp = sq ? d01.as<u64>() : fy.as<u64>();
         ntt_inverse_product(C.dev, d01.as<u64>(), fyp, d2.as<u64>(), lv, m, L);
         crt_digits(C.dev, d2.as<u64>(), dig.as<u32>(), lv, static_cast<int>(D), m, L);
-        keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(), C.evk_f.as<double>(),
-                      d01.as<u64>(), lv, static_cast<int>(D), m, L, sq ? 1 : 2, sq ? nullptr : fy.as<u64>(),
-                      aux ? auxs.as<u64>() : nullptr);
-        if (!ntt_inverse_rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L)) {
+        // limb 0's E (aux path) stays in coefficients and joins after the INTT
+        const u64* e0 = keyswitch_mac(C.dev, dig.as<u32>(), C.evk.as<u64>(), C.evk_sh.as<u64>(),
+                                      C.evk_f.as<double>(), d01.as<u64>(), lv, static_cast<int>(D), m, L, sq ? 1 : 2,
+                                      sq ? nullptr : fy.as<u64>(), aux ? auxs.as<u64>() : nullptr, true);
+        if (!ntt_inverse_rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L, e0)) {
             ntt_inverse(C.dev, d01.as<u64>(), lv, 2 * m, L);
+            if (e0) add_limb0(C.dev, d01.as<u64>(), e0, lv + 1, 2 * m, L);
             rescale(C.dev, d01.as<u64>(), out->cell(c0), lv, 2 * m, L);
         }
     }

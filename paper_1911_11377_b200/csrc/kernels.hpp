@@ -102,8 +102,10 @@ void ntt_forward(const DevRing& R, u64* polys, int level, std::size_t count, con
 void ntt_forward_to(const DevRing& R, const u64* src, u64* dst, int level, std::size_t count, const Launch& L);
 void ntt_inverse(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L);
 // out = rescale(INTT(d)) for `groups` polys of level+1 limbs (d is overwritten); false (nothing
-// launched) when the ring needs a column pass (N > 2^14): call ntt_inverse + rescale instead
-bool ntt_inverse_rescale(const DevRing& R, u64* d, u64* out, int level, std::size_t groups, const Launch& L);
+// launched) when the ring needs a column pass (N > 2^14): call ntt_inverse + rescale instead.
+// add0 (optional, [groups][n] coefficients mod q0) is added to limb 0 after its INTT
+bool ntt_inverse_rescale(const DevRing& R, u64* d, u64* out, int level, std::size_t groups, const Launch& L,
+                         const u64* add0 = nullptr);
 // in-place inverse NTT (with n^-1, canonical) of limbs [limb0, limb0 + nsel) of
 // `groups` groups of `limbs` polys [groups][limbs][n] (N <= 2^14)
 void ntt_inverse_limbs(const DevRing& R, u64* data, int limbs, int limb0, int nsel, std::size_t groups, const Launch& L,
@@ -165,9 +167,15 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
 // aux_scratch: optional [count][(2 x 4 + 2) n] words; when given and the
 // chain allows it, limb 0's key switch runs through limbs 1..3 (exact CRT)
 // instead of on the integer pipes
-void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
-                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode = 0,
-                   const u64* fy = nullptr, u64* aux_scratch = nullptr);
+// defer_limb0: the caller inverse-transforms acc01 next, so limb 0's E is not
+// forward-transformed: the return value (non-null when deferred) holds E mod q0
+// as coefficients [count][2][n], to be added to limb 0 after that INTT
+// (ntt_inverse_rescale's add0, or add_limb0)
+const u64* keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
+                         u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode = 0,
+                         const u64* fy = nullptr, u64* aux_scratch = nullptr, bool defer_limb0 = false);
+// d [groups][limbs][n] (coefficients): limb 0 += add0 [groups][n] mod q0
+void add_limb0(const DevRing& R, u64* d, const u64* add0, int limbs, std::size_t groups, const Launch& L);
 // the limb-0-through-limbs-1..3 key switch is usable at this level / digit count
 bool keyswitch_aux_ok(const DevRing& R, int level, int D);
 // aux_tab of DevRing from the evaluation key (one-time, at keygen / key import):

@@ -920,6 +920,40 @@ __global__ void k_limb0_combine(DevRing R, u64* __restrict__ acc01, const u64* _
     *o1 = add_mod(b1, e0[(ct * 2 + 1) * R.n + j], m.q);
 }
 
+// deferred variant (the caller inverse-transforms acc01 next): limb 0 of
+// acc01 gets the tensor product's (d0, d1) only, and e0 [ct * 2 + comp][n]
+// receives E mod q0 as coefficients, to be added after the caller's INTT --
+// NTT_q0 followed by INTT_q0 of E cancels, so neither runs
+__global__ void k_limb0_crt_combine(DevRing R, u64* __restrict__ acc01, const u64* __restrict__ aux_out,
+                                    u64* __restrict__ e0, const u64* __restrict__ fy, int limbs, int mode,
+                                    long long count) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= count * R.n) return;
+    const long long ct = t / R.n, n = R.n;
+    const int j = static_cast<int>(t % R.n);
+#pragma unroll
+    for (int comp = 0; comp < 2; ++comp) {
+        const u64* a1 = aux_out + ((ct * 2 + comp) * 4 + 1) * n + j;
+        const u64 res[3] = {a1[0], a1[n], a1[2 * n]};
+        e0[(ct * 2 + comp) * n + j] = aux_crt_value(R, res);
+    }
+    if (mode == 0) return;
+    const ModConst m = R.mod[0];
+    u64* o0 = acc01 + (ct * 2) * limbs * n + j;
+    u64* o1 = o0 + static_cast<long long>(limbs) * n;
+    const u64 xa = *o0, xb = *o1;
+    if (mode == 1) {
+        *o0 = mul_mod(xa, xa, m);
+        const u64 c = mul_mod(xa, xb, m);
+        *o1 = add_mod(c, c, m.q);
+    } else {
+        const u64* y0 = fy + (ct * 2) * limbs * n + j;
+        const u64 va = y0[0], vb = y0[static_cast<long long>(limbs) * n];
+        *o0 = mul_mod(xa, va, m);
+        *o1 = add_mod(mul_mod(xa, vb, m), mul_mod(xb, va, m), m.q);
+    }
+}
+
 // aux_tab build: rows of B (coefficients mod q0) -> slot s of [rows][4][n] = B mod q_s
 __global__ void k_aux_rows(DevRing R, const u64* __restrict__ b, u64* __restrict__ w, long long rows) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -933,9 +967,9 @@ __global__ void k_aux_rows(DevRing R, const u64* __restrict__ b, u64* __restrict
 }
 
 template <int LOGN>
-void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
-                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy,
-                   u64* aux_scratch) {
+const u64* run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
+                         u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy,
+                         u64* aux_scratch, bool defer) {
     using P = KsPlan<LOGN>;
 #ifdef HECNN_KS_FORCE_LIFT
     const bool lift = true;
@@ -1020,6 +1054,14 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
         u64* e0 = aux_scratch + count * 2 * 4 * (1ull << LOGN);
         if constexpr (LOGN > P::LOGB) ntt_inverse_limbs(R, aux_scratch, 4, 1, 3, count * 2, L, "k_ks_aux_intt");
         // (N <= 2^13: the key-switch CTAs of limbs 1..3 wrote coefficients already)
+        const long long pos = static_cast<long long>(count) << LOGN;
+        if (defer) {
+            L.begin("k_ks_aux_crt", double(pos) * 2 * 12, 8.0 * pos * (6 + 2 + (mode ? 4 : 0) + (mode == 2 ? 2 : 0)));
+            k_limb0_crt_combine<<<static_cast<unsigned>((pos + 255) / 256), 256, 0, L.stream>>>(
+                R, acc01, aux_scratch, e0, fy, limbs, mode, static_cast<long long>(count));
+            L.count();
+            return e0;
+        }
         constexpr int TN = (1 << LOGN) / 8 >= 512 ? 512 : ((1 << LOGN) / 8 >= 32 ? (1 << LOGN) / 8 : 32);
         constexpr int MB = LOGN <= 13 ? 2 : 1;
         auto kc = k_aux_crt_ntt<LOGN, TN, MB>;
@@ -1033,12 +1075,12 @@ void run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, const u6
         L.begin("k_ks_aux_crt_ntt", cells * (LOGN / 2.0 + 6), 8.0 * cells * 4);
         kc<<<static_cast<unsigned>(count * 2), TN, csm, L.stream>>>(R, aux_scratch, e0);
         L.count();
-        const long long pos = static_cast<long long>(count) << LOGN;
         L.begin("k_ks_aux_combine", double(pos) * 4, 8.0 * pos * 6);
         k_limb0_combine<<<static_cast<unsigned>((pos + 255) / 256), 256, 0, L.stream>>>(R, acc01, e0, fy, limbs, mode,
                                                                                       static_cast<long long>(count));
         L.count();
     }
+    return nullptr;
 }
 
 }  // namespace
@@ -1111,13 +1153,14 @@ void keyswitch_aux_tables(const DevRing& R, const u64* evk, std::size_t evk_limb
     check_launch("keyswitch_aux_tables");
 }
 
-void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
-                   u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy,
-                   u64* aux_scratch) {
-    if (!count) return;
+const u64* keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u64* evk_sh, const double* evk_f,
+                         u64* acc01, int level, int D, std::size_t count, const Launch& L, int mode, const u64* fy,
+                         u64* aux_scratch, bool defer_limb0) {
+    if (!count) return nullptr;
+    const u64* e0 = nullptr;
     if (mode == 2 && !fy) throw std::invalid_argument("keyswitch_mac: product mode needs the second operand");
 #define HECNN_KS_CASE(LG) \
-    case LG: run_keyswitch<LG>(R, digits, evk, evk_sh, evk_f, acc01, level, D, count, L, mode, fy, aux_scratch); break;
+    case LG: e0 = run_keyswitch<LG>(R, digits, evk, evk_sh, evk_f, acc01, level, D, count, L, mode, fy, aux_scratch, defer_limb0); break;
     switch (R.logn) {
         HECNN_KS_CASE(3) HECNN_KS_CASE(4) HECNN_KS_CASE(5) HECNN_KS_CASE(6) HECNN_KS_CASE(7) HECNN_KS_CASE(8)
         HECNN_KS_CASE(9) HECNN_KS_CASE(10) HECNN_KS_CASE(11) HECNN_KS_CASE(12) HECNN_KS_CASE(13)
@@ -1126,6 +1169,26 @@ void keyswitch_mac(const DevRing& R, const u32* digits, const u64* evk, const u6
     }
 #undef HECNN_KS_CASE
     check_launch("keyswitch_mac");
+    return e0;
+}
+
+__global__ void k_add_limb0(DevRing R, u64* __restrict__ d, const u64* __restrict__ add0, int limbs, long long groups) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= groups * R.n) return;
+    const long long g = t / R.n;
+    const int j = static_cast<int>(t % R.n);
+    u64* p = d + g * limbs * R.n + j;
+    *p = add_mod(*p, add0[t], R.mod[0].q);
+}
+
+void add_limb0(const DevRing& R, u64* d, const u64* add0, int limbs, std::size_t groups, const Launch& L) {
+    if (!groups) return;
+    const long long cells = static_cast<long long>(groups) * R.n;
+    L.begin("k_ks_aux_add", double(cells), 24.0 * cells);
+    k_add_limb0<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, L.stream>>>(R, d, add0, limbs,
+                                                                               static_cast<long long>(groups));
+    L.count();
+    check_launch("add_limb0");
 }
 
 }  // namespace hecnn_b200

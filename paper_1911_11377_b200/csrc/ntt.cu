@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_block(DevRing R, u64*
 // previous launch (RESCALE = false, limb0 = L) transformed in place.
 template <int LOGN, int LOGE, int THREADS, int MINB, bool RESCALE>
 __global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_sel(DevRing R, u64* __restrict__ data, u64* __restrict__ out,
-                                                               int limbs, int limb0, int nsel) {
+                                                               int limbs, int limb0, int nsel,
+                                                               const u64* __restrict__ add0) {
     extern __shared__ u64 smem[];
     const long long cta = blockIdx.x;
     const long long grp = cta / nsel;
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_sel(DevRing R, u64* _
             u64 centred = reduce_near(vt, m);
             if (vt > (R.mod[L].q >> 1)) centred = sub_mod(centred, R.p_mod[L * R.limbs + limb], m.q);
             const ulonglong2 inv = R.inv_dropped[L * R.limbs + limb];
+            if (limb == 0 && add0) c = add_mod(c, add0[(grp << LOGN) + i], m.q);
             o[i] = mul_shoup(sub_mod(c, centred, m.q), inv.x, inv.y, m.q);
         } else {
             g[i] = c;
@@ -378,7 +380,8 @@ void ntt_inverse(const DevRing& R, u64* polys, int level, std::size_t count, con
 
 namespace {
 template <int LOGN>
-bool run_inverse_rescale(const DevRing& R, u64* d, u64* out, int limbs, std::size_t groups, const Launch& L) {
+bool run_inverse_rescale(const DevRing& R, u64* d, u64* out, int limbs, std::size_t groups, const Launch& L,
+                         const u64* add0) {
     using P = NttPlan<LOGN>;
     if constexpr (P::C > 0) {
         return false;
@@ -390,11 +393,11 @@ bool run_inverse_rescale(const DevRing& R, u64* d, u64* out, int limbs, std::siz
         (void)init;
         const double bfly = double(1 << (LOGN - 1)) * LOGN, nn = double(1 << LOGN);
         L.begin("k_ntt_inv_block", double(groups) * bfly, 16.0 * groups * nn);
-        ktop<<<static_cast<unsigned>(groups), P::THREADS, smem, L.stream>>>(R, d, out, limbs, limbs - 1, 1);
+        ktop<<<static_cast<unsigned>(groups), P::THREADS, smem, L.stream>>>(R, d, out, limbs, limbs - 1, 1, nullptr);
         L.count();
         const std::size_t polys = groups * static_cast<std::size_t>(limbs - 1);
         L.begin("k_ntt_inv_rescale", double(polys) * (bfly + 2 * nn), 8.0 * nn * (2.0 * polys + groups));
-        kres<<<static_cast<unsigned>(polys), P::THREADS, smem, L.stream>>>(R, d, out, limbs, 0, limbs - 1);
+        kres<<<static_cast<unsigned>(polys), P::THREADS, smem, L.stream>>>(R, d, out, limbs, 0, limbs - 1, add0);
         L.count();
         return true;
     }
@@ -415,7 +418,7 @@ void run_inverse_limbs(const DevRing& R, u64* data, int limbs, int limb0, int ns
         (void)init;
         const std::size_t polys = groups * static_cast<std::size_t>(nsel);
         L.begin(name ? name : "k_ntt_inv_block", double(polys) * (1 << (LOGN - 1)) * LOGN, 16.0 * polys * (1 << LOGN));
-        kern<<<static_cast<unsigned>(polys), P::THREADS, smem, L.stream>>>(R, data, data, limbs, limb0, nsel);
+        kern<<<static_cast<unsigned>(polys), P::THREADS, smem, L.stream>>>(R, data, data, limbs, limb0, nsel, nullptr);
         L.count();
     }
 }
@@ -436,11 +439,12 @@ void ntt_inverse_limbs(const DevRing& R, u64* data, int limbs, int limb0, int ns
     check_launch("ntt_inverse_limbs");
 }
 
-bool ntt_inverse_rescale(const DevRing& R, u64* d, u64* out, int level, std::size_t groups, const Launch& L) {
+bool ntt_inverse_rescale(const DevRing& R, u64* d, u64* out, int level, std::size_t groups, const Launch& L,
+                         const u64* add0) {
     if (level < 1 || !groups) return false;
     bool done = false;
 #define HECNN_NTT_CASE(LG) \
-    case LG: done = run_inverse_rescale<LG>(R, d, out, level + 1, groups, L); break;
+    case LG: done = run_inverse_rescale<LG>(R, d, out, level + 1, groups, L, add0); break;
     switch (R.logn) {
         HECNN_NTT_CASE(3) HECNN_NTT_CASE(4) HECNN_NTT_CASE(5) HECNN_NTT_CASE(6) HECNN_NTT_CASE(7)
         HECNN_NTT_CASE(8) HECNN_NTT_CASE(9) HECNN_NTT_CASE(10) HECNN_NTT_CASE(11) HECNN_NTT_CASE(12)
