@@ -765,11 +765,31 @@ static TensorPtr eval_activation_cells(Context& C, const Activation& act, const 
     };
     const double target = C.scale;
     std::vector<TensorPtr> terms;
+    // degree 2: the linear term c1 x is not stored -- its mul_plain + rescale
+    // runs inside the final fused kernel (SumTerms::rs), read straight from x
+    DevBuf lazy_c;
+    bool lazy = false;
+    double lazy_scale = 0.0;
     for (std::size_t k = 1; k < d; ++k) {
         const Tensor& p = power(k);
         double u = target * static_cast<double>(C.ring.primes[p.level]) / p.scale;
+        if (k == 1 && d == 2) {
+            lazy_c = mul_const_table(C, p, act.coefficients[k], u);  // the same checks, in order
+            lazy_scale = p.scale * u / static_cast<double>(C.ring.primes[p.level]);
+            lazy = true;
+            continue;
+        }
         terms.push_back(ct_mul_const(C, p, act.coefficients[k], u));
     }
+    auto materialize_lazy = [&] {
+        if (!lazy) return;
+        TensorPtr t = make_tensor(C, x.cells, x.level - 1, lazy_scale);
+        t->shape = x.shape;
+        t->batch = x.batch;
+        rescale(C.dev, x.data(), t->data(), static_cast<int>(x.level), 2 * x.cells, C.L(), lazy_c.as<ulonglong2>());
+        terms.insert(terms.begin(), std::move(t));
+        lazy = false;
+    };
     {
         // The last term (the highest power, lowest level) is rescaled with the
         // other terms and the constant added on the way out when its level is
@@ -779,13 +799,23 @@ static TensorPtr eval_activation_cells(Context& C, const Activation& act, const 
         const std::uint32_t lvl = p.level - (p.level ? 1 : 0);
         bool fuse = p.level > 0 && terms.size() + 1 <= static_cast<std::size_t>(kMaxTerms);
         for (auto& t : terms) fuse = fuse && t->level >= lvl;
+        if (lazy && !(fuse && x.level - 1 >= lvl)) materialize_lazy();
         if (fuse) {
             DevBuf dc = mul_const_table(C, p, act.coefficients[d], u);
             const double sc = p.scale * u / static_cast<double>(C.ring.primes[p.level]);
-            const double s0 = terms.empty() ? sc : terms[0]->scale;
-            for (std::size_t i = 1; i < terms.size(); ++i) require_scale_match(s0, terms[i]->scale, "add");
-            if (!terms.empty()) require_scale_match(s0, sc, "add");
+            // the terms in the reference's order: [c1 x (lazy)], materialized terms, c_d x^d
+            std::vector<double> scales;
+            if (lazy) scales.push_back(lazy_scale);
+            for (auto& t : terms) scales.push_back(t->scale);
+            const double s0 = scales.empty() ? sc : scales[0];
+            for (std::size_t i = 1; i < scales.size(); ++i) require_scale_match(s0, scales[i], "add");
+            if (!scales.empty()) require_scale_match(s0, sc, "add");
             SumTerms st{};
+            if (lazy) {
+                st.rs = x.data();
+                st.rs_level = static_cast<int>(x.level);
+                st.rs_c = lazy_c.as<ulonglong2>();
+            }
             st.count = static_cast<int>(terms.size());
             for (std::size_t i = 0; i < terms.size(); ++i) {
                 st.ptr[i] = terms[i]->data();
@@ -813,6 +843,7 @@ static TensorPtr eval_activation_cells(Context& C, const Activation& act, const 
             acc->batch = x.batch;
             return acc;
         }
+        materialize_lazy();
         terms.push_back(ct_mul_const(C, p, act.coefficients[d], u));
     }
     std::uint32_t out_level = terms.back()->level;

@@ -128,6 +128,11 @@ struct SumTerms {
     int limbs[kMaxTerms];
     int count;
     const u64* c0;  // [level+1] residues or null
+    // optional: + rescale(rs_c * rs) for a ciphertext tensor rs at rs_level > level
+    // (mul_plain + rescale, then mod-switched: ckks.hpp:395-398, 474-493)
+    const u64* rs;
+    int rs_level;
+    const ulonglong2* rs_c;  // [rs_level+1] (c, shoup)
 };
 // scale_by: optional per-limb (c, shoup) multiplied into the input first (mul_plain + rescale);
 // add: optional terms (ciphertext tensors of >= level limbs, read as their first `level` limbs,

@@ -59,7 +59,7 @@ __global__ void k_elementwise(DevRing R, int op, const u64* __restrict__ a, cons
 #ifndef HECNN_RESCALE_VEC
 #define HECNN_RESCALE_VEC 2  // coefficients per thread (16-byte loads / stores when 2)
 #endif
-template <bool SCALED, bool ADD>
+template <bool SCALED, bool ADD, bool RS = false>
 __global__ void __launch_bounds__(TPB, HECNN_RESCALE_MINB) k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level,
                           const ulonglong2* __restrict__ c, SumTerms t) {
     constexpr int VW = HECNN_RESCALE_VEC;
@@ -91,11 +91,32 @@ __global__ void __launch_bounds__(TPB, HECNN_RESCALE_MINB) k_rescale(DevRing R, 
         v_fp = v_fp && v[h] < (1ull << 51);
         vf[h] = ntt::to_fp(v[h] & ((1ull << 51) - 1));
     }
+    // RS: one more term, rescale(t.rs_c * t.rs) of a ciphertext at level t.rs_level
+    // (a mul_plain + rescale whose output is never stored), same centring scheme
+    [[maybe_unused]] const u64* rsrc = nullptr;
+    [[maybe_unused]] u64 w[VW];
+    [[maybe_unused]] bool wupper[VW];
+    [[maybe_unused]] double wf[VW];
+    if constexpr (RS) {
+        const int rl = t.rs_level;
+        const u64 pr = R.mod[rl].q;
+        rsrc = t.rs + poly * (rl + 1) * R.n;
+        ld(rsrc + static_cast<long long>(rl) * R.n + j, w);
+#pragma unroll
+        for (int h = 0; h < VW; ++h) {
+            w[h] = mul_shoup(w[h], t.rs_c[rl].x, t.rs_c[rl].y, pr);
+            wupper[h] = w[h] > (pr >> 1);
+            v_fp = v_fp && w[h] < (1ull << 51);
+            wf[h] = ntt::to_fp(w[h] & ((1ull << 51) - 1));
+        }
+    }
     for (int i = 0; i < level; ++i) {
         const ModConst m = R.mod[i];
         const ulonglong2 inv = R.inv_dropped[level * R.limbs + i];
         u64 a[VW], r[VW];
+        [[maybe_unused]] u64 b[VW];
         ld(src + static_cast<long long>(i) * R.n + j, a);
+        if constexpr (RS) ld(rsrc + static_cast<long long>(i) * R.n + j, b);
         if (v_fp && ntt::fp_limb(m.q)) {
             const double q = static_cast<double>(m.q), qinv = R.inv_q[i];
             const double pm = ntt::to_fp(R.p_mod[level * R.limbs + i]), invf = ntt::to_fp(inv.x);
@@ -112,6 +133,13 @@ __global__ void __launch_bounds__(TPB, HECNN_RESCALE_MINB) k_rescale(DevRing R, 
                         if (k < t.count) y += ntt::to_fp(__ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j + h));
                     if (t.c0 && j + h == 0 && (poly & 1) == 0) y += ntt::to_fp(t.c0[i]);
                 }
+                if constexpr (RS) {
+                    const int rl = t.rs_level;
+                    double wc = ntt::fcentre(wf[h], q, qinv);
+                    if (wupper[h]) wc -= ntt::to_fp(R.p_mod[rl * R.limbs + i]);
+                    const double xb = ntt::fmodmul(ntt::to_fp(b[h]), ntt::to_fp(t.rs_c[i].x), q, qinv);
+                    y += ntt::fmodmul(xb - wc, ntt::to_fp(R.inv_dropped[rl * R.limbs + i].x), q, qinv);
+                }
                 r[h] = ntt::fcanon(y, q, qinv);
             }
         } else {
@@ -127,6 +155,14 @@ __global__ void __launch_bounds__(TPB, HECNN_RESCALE_MINB) k_rescale(DevRing R, 
                     for (int k = 0; k < kMaxTerms; ++k)
                         if (k < t.count) r[h] = add_mod(r[h], __ldg(t.ptr[k] + (poly * t.limbs[k] + i) * R.n + j + h), m.q);
                     if (t.c0 && j + h == 0 && (poly & 1) == 0) r[h] = add_mod(r[h], t.c0[i], m.q);
+                }
+                if constexpr (RS) {
+                    const int rl = t.rs_level;
+                    u64 wc = reduce_near(w[h], m);
+                    if (wupper[h]) wc = sub_mod(wc, R.p_mod[rl * R.limbs + i], m.q);
+                    const u64 xb = mul_shoup(b[h], t.rs_c[i].x, t.rs_c[i].y, m.q);
+                    const ulonglong2 iv = R.inv_dropped[rl * R.limbs + i];
+                    r[h] = add_mod(r[h], mul_shoup(sub_mod(xb, wc, m.q), iv.x, iv.y, m.q), m.q);
                 }
             }
         }
@@ -392,11 +428,12 @@ void rescale(const DevRing& R, const u64* in, u64* out, int level, std::size_t c
              const ulonglong2* scale_by, const SumTerms* add) {
     if (!count) return;
     const SumTerms none{};
-    const double extra = add ? add->count : 0;
+    const double extra = add ? add->count + (add->rs ? 1 : 0) : 0;
     L.begin("k_rescale", double(count) * level * R.n * (scale_by ? 2 : 1),
             8.0 * count * R.n * (2 * level + 1 + extra * level));
     const dim3 grid = rows_grid(count, R.n / HECNN_RESCALE_VEC);
-    if (add) k_rescale<true, true><<<grid, TPB, 0, L.stream>>>(R, in, out, level, scale_by, *add);
+    if (add && add->rs) k_rescale<true, true, true><<<grid, TPB, 0, L.stream>>>(R, in, out, level, scale_by, *add);
+    else if (add) k_rescale<true, true><<<grid, TPB, 0, L.stream>>>(R, in, out, level, scale_by, *add);
     else if (scale_by) k_rescale<true, false><<<grid, TPB, 0, L.stream>>>(R, in, out, level, scale_by, none);
     else k_rescale<false, false><<<grid, TPB, 0, L.stream>>>(R, in, out, level, nullptr, none);
     L.count();
