@@ -184,6 +184,31 @@ int hecnn_ct_mod_switch(hecnn_context* ctx, const hecnn_tensor* x, uint32_t to_l
 int hecnn_ct_mul_const(hecnn_context* ctx, const hecnn_tensor* x, double c, double scale, hecnn_tensor** out);
 /* add_plain(x, encode_const(c, x.scale, x.level)) (ckks.hpp:305-311) */
 int hecnn_ct_add_const(hecnn_context* ctx, const hecnn_tensor* x, double c, hecnn_tensor** out);
+/* ---- scalar fast path and plaintext operands (ckks.hpp:283-311, 372-472) --
+ * CkksEngine's per-ciphertext helpers, applied to every cell of a tensor.
+ * In-place functions modify `acc` / `ct`. Errors carry the reference's texts
+ * ("mul_scalar_mac: level mismatch", "add_plain: level mismatch", ...). */
+/* make_scalar_plain (:407-423): residues_out[level+1] = round(c * scale) mod q_i */
+int hecnn_make_scalar_plain(hecnn_context* ctx, double c, double scale, size_t level, uint64_t* residues_out);
+/* make_zero_ciphertext (:431-438): `cells` zero ciphertexts at (level, scale) */
+int hecnn_ct_zero(hecnn_context* ctx, size_t cells, uint32_t level, double scale, hecnn_tensor** out);
+/* add_inplace (:440-445): acc += x */
+int hecnn_ct_add_inplace(hecnn_context* ctx, hecnn_tensor* acc, const hecnn_tensor* x);
+/* mul_scalar_mac (:448-465): acc += x * sp, residues [ncs][sp_level+1] from
+ * hecnn_make_scalar_plain; ncs = 1 (one scalar for every cell) or the cell count */
+int hecnn_ct_scalar_mac(hecnn_context* ctx, hecnn_tensor* acc, const hecnn_tensor* x, const uint64_t* residues,
+                        size_t ncs, double sp_scale, uint32_t sp_level);
+/* add_scalar_inplace (:468-472): ct += c, encoded at ct's own scale */
+int hecnn_ct_add_scalar(hecnn_context* ctx, hecnn_tensor* ct, double c);
+/* add_plain (:305-311), mul_plain_raw / mul_plain (:372-398) with one plaintext
+ * polynomial pt (host, [pt_level+1][n], coefficient domain) for every cell;
+ * is_constant: pt is a constant polynomial (encode_const), multiplied as a
+ * scalar; rescale != 0: mul_plain, else mul_plain_raw */
+int hecnn_ct_add_plain(hecnn_context* ctx, const hecnn_tensor* x, const uint64_t* pt, uint32_t pt_level,
+                       double pt_scale, hecnn_tensor** out);
+int hecnn_ct_mul_plain(hecnn_context* ctx, const hecnn_tensor* x, const uint64_t* pt, uint32_t pt_level,
+                       double pt_scale, int is_constant, int rescale, hecnn_tensor** out);
+
 /* eval_encrypted (activation.hpp:228-265) on every cell */
 int hecnn_eval_activation(hecnn_context* ctx, const double* coefficients, size_t n_coefficients,
                           double interval_bound, const hecnn_tensor* x, hecnn_tensor** out);

@@ -31,6 +31,13 @@ using u32 = std::uint32_t;
 using u64 = std::uint64_t;
 
 namespace b200_detail {
+inline u64 splitmix64(u64 x) {  // common.hpp:164-169
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+inline u64 derive_seed(u64 seed, u64 domain) { return splitmix64(seed ^ splitmix64(domain)); }
 inline void check(int st) {
     if (st == HECNN_OK) return;
     if (st == HECNN_EINVAL) throw std::invalid_argument(hecnn_last_error());
@@ -223,6 +230,73 @@ public:
         return download(o)[0];
     }
 
+    // ---- plaintext operands and the scalar fast path (ckks.hpp:132-140, 305-311, 372-472)
+    EncodedPlaintext encode_const(double c, double scale, std::size_t level) const {
+        std::vector<u64> r(level + 1);
+        b200_detail::check(hecnn_make_scalar_plain(ctx_, c, scale, level, r.data()));
+        RingPoly p;
+        p.level = static_cast<u32>(level);
+        p.rns.assign(level + 1, std::vector<u64>(par_.ring.n, 0));
+        for (std::size_t i = 0; i <= level; ++i) p.rns[i][0] = r[i];
+        return EncodedPlaintext{std::move(p), scale, true};
+    }
+    Ciphertext add_plain(const Ciphertext& x, const EncodedPlaintext& m) const {
+        b200_detail::TensorHandle a(upload({x}));
+        std::vector<u64> flat = from_poly(m.poly);
+        hecnn_tensor* o = nullptr;
+        b200_detail::check(hecnn_ct_add_plain(ctx_, a.h, flat.data(), m.poly.level, m.scale, &o));
+        b200_detail::TensorHandle r(o);
+        return download(o)[0];
+    }
+    Ciphertext mul_plain_raw(const Ciphertext& x, const EncodedPlaintext& m) const { return plain_mul(x, m, 0); }
+    Ciphertext mul_plain(const Ciphertext& x, const EncodedPlaintext& m) const { return plain_mul(x, m, 1); }
+
+    struct ScalarPlain {  // ckks.hpp:400-405
+        std::vector<u64> residues, residues_shoup;
+        double scale = 0.0;
+        u32 level = 0;
+    };
+    ScalarPlain make_scalar_plain(double c, double scale, std::size_t level) const {
+        ScalarPlain sp;
+        sp.residues.resize(level + 1);
+        b200_detail::check(hecnn_make_scalar_plain(ctx_, c, scale, level, sp.residues.data()));
+        for (std::size_t i = 0; i <= level; ++i)
+            sp.residues_shoup.push_back(static_cast<u64>((static_cast<unsigned __int128>(sp.residues[i]) << 64) /
+                                                         par_.ring.primes[i]));
+        sp.scale = scale;
+        sp.level = static_cast<u32>(level);
+        return sp;
+    }
+    Ciphertext make_zero_ciphertext(std::size_t level, double scale) const {
+        Ciphertext ct;
+        ct.c0.level = ct.c1.level = static_cast<u32>(level);
+        ct.c0.rns.assign(level + 1, std::vector<u64>(par_.ring.n, 0));
+        ct.c1.rns = ct.c0.rns;
+        ct.scale = scale;
+        ct.level = static_cast<u32>(level);
+        return ct;
+    }
+    void add_inplace(Ciphertext& acc, const Ciphertext& x) const {
+        b200_detail::TensorHandle a(upload({acc})), b(upload({x}));
+        b200_detail::check(hecnn_ct_add_inplace(ctx_, a.h, b.h));
+        acc = download(a.h)[0];
+    }
+    // acc += x * sp; on device tensors prefer hecnn_ct_scalar_mac over a whole
+    // tensor of cells (one launch) -- this per-ciphertext form round-trips
+    void mul_scalar_mac(Ciphertext& acc, const Ciphertext& x, const ScalarPlain& sp) const {
+        b200_detail::TensorHandle a(upload({acc})), b(upload({x}));
+        b200_detail::check(hecnn_ct_scalar_mac(ctx_, a.h, b.h, sp.residues.data(), 1, sp.scale, sp.level));
+        acc = download(a.h)[0];
+    }
+    void add_scalar_inplace(Ciphertext& ct, double c) const {
+        b200_detail::TensorHandle a(upload({ct}));
+        b200_detail::check(hecnn_ct_add_scalar(ctx_, a.h, c));
+        ct = download(a.h)[0];
+    }
+    static u64 derive_seed(u64 seed, u64 domain) {  // ckks.hpp:507
+        return b200_detail::derive_seed(seed, domain);
+    }
+
     // ---- host <-> device conversion of value-semantic ciphertexts
     hecnn_tensor* upload(const std::vector<Ciphertext>& cts) const {
         if (cts.empty()) throw std::invalid_argument("upload: empty ciphertext list");
@@ -264,6 +338,15 @@ public:
     }
 
 private:
+    Ciphertext plain_mul(const Ciphertext& x, const EncodedPlaintext& m, int rescale) const {
+        b200_detail::TensorHandle a(upload({x}));
+        std::vector<u64> flat = from_poly(m.poly);
+        hecnn_tensor* o = nullptr;
+        b200_detail::check(hecnn_ct_mul_plain(ctx_, a.h, flat.data(), m.poly.level, m.scale, m.is_constant ? 1 : 0,
+                                              rescale, &o));
+        b200_detail::TensorHandle r(o);
+        return download(o)[0];
+    }
     template <class F>
     Ciphertext binary(F fn, const Ciphertext& x, const Ciphertext& y) const {
         b200_detail::TensorHandle a(upload({x})), b(upload({y}));

@@ -240,6 +240,34 @@ class RefEngine:
                                    ctypes.c_double(cscale), _p(out), ctypes.byref(s)))
         return out, s.value
 
+    def scalar_plain(self, c: float, scale: float, level: int) -> np.ndarray:
+        out = np.empty(level + 1, dtype=np.uint64)
+        _check(lib().ref_scalar_plain(self.h, ctypes.c_double(c), ctypes.c_double(scale), ctypes.c_size_t(level),
+                                      _p(out)))
+        return out
+
+    def scalar_mac(self, acc, x, level: int, acc_scale: float, sx: float, c: float, cscale: float, b=None):
+        acc = np.ascontiguousarray(acc, dtype=np.uint64)
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        out = np.empty((2, level + 1, self.n), dtype=np.uint64)
+        _check(lib().ref_scalar_mac(self.h, _p(acc), _p(x), ctypes.c_size_t(level), ctypes.c_double(acc_scale),
+                                    ctypes.c_double(sx), ctypes.c_double(c), ctypes.c_double(cscale),
+                                    ctypes.c_int(b is not None), ctypes.c_double(b or 0.0), _p(out)))
+        return out
+
+    def plain_op(self, op: int, x, level: int, sx: float, slots, pscale: float, constant: bool):
+        """op 0 add_plain, 1 mul_plain_raw, 2 mul_plain with encode_real(slots) or encode_const(slots[0])."""
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        v = np.ascontiguousarray(slots, dtype=np.float64)
+        out = np.empty(2 * (level + 1) * self.n, dtype=np.uint64)
+        lv = ctypes.c_uint32()
+        s = ctypes.c_double()
+        _check(lib().ref_plain_op(self.h, ctypes.c_int(op), _p(x), ctypes.c_size_t(level), ctypes.c_double(sx),
+                                  _p(v, ctypes.c_double), ctypes.c_size_t(v.size), ctypes.c_double(pscale),
+                                  ctypes.c_int(constant), _p(out), ctypes.byref(lv), ctypes.byref(s)))
+        k = lv.value + 1
+        return out[: 2 * k * self.n].reshape(2, k, self.n).copy(), lv.value, s.value
+
     def eval_activation(self, coeffs, bound: float, x, level: int, sx: float):
         c = np.ascontiguousarray(coeffs, dtype=np.float64)
         x = np.ascontiguousarray(x, dtype=np.uint64)

@@ -313,6 +313,44 @@ int ref_mul_const(void* e, const uint64_t* x, size_t level, double sx, double c,
     });
 }
 
+// make_scalar_plain (ckks.hpp:407-423): residues of round(c * scale)
+int ref_scalar_plain(void* e, double c, double scale, size_t level, uint64_t* out) {
+    return guard([&] {
+        const CkksEngine& eng = static_cast<RefEngine*>(e)->eng;
+        CkksEngine::ScalarPlain sp = eng.make_scalar_plain(c, scale, level);
+        std::memcpy(out, sp.residues.data(), sp.residues.size() * 8);
+    });
+}
+
+// acc' = acc + x * make_scalar_plain(c, cscale) (mul_scalar_mac, ckks.hpp:448-465),
+// then add_scalar_inplace(acc', b) when add_b != 0 (:468-472)
+int ref_scalar_mac(void* e, const uint64_t* acc, const uint64_t* x, size_t level, double acc_scale, double sx,
+                   double c, double cscale, int add_b, double b, uint64_t* out) {
+    return guard([&] {
+        const CkksEngine& eng = static_cast<RefEngine*>(e)->eng;
+        Ciphertext a = ct_from(eng, acc, level, acc_scale);
+        eng.mul_scalar_mac(a, ct_from(eng, x, level, sx), eng.make_scalar_plain(c, cscale, level));
+        if (add_b) eng.add_scalar_inplace(a, b);
+        ct_to(eng, a, out);
+    });
+}
+
+// add_plain / mul_plain_raw / mul_plain of an encode_real plaintext (or
+// encode_const(slots[0]) when constant) (ckks.hpp:305-311, 372-398)
+int ref_plain_op(void* e, int op, const uint64_t* x, size_t level, double sx, const double* slots, size_t nslots,
+                 double pscale, int constant, uint64_t* out, uint32_t* out_level, double* out_scale) {
+    return guard([&] {
+        const CkksEngine& eng = static_cast<RefEngine*>(e)->eng;
+        EncodedPlaintext m = constant ? eng.encode_const(slots[0], pscale, level)
+                                      : eng.encode_real(std::vector<double>(slots, slots + nslots), pscale, level);
+        Ciphertext in = ct_from(eng, x, level, sx);
+        Ciphertext r = op == 0 ? eng.add_plain(in, m) : (op == 1 ? eng.mul_plain_raw(in, m) : eng.mul_plain(in, m));
+        ct_to(eng, r, out);
+        *out_level = r.level;
+        *out_scale = r.scale;
+    });
+}
+
 // eval_encrypted (activation.hpp:228-265)
 int ref_eval_activation(void* e, void* k, const double* coeffs, size_t ncoeffs, double bound, const uint64_t* x,
                         size_t level, double sx, uint64_t* out, uint32_t* out_level, double* out_scale) {

@@ -49,7 +49,8 @@ EXPORTED_SYMBOLS = (
     "hecnn_tensor_copy_to_device", "hecnn_host_encode_real", "hecnn_host_decode_real",
     "hecnn_host_encryption_randomness", "hecnn_fp64_modmul_peak", "hecnn_context_trim",
     "hecnn_blob_params", "hecnn_blob_save_key", "hecnn_blob_load_key", "hecnn_blob_save_ciphertext",
-    "hecnn_blob_load_ciphertexts",
+    "hecnn_blob_load_ciphertexts", "hecnn_make_scalar_plain", "hecnn_ct_zero", "hecnn_ct_add_inplace",
+    "hecnn_ct_scalar_mac", "hecnn_ct_add_scalar", "hecnn_ct_add_plain", "hecnn_ct_mul_plain",
 )
 
 _lib = None
@@ -125,6 +126,13 @@ _SIGNATURES = {
     "hecnn_ct_mul_const": [_V, _V, _D, _D, _PV],
     "hecnn_ct_add_const": [_V, _V, _D, _PV],
     "hecnn_eval_activation": [_V, _PD, _SZ, _D, _V, _PV],
+    "hecnn_make_scalar_plain": [_V, _D, _D, _SZ, _PU64],
+    "hecnn_ct_zero": [_V, _SZ, _U32, _D, _PV],
+    "hecnn_ct_add_inplace": [_V, _V, _V],
+    "hecnn_ct_scalar_mac": [_V, _V, _V, _PU64, _SZ, _D, _U32],
+    "hecnn_ct_add_scalar": [_V, _V, _D],
+    "hecnn_ct_add_plain": [_V, _V, _PU64, _U32, _D, _PV],
+    "hecnn_ct_mul_plain": [_V, _V, _PU64, _U32, _D, _I, _I, _PV],
     "hecnn_model_create": [_V, _V, _PV],
     "hecnn_model_destroy": [_V],
     "hecnn_model_depth_cost": [_V, _PSZ],
@@ -632,6 +640,23 @@ class Model:
 
 # ---------------------------------------------------------------- engine
 
+@dataclass
+class ScalarPlain:
+    """CkksEngine::ScalarPlain (ckks.hpp:400-405): residues per active prime."""
+    residues: np.ndarray
+    scale: float
+    level: int
+
+
+@dataclass
+class EncodedPlaintext:
+    """EncodedPlaintext (ckks.hpp:21-72): coefficient-domain residues [level+1][n]."""
+    poly: np.ndarray
+    scale: float
+    level: int
+    is_constant: bool = False
+
+
 class CkksEngine:
     """CkksEngine (ckks.hpp:77-636) on one B200. Keys live on the device."""
 
@@ -932,6 +957,69 @@ class CkksEngine:
     def add_const(self, x, c):
         """add_plain(x, encode_const(c, x.scale, x.level))"""
         return self._unary(lib().hecnn_ct_add_const, x.handle, ctypes.c_double(c))
+
+    # ---- the scalar fast path and plaintext operands (ckks.hpp:283-311, 372-472),
+    # applied to every cell of a tensor
+
+    def make_scalar_plain(self, c: float, scale: float, level: int) -> "ScalarPlain":
+        """make_scalar_plain (ckks.hpp:407-423): round(c * scale) mod q_i, i <= level."""
+        r = np.empty(level + 1, dtype=np.uint64)
+        _check(lib().hecnn_make_scalar_plain(self.ctx, ctypes.c_double(c), ctypes.c_double(scale),
+                                             ctypes.c_size_t(level), _ptr(r)))
+        return ScalarPlain(r, scale, level)
+
+    def make_zero_ciphertext(self, level: int, scale: float, cells: int = 1) -> EncryptedTensor:
+        """make_zero_ciphertext (ckks.hpp:431-438), `cells` of them."""
+        return self._unary(lib().hecnn_ct_zero, ctypes.c_size_t(cells), ctypes.c_uint32(level), ctypes.c_double(scale))
+
+    def add_inplace(self, acc: EncryptedTensor, x: EncryptedTensor) -> None:
+        """add_inplace (ckks.hpp:440-445)."""
+        _check(lib().hecnn_ct_add_inplace(self.ctx, acc.handle, x.handle))
+
+    def mul_scalar_mac(self, acc: EncryptedTensor, x: EncryptedTensor, sp) -> None:
+        """mul_scalar_mac (ckks.hpp:448-465): acc += x * sp. `sp` is one
+        ScalarPlain for every cell or a sequence of them, one per cell (same
+        scale and level)."""
+        sps = [sp] if isinstance(sp, ScalarPlain) else list(sp)
+        if not sps:
+            raise ValueError("mul_scalar_mac: no scalar")
+        r = np.ascontiguousarray(np.stack([q.residues for q in sps]), dtype=np.uint64)
+        _check(lib().hecnn_ct_scalar_mac(self.ctx, acc.handle, x.handle, _ptr(r), ctypes.c_size_t(len(sps)),
+                                         ctypes.c_double(sps[0].scale), ctypes.c_uint32(sps[0].level)))
+
+    def add_scalar_inplace(self, ct: EncryptedTensor, c: float) -> None:
+        """add_scalar_inplace (ckks.hpp:468-472): c encoded at ct's own scale."""
+        _check(lib().hecnn_ct_add_scalar(self.ctx, ct.handle, ctypes.c_double(c)))
+
+    def encode_const(self, c: float, scale: float, level: int) -> "EncodedPlaintext":
+        """encode_const (ckks.hpp:132-140): the constant polynomial round(c * scale)."""
+        sp = self.make_scalar_plain(c, scale, level)
+        poly = np.zeros((level + 1, self.params.n), dtype=np.uint64)
+        poly[:, 0] = sp.residues
+        return EncodedPlaintext(poly, scale, level, True)
+
+    def encode_real(self, values, scale: float, level: int) -> "EncodedPlaintext":
+        """encode_real (ckks.hpp:124-129) on the host."""
+        return EncodedPlaintext(host_encode_real(self.params, values, level, scale), scale, level, False)
+
+    def add_plain(self, x: EncryptedTensor, m: "EncodedPlaintext") -> EncryptedTensor:
+        """add_plain (ckks.hpp:305-311) of one plaintext to every cell."""
+        poly = np.ascontiguousarray(m.poly, dtype=np.uint64)
+        return self._unary(lib().hecnn_ct_add_plain, x.handle, _ptr(poly), ctypes.c_uint32(m.level),
+                           ctypes.c_double(m.scale))
+
+    def mul_plain_raw(self, x: EncryptedTensor, m: "EncodedPlaintext") -> EncryptedTensor:
+        """mul_plain_raw (ckks.hpp:372-393): scale multiplies, level unchanged."""
+        return self._mul_plain(x, m, 0)
+
+    def mul_plain(self, x: EncryptedTensor, m: "EncodedPlaintext") -> EncryptedTensor:
+        """mul_plain (ckks.hpp:395-398): mul_plain_raw then rescale."""
+        return self._mul_plain(x, m, 1)
+
+    def _mul_plain(self, x, m, rescale):
+        poly = np.ascontiguousarray(m.poly, dtype=np.uint64)
+        return self._unary(lib().hecnn_ct_mul_plain, x.handle, _ptr(poly), ctypes.c_uint32(m.level),
+                           ctypes.c_double(m.scale), ctypes.c_int(1 if m.is_constant else 0), ctypes.c_int(rescale))
 
     def eval_activation(self, act: PolyActivation, x: EncryptedTensor) -> EncryptedTensor:
         c = np.ascontiguousarray(act.coefficients, dtype=np.float64)

@@ -61,6 +61,10 @@ const Tensor& T(const hecnn_tensor* t) {
     if (!t || !t->t) throw std::invalid_argument("null tensor");
     return *t->t;
 }
+Tensor& TM(hecnn_tensor* t) {
+    if (!t || !t->t) throw std::invalid_argument("null tensor");
+    return *t->t;
+}
 std::shared_ptr<Context> owner(hecnn_context* c) { return c->ctx; }
 
 hecnn_tensor* wrap(hecnn_context* c, TensorPtr t) {
@@ -481,6 +485,38 @@ int hecnn_ct_mul_const(hecnn_context* ctx, const hecnn_tensor* x, double c, doub
 }
 int hecnn_ct_add_const(hecnn_context* ctx, const hecnn_tensor* x, double c, hecnn_tensor** out) {
     return guard([&] { *out = wrap(ctx, ct_add_const(C(ctx), T(x), c)); });
+}
+
+int hecnn_make_scalar_plain(hecnn_context* ctx, double c, double scale, size_t level, uint64_t* residues_out) {
+    return guard([&] {
+        Context& cx = C(ctx);
+        if (level > cx.top()) throw std::invalid_argument("make_scalar_plain: level above the chain");
+        const ScalarPlain sp = make_scalar_plain(cx, c, scale, level);
+        std::copy(sp.residues.begin(), sp.residues.end(), residues_out);
+    });
+}
+int hecnn_ct_zero(hecnn_context* ctx, size_t cells, uint32_t level, double scale, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ctx, ct_zero(C(ctx), cells, level, scale)); });
+}
+int hecnn_ct_add_inplace(hecnn_context* ctx, hecnn_tensor* acc, const hecnn_tensor* x) {
+    return guard([&] { ct_add_inplace(C(ctx), TM(acc), T(x)); });
+}
+int hecnn_ct_scalar_mac(hecnn_context* ctx, hecnn_tensor* acc, const hecnn_tensor* x, const uint64_t* residues,
+                        size_t ncs, double sp_scale, uint32_t sp_level) {
+    return guard([&] { ct_scalar_mac(C(ctx), TM(acc), T(x), residues, ncs, sp_scale, sp_level); });
+}
+int hecnn_ct_add_scalar(hecnn_context* ctx, hecnn_tensor* ct, double c) {
+    return guard([&] { ct_add_scalar(C(ctx), TM(ct), c); });
+}
+int hecnn_ct_add_plain(hecnn_context* ctx, const hecnn_tensor* x, const uint64_t* pt, uint32_t pt_level,
+                       double pt_scale, hecnn_tensor** out) {
+    return guard([&] { *out = wrap(ctx, ct_add_plain(C(ctx), T(x), pt, pt_level, pt_scale)); });
+}
+int hecnn_ct_mul_plain(hecnn_context* ctx, const hecnn_tensor* x, const uint64_t* pt, uint32_t pt_level,
+                       double pt_scale, int is_constant, int rescale, hecnn_tensor** out) {
+    return guard([&] {
+        *out = wrap(ctx, ct_mul_plain(C(ctx), T(x), pt, pt_level, pt_scale, is_constant != 0, rescale != 0));
+    });
 }
 
 int hecnn_eval_activation(hecnn_context* ctx, const double* coefficients, size_t n_coefficients, double interval_bound,

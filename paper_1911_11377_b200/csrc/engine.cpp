@@ -726,6 +726,117 @@ TensorPtr ct_add_const(Context& C, const Tensor& x, double c) {
     return out;
 }
 
+// ---------------------------------------------------------------- scalar fast path / plaintexts
+
+// CkksEngine::make_scalar_plain (ckks.hpp:407-423)
+ScalarPlain make_scalar_plain(const Context& C, double c, double scale, std::size_t level) {
+    C.enc->check_encode(1, std::abs(c), scale, level);
+    ScalarPlain sp;
+    sp.scale = scale;
+    sp.level = static_cast<std::uint32_t>(level);
+    sp.residues = C.enc->residues_of_rounded(roundl(static_cast<long double>(c) * static_cast<long double>(scale)), level);
+    return sp;
+}
+
+// make_zero_ciphertext (ckks.hpp:431-438)
+TensorPtr ct_zero(Context& C, std::size_t cells, std::uint32_t level, double scale) {
+    if (level > C.top()) throw std::invalid_argument("make_zero_ciphertext: level above the chain");
+    TensorPtr out = make_tensor(C, cells, level, scale);
+    cuda_check(cudaMemsetAsync(out->data(), 0, cells * out->cell_words() * 8, C.stream), "memset");
+    return out;
+}
+
+// add_inplace (ckks.hpp:440-445)
+void ct_add_inplace(Context& C, Tensor& acc, const Tensor& x) {
+    if (acc.level != x.level) throw std::invalid_argument("add: level mismatch (use rescale/mod_switch first)");
+    require_scale_match(acc.scale, x.scale, "add");
+    if (acc.cells != x.cells) throw std::invalid_argument("add: cell count mismatch");
+    poly_elementwise(C.dev, EwOp::Add, acc.data(), x.data(), acc.data(), static_cast<int>(acc.level), 2 * acc.cells,
+                     C.L());
+}
+
+static void check_residues(const Context& C, const u64* r, std::size_t rows, std::size_t limbs, std::size_t stride,
+                           const char* what) {
+    for (std::size_t k = 0; k < rows; ++k)
+        for (std::size_t i = 0; i < limbs; ++i)
+            if (r[k * limbs * stride + i * stride] >= C.ring.primes[i])
+                throw std::invalid_argument(std::string(what) + ": residue not below its prime");
+}
+
+// mul_scalar_mac (ckks.hpp:448-465)
+void ct_scalar_mac(Context& C, Tensor& acc, const Tensor& x, const u64* residues, std::size_t ncs, double sp_scale,
+                   std::uint32_t sp_level) {
+    if (x.level != acc.level || sp_level != acc.level) throw std::invalid_argument("mul_scalar_mac: level mismatch");
+    require_scale_match(acc.scale, x.scale * sp_scale, "mul_scalar_mac");
+    if (acc.cells != x.cells) throw std::invalid_argument("mul_scalar_mac: cell count mismatch");
+    if (ncs != 1 && ncs != acc.cells) throw std::invalid_argument("mul_scalar_mac: one scalar, or one per cell");
+    const std::size_t limbs = acc.level + 1;
+    check_residues(C, residues, ncs, limbs, 1, "mul_scalar_mac");
+    std::vector<ulonglong2> cs(ncs * limbs);
+    for (std::size_t k = 0; k < ncs; ++k)
+        for (std::size_t i = 0; i < limbs; ++i) {
+            const u64 r = residues[k * limbs + i];
+            cs[k * limbs + i] = make_ulonglong2(r, shoup_of(r, C.ring.primes[i]));
+        }
+    DevBuf dc = C.upload_vec(cs);
+    scalar_mac(C.dev, x.data(), dc.as<ulonglong2>(), ncs, acc.data(), static_cast<int>(acc.level), acc.cells, C.L());
+}
+
+// add_scalar_inplace (ckks.hpp:468-472)
+void ct_add_scalar(Context& C, Tensor& ct, double c) {
+    const ScalarPlain sp = make_scalar_plain(C, c, ct.scale, ct.level);
+    DevBuf dc = C.upload_vec(sp.residues);
+    add_coeff0(C.dev, ct.data(), dc.as<u64>(), static_cast<int>(ct.level), ct.cells, C.L());
+}
+
+// add_plain (ckks.hpp:305-311)
+TensorPtr ct_add_plain(Context& C, const Tensor& x, const u64* pt, std::uint32_t pt_level, double pt_scale) {
+    if (pt_level != x.level) throw std::invalid_argument("add_plain: level mismatch");
+    require_scale_match(x.scale, pt_scale, "add_plain");
+    const std::size_t n = C.n(), limbs = x.level + 1;
+    for (std::size_t i = 0; i < limbs; ++i)
+        for (std::size_t j = 0; j < n; ++j)
+            if (pt[i * n + j] >= C.ring.primes[i]) throw std::invalid_argument("add_plain: residue not below its prime");
+    DevBuf dp = C.upload_vec(std::vector<u64>(pt, pt + limbs * n));
+    TensorPtr out = make_tensor(C, x.cells, x.level, x.scale);
+    out->shape = x.shape;
+    out->batch = x.batch;
+    plain_bcast(C.dev, x.data(), dp.as<u64>(), out->data(), static_cast<int>(x.level), x.cells, 0, C.L());
+    return out;
+}
+
+// mul_plain_raw / mul_plain (ckks.hpp:372-398): a constant plaintext multiplies
+// every coefficient by its coefficient 0 (scalar_mul, :588-597), any other goes
+// through the NTT
+TensorPtr ct_mul_plain(Context& C, const Tensor& x, const u64* pt, std::uint32_t pt_level, double pt_scale,
+                       bool is_constant, bool rescale) {
+    if (rescale && x.level == 0) throw std::invalid_argument("mul_plain: at last level, no room to rescale");
+    if (pt_level != x.level) throw std::invalid_argument("mul_plain: level mismatch");
+    check_scale_headroom(C, x.scale, pt_scale, x.level);
+    const std::size_t n = C.n(), limbs = x.level + 1;
+    for (std::size_t i = 0; i < limbs; ++i)
+        for (std::size_t j = 0; j < (is_constant ? 1 : n); ++j)
+            if (pt[i * n + j] >= C.ring.primes[i]) throw std::invalid_argument("mul_plain: residue not below its prime");
+    TensorPtr raw = make_tensor(C, x.cells, x.level, x.scale * pt_scale);
+    raw->shape = x.shape;
+    raw->batch = x.batch;
+    const int lv = static_cast<int>(x.level);
+    Launch L = C.L();
+    if (is_constant) {
+        std::vector<u64> c0(limbs);
+        for (std::size_t i = 0; i < limbs; ++i) c0[i] = pt[i * n];
+        DevBuf dc = C.upload_vec(with_shoup(C.ring, c0));
+        scalar_mul(C.dev, x.data(), dc.as<ulonglong2>(), raw->data(), lv, 2 * x.cells, L);
+    } else {
+        DevBuf dp = C.upload_vec(std::vector<u64>(pt, pt + limbs * n));
+        ntt_forward(C.dev, dp.as<u64>(), lv, 1, L);
+        ntt_forward_to(C.dev, x.data(), raw->data(), lv, 2 * x.cells, L);
+        plain_bcast(C.dev, raw->data(), dp.as<u64>(), raw->data(), lv, x.cells, 1, L);
+        ntt_inverse(C.dev, raw->data(), lv, 2 * x.cells, L);
+    }
+    return rescale ? ct_rescale(C, *raw) : std::move(raw);
+}
+
 // ---------------------------------------------------------------- activation
 
 std::size_t Activation::encrypted_depth() const {

@@ -171,6 +171,24 @@ TensorPtr ct_rescale(Context& C, const Tensor& x);
 TensorPtr ct_mod_switch(Context& C, const Tensor& x, std::uint32_t to_level);
 TensorPtr ct_mul_const(Context& C, const Tensor& x, double c, double scale);
 TensorPtr ct_add_const(Context& C, const Tensor& x, double c);
+// ---- the reference's scalar fast path and plaintext ops (ckks.hpp:283-311, 372-472),
+// each applied to every cell of a tensor
+struct ScalarPlain {  // CkksEngine::ScalarPlain (residues per active prime)
+    std::vector<u64> residues;
+    double scale = 0.0;
+    std::uint32_t level = 0;
+};
+ScalarPlain make_scalar_plain(const Context& C, double c, double scale, std::size_t level);
+TensorPtr ct_zero(Context& C, std::size_t cells, std::uint32_t level, double scale);
+void ct_add_inplace(Context& C, Tensor& acc, const Tensor& x);
+// acc += x * sp; residues [ncs][level+1] with ncs = 1 (every cell) or acc.cells (one scalar per cell)
+void ct_scalar_mac(Context& C, Tensor& acc, const Tensor& x, const u64* residues, std::size_t ncs, double sp_scale,
+                   std::uint32_t sp_level);
+void ct_add_scalar(Context& C, Tensor& ct, double c);
+// plaintext operand: a host polynomial [pt_level+1][n] in the coefficient domain
+TensorPtr ct_add_plain(Context& C, const Tensor& x, const u64* pt, std::uint32_t pt_level, double pt_scale);
+TensorPtr ct_mul_plain(Context& C, const Tensor& x, const u64* pt, std::uint32_t pt_level, double pt_scale,
+                       bool is_constant, bool rescale);
 // key_switch on raw d2 polys: out [count][2][level+1][n] NTT domain
 void key_switch_raw(Context& C, const u64* d2, u64* out, std::size_t level, std::size_t count);
 

@@ -154,6 +154,13 @@ void scalar_mul(const DevRing& R, const u64* in, const ulonglong2* consts, u64* 
 // c0[ct][i][0] += consts[i] for every ciphertext of a [count][2][level+1][n] batch
 // (add_scalar_inplace / add_plain of a constant, ckks.hpp:305-311, 468-472)
 void add_coeff0(const DevRing& R, u64* cts, const u64* consts, int level, std::size_t count, const Launch& L);
+// ciphertexts [cells][2][level+1][n] against one plaintext [level+1][n]: op 0 c0 += p
+// (coefficient domain), op 1 c0, c1 *= p (NTT domain); out may equal x
+void plain_bcast(const DevRing& R, const u64* x, const u64* p, u64* out, int level, std::size_t cells, int op,
+                 const Launch& L);
+// acc [cells][2][level+1][n] += x * c_i; consts [ncs][level+1] (c, shoup), cell k uses row k % ncs
+void scalar_mac(const DevRing& R, const u64* x, const ulonglong2* consts, std::size_t ncs, u64* acc, int level,
+                std::size_t cells, const Launch& L);
 
 // Shoup companions floor(w * 2^64 / q_i) of a [count][limbs][n] table (evk)
 void shoup_table(const DevRing& R, const u64* in, u64* out, int limbs, std::size_t count, const Launch& L);

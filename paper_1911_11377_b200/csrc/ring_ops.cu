@@ -224,6 +224,37 @@ __global__ void k_scalar_mul(DevRing R, const u64* __restrict__ in, const ulongl
     out[row * R.n + j] = mul_shoup(in[row * R.n + j], c.x, c.y, q);
 }
 
+// acc += x * c_i (CkksEngine::mul_scalar_mac, ckks.hpp:448-465): rows (cell, comp, limb);
+// consts [ncs][limbs] (c, shoup), cell k uses row k % ncs
+__global__ void k_scalar_mac(DevRing R, const u64* __restrict__ x, const ulonglong2* __restrict__ consts,
+                             u64* __restrict__ acc, int limbs, long long ncs) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const int i = static_cast<int>(row % limbs);
+    const long long cell = row / limbs / 2;
+    const u64 q = R.mod[i].q;
+    const ulonglong2 c = consts[(cell % ncs) * limbs + i];
+    const long long o = row * R.n + j;
+    acc[o] = add_mod(acc[o], mul_shoup(x[o], c.x, c.y, q), q);
+}
+
+// ciphertexts [cells][2][limbs][n] against one plaintext polynomial [limbs][n]:
+// op 0: c0 += p (add_plain), op 1: c0 *= p, c1 *= p (NTT-domain mul_plain)
+__global__ void k_plain_bcast(DevRing R, const u64* __restrict__ x, const u64* __restrict__ p, u64* __restrict__ out,
+                              int limbs, int op) {
+    const int j = blockIdx.y * TPB + threadIdx.x;
+    if (j >= R.n) return;
+    const long long row = blockIdx.x;
+    const int i = static_cast<int>(row % limbs);
+    const int comp = static_cast<int>((row / limbs) & 1);
+    const ModConst m = R.mod[i];
+    const long long o = row * R.n + j;
+    const u64 v = x[o], w = p[static_cast<long long>(i) * R.n + j];
+    if (op == 0) out[o] = comp == 0 ? add_mod(v, w, m.q) : v;
+    else out[o] = mul_mod(v, w, m);
+}
+
 __global__ void k_add_coeff0(DevRing R, u64* __restrict__ cts, const u64* __restrict__ consts, int limbs,
                              long long count) {
     const long long t = static_cast<long long>(blockIdx.x) * TPB + threadIdx.x;
@@ -478,6 +509,26 @@ void scalar_mul(const DevRing& R, const u64* in, const ulonglong2* consts, u64* 
     k_scalar_mul<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, in, consts, out, level + 1);
     L.count();
     check_launch("scalar_mul");
+}
+
+void scalar_mac(const DevRing& R, const u64* x, const ulonglong2* consts, std::size_t ncs, u64* acc, int level,
+                std::size_t cells, const Launch& L) {
+    const std::size_t rows = cells * 2 * (level + 1);
+    if (!rows) return;
+    L.begin("k_scalar_mac", double(rows) * R.n, 24.0 * rows * R.n);
+    k_scalar_mac<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, x, consts, acc, level + 1, static_cast<long long>(ncs));
+    L.count();
+    check_launch("scalar_mac");
+}
+
+void plain_bcast(const DevRing& R, const u64* x, const u64* p, u64* out, int level, std::size_t cells, int op,
+                 const Launch& L) {
+    const std::size_t rows = cells * 2 * (level + 1);
+    if (!rows) return;
+    L.begin("k_plain_bcast", double(rows) * R.n, 24.0 * rows * R.n);
+    k_plain_bcast<<<rows_grid(rows, R.n), TPB, 0, L.stream>>>(R, x, p, out, level + 1, op);
+    L.count();
+    check_launch("plain_bcast");
 }
 
 void add_coeff0(const DevRing& R, u64* cts, const u64* consts, int level, std::size_t count, const Launch& L) {

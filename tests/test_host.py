@@ -110,3 +110,12 @@ def test_no_silent_cpu_fallback():
         pytest.skip("a GPU is present")
     with pytest.raises(RuntimeError, match="CUDA"):
         hb.CkksEngine(hb.preset_params("toy-n16"))
+
+
+def test_dropin_header_compiles():
+    """The C++ drop-in header (include/hecnn_b200/hecnn.hpp) and both sample
+    programs written against it compile (syntax only: no GPU, no link)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for src in ("dropin_inference.cpp", "dropin_scalar.cpp"):
+        subprocess.run(["g++", "-std=c++20", "-fsyntax-only", f"-I{root}/include", f"{root}/tests/cpp/{src}"], check=True)
