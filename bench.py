@@ -413,6 +413,17 @@ def reference_c4_images_per_s(threads):
     return p.n // 2 / est, est, wall, [float(s) for s in secs]
 
 
+def c4_config(world):
+    """The `config` object of both arms' lines (the driver compares them)."""
+    in_gib = 32 * 32 * 3 * 2 * 9 * 8192 * 8 / 2 ** 30  # input set: 3072 cells x 2 polys x 9 limbs x N words
+    return {"workload": "C4 CIFAR-10-shaped CNN + poly ReLU (conv16-act-pool-conv32-act-dense10), "
+                        "net-n8192-d8, 4096 encrypted images per set per GPU",
+            "preset": "net-n8192-d8", "images_per_set": 4096, "sets_per_gpu_per_step": 1,
+            "parallelism": f"dp{world} (batch sharding; NCCL all_gather of output ciphertexts only)",
+            "l2": f"inputs larger than L2 ({in_gib:.2f} GiB of input ciphertexts)",
+            "profiling": "per-kernel CUDA events on the launching stream inside the timed region"}
+
+
 def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
@@ -429,8 +440,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "C4 CIFAR-10-shaped CNN + poly ReLU, net-n8192-d8, 4096 encrypted 32x32x3 "
-                                   "images per set", "parallelism": "host threads (reference parallel_for)"},
+            "config": c4_config(world),
+            "execution": f"reference forward_encrypted on {threads} host threads (its parallel_for), rank 0 only",
             "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -507,6 +518,7 @@ def run_ours(args):
     data = rng.uniform(0, 1, size=(batch, spec.input.positions()))
     x = eng.encrypt_tensor(data, seed=11 + rank, shape=spec.input)     # client side, untimed
     in_words = x.words()
+    assert batch == c4_config(world)["images_per_set"] and in_words.nbytes == 32 * 32 * 3 * 2 * 9 * 8192 * 8
     host_in = torch.from_numpy(in_words.reshape(-1).view(np.int64)).pin_memory()
     h2d_bytes = in_words.nbytes
 
@@ -649,12 +661,7 @@ def run_ours(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic (uniform [0,1] 32x32x3 images, numpy Glorot weights)",
-                "config": {"workload": "C4 CIFAR-10-shaped CNN + poly ReLU (conv16-act-pool-conv32-act-dense10), "
-                                       "net-n8192-d8, 4096 encrypted images per set per GPU",
-                           "preset": "net-n8192-d8", "images_per_set": batch, "sets_per_gpu_per_step": 1,
-                           "parallelism": f"dp{world} (batch sharding; NCCL all_gather of output ciphertexts only)",
-                           "l2": f"inputs larger than L2 ({in_words.nbytes / 2**30:.2f} GiB of input ciphertexts)",
-                           "profiling": "per-kernel CUDA events on the launching stream inside the timed region"},
+                "config": c4_config(world),
                 "clocks": clk.summary(),
                 "e2e": {"value": images / e2e_s, "unit": "images/s", "h2d_bytes_per_step": h2d_bytes,
                         "d2h_bytes_per_step": out_words_n * 8},

@@ -4,7 +4,8 @@ set -e
 cd "$(dirname "$0")/.."
 declare -A V
 V[na]=""
-V[p512]="-DHECNN_TC_PROD=512"
+V[col512]="-DHECNN_KS_MAXT_COL=512"
+V[col512m]="-DHECNN_KS_MAXT_COL=512 -DHECNN_KS_LOGE=3"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
