@@ -491,6 +491,7 @@ int hecnn_make_scalar_plain(hecnn_context* ctx, double c, double scale, size_t l
     return guard([&] {
         Context& cx = C(ctx);
         if (level > cx.top()) throw std::invalid_argument("make_scalar_plain: level above the chain");
+        if (!residues_out) throw std::invalid_argument("make_scalar_plain: null output");
         const ScalarPlain sp = make_scalar_plain(cx, c, scale, level);
         std::copy(sp.residues.begin(), sp.residues.end(), residues_out);
     });
@@ -503,18 +504,25 @@ int hecnn_ct_add_inplace(hecnn_context* ctx, hecnn_tensor* acc, const hecnn_tens
 }
 int hecnn_ct_scalar_mac(hecnn_context* ctx, hecnn_tensor* acc, const hecnn_tensor* x, const uint64_t* residues,
                         size_t ncs, double sp_scale, uint32_t sp_level) {
-    return guard([&] { ct_scalar_mac(C(ctx), TM(acc), T(x), residues, ncs, sp_scale, sp_level); });
+    return guard([&] {
+        if (!residues) throw std::invalid_argument("mul_scalar_mac: null residues");
+        ct_scalar_mac(C(ctx), TM(acc), T(x), residues, ncs, sp_scale, sp_level);
+    });
 }
 int hecnn_ct_add_scalar(hecnn_context* ctx, hecnn_tensor* ct, double c) {
     return guard([&] { ct_add_scalar(C(ctx), TM(ct), c); });
 }
 int hecnn_ct_add_plain(hecnn_context* ctx, const hecnn_tensor* x, const uint64_t* pt, uint32_t pt_level,
                        double pt_scale, hecnn_tensor** out) {
-    return guard([&] { *out = wrap(ctx, ct_add_plain(C(ctx), T(x), pt, pt_level, pt_scale)); });
+    return guard([&] {
+        if (!pt) throw std::invalid_argument("add_plain: null plaintext");
+        *out = wrap(ctx, ct_add_plain(C(ctx), T(x), pt, pt_level, pt_scale));
+    });
 }
 int hecnn_ct_mul_plain(hecnn_context* ctx, const hecnn_tensor* x, const uint64_t* pt, uint32_t pt_level,
                        double pt_scale, int is_constant, int rescale, hecnn_tensor** out) {
     return guard([&] {
+        if (!pt) throw std::invalid_argument("mul_plain: null plaintext");
         *out = wrap(ctx, ct_mul_plain(C(ctx), T(x), pt, pt_level, pt_scale, is_constant != 0, rescale != 0));
     });
 }
