@@ -589,8 +589,7 @@ void launch_imma(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int l
                  int pg, long long blocks, cudaStream_t st) {
     auto kern = k_conv_imma<MT, SHORT, WIDE>;
     constexpr int smem = ImmaShape<WIDE, MT>::SMEM;
-    static bool init = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true);
-    (void)init;
+    smem_opt_in(kern, smem);
     kern<<<static_cast<unsigned>(blocks), WARPS * 32, smem, st>>>(R, g, x, y, level, limb0, nl, groups, pg);
 }
 

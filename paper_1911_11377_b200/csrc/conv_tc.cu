@@ -418,10 +418,7 @@ void tc_mac(const DevRing& R, const ImmaMac& g, const u64* x, u64* y, int level,
     auto kern = wide ? k_conv_tc<true> : k_conv_tc<false>;
     const int smem = wide ? TcShape<true>::SMEM : TcShape<false>::SMEM;
     const int oc_tile = tc_oc_tile(wide);
-    static bool init = (cudaFuncSetAttribute(k_conv_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcShape<true>::SMEM),
-                        cudaFuncSetAttribute(k_conv_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcShape<false>::SMEM),
-                        true);
-    (void)init;
+    smem_opt_in(kern, smem);
     const long long rows = 2LL * nl, nj = R.n / TC_M;
     const long long blocks = rows * nj * g.pixels * ((g.oc + oc_tile - 1) / oc_tile);
     if (blocks > 0x7fffffffLL) throw std::runtime_error("tc_mac: grid too large");

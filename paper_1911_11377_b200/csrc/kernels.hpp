@@ -95,6 +95,14 @@ struct Launch {
 
 void check_launch(const char* what);
 void cuda_check(cudaError_t e, const char* what);  // throws std::runtime_error on failure
+// Dynamic shared memory above 48 KB for `kernel` on the current device. The
+// attribute lives in each device's context, so it is set once per (kernel,
+// device, size), not once per process: a process driving two GPUs sets both.
+void smem_opt_in(const void* kernel, int bytes);
+template <class K>
+void smem_opt_in(K* kernel, int bytes) {
+    smem_opt_in(reinterpret_cast<const void*>(kernel), bytes);
+}
 
 // ---- NTT (ntt.cu). polys: [count][level+1][n], limb index = poly % (level+1)
 void ntt_forward(const DevRing& R, u64* polys, int level, std::size_t count, const Launch& L);

@@ -990,14 +990,7 @@ const u64* run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, co
     // data + staged twiddles (u64 Shoup pairs on the integer path; double
     // twiddles + the b_t stage or c1 accumulators on the FP64 path) + mbarriers
     const int smem = P::B * (8 + 16) + 64;
-    static bool init = (smem > 48 * 1024
-                            ? (cudaFuncSetAttribute(pick(true, false), cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                               cudaFuncSetAttribute(pick(false, false), cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                               cudaFuncSetAttribute(pick(true, true), cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                               cudaFuncSetAttribute(pick(false, true), cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                               true)
-                            : true);
-    (void)init;
+    smem_opt_in(kern, smem);
     const int limbs = level + 1;
     const unsigned long long lmask = limbs >= 64 ? ~0ull : (1ull << limbs) - 1;
     const unsigned long long int_mask = R.int_limbs & lmask;
@@ -1066,11 +1059,7 @@ const u64* run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, co
         constexpr int MB = LOGN <= 13 ? 2 : 1;
         auto kc = k_aux_crt_ntt<LOGN, TN, MB>;
         const int csm = (1 << LOGN) * 8;
-        static const bool cinit = [&] {
-            if (csm > 48 * 1024) cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, csm);
-            return true;
-        }();
-        (void)cinit;
+        smem_opt_in(kc, csm);
         const double cells = double(count) * 2 * (1 << LOGN);
         L.begin("k_ks_aux_crt_ntt", cells * (LOGN / 2.0 + 6), 8.0 * cells * 4);
         kc<<<static_cast<unsigned>(count * 2), TN, csm, L.stream>>>(R, aux_scratch, e0);

@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256) k_ntt_inv_cols(DevRing R, u64* __restrict
 
 template <class K>
 void set_smem(K kernel, int bytes) {
-    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    smem_opt_in(kernel, bytes);
 }
 
 #ifndef HECNN_NTT_LOGE
@@ -289,8 +289,7 @@ void run_forward(const DevRing& R, const u64* src, u64* data, int limbs, std::si
     }
     auto kern = k_ntt_fwd_block<LOGN, P::LOGB, P::LOGE, P::THREADS, P::MINB>;
     const int smem = (1 << P::LOGB) * 8;
-    static bool init = (set_smem(kern, smem), true);
-    (void)init;
+    set_smem(kern, smem);
     L.begin("k_ntt_fwd_block", double(polys) * (1 << (LOGN - 1)) * P::LOGB, 16.0 * polys * (1 << LOGN));
     kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, src, data, limbs);
     L.count();
@@ -301,8 +300,7 @@ void run_inverse(const DevRing& R, u64* data, int limbs, std::size_t polys, cons
     using P = NttPlan<LOGN>;
     auto kern = k_ntt_inv_block<LOGN, P::LOGB, P::LOGE, P::THREADS, P::MINB>;
     const int smem = (1 << P::LOGB) * 8;
-    static bool init = (set_smem(kern, smem), true);
-    (void)init;
+    set_smem(kern, smem);
     L.begin("k_ntt_inv_block", double(polys) * (1 << (LOGN - 1)) * P::LOGB, 16.0 * polys * (1 << LOGN));
     kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, data, limbs);
     L.count();
@@ -320,8 +318,7 @@ void run_inverse_product(const DevRing& R, const u64* x, const u64* y, u64* d2, 
     using P = NttPlan<LOGN>;
     auto kern = k_ntt_inv_prod<LOGN, P::LOGB, P::LOGE, P::THREADS, P::MINB>;
     const int smem = (1 << P::LOGB) * 8;
-    static bool init = (set_smem(kern, smem), true);
-    (void)init;
+    set_smem(kern, smem);
     L.begin("k_ntt_inv_block", double(polys) * ((1 << (LOGN - 1)) * P::LOGB + (1 << LOGN)), 24.0 * polys * (1 << LOGN));
     kern<<<static_cast<unsigned>(polys << P::C), P::THREADS, smem, L.stream>>>(R, x, y, d2, limbs);
     L.count();
@@ -389,8 +386,8 @@ bool run_inverse_rescale(const DevRing& R, u64* d, u64* out, int limbs, std::siz
         auto ktop = k_ntt_inv_sel<LOGN, P::LOGE, P::THREADS, P::MINB, false>;
         auto kres = k_ntt_inv_sel<LOGN, P::LOGE, P::THREADS, P::MINB, true>;
         const int smem = (1 << LOGN) * 8;
-        static bool init = (set_smem(ktop, smem), set_smem(kres, smem), true);
-        (void)init;
+        set_smem(ktop, smem);
+        set_smem(kres, smem);
         const double bfly = double(1 << (LOGN - 1)) * LOGN, nn = double(1 << LOGN);
         L.begin("k_ntt_inv_block", double(groups) * bfly, 16.0 * groups * nn);
         ktop<<<static_cast<unsigned>(groups), P::THREADS, smem, L.stream>>>(R, d, out, limbs, limbs - 1, 1, nullptr);
@@ -414,8 +411,7 @@ void run_inverse_limbs(const DevRing& R, u64* data, int limbs, int limb0, int ns
     } else {
         auto kern = k_ntt_inv_sel<LOGN, P::LOGE, P::THREADS, P::MINB, false>;
         const int smem = (1 << LOGN) * 8;
-        static bool init = (set_smem(kern, smem), true);
-        (void)init;
+        set_smem(kern, smem);
         const std::size_t polys = groups * static_cast<std::size_t>(nsel);
         L.begin(name ? name : "k_ntt_inv_block", double(polys) * (1 << (LOGN - 1)) * LOGN, 16.0 * polys * (1 << LOGN));
         kern<<<static_cast<unsigned>(polys), P::THREADS, smem, L.stream>>>(R, data, data, limbs, limb0, nsel, nullptr);

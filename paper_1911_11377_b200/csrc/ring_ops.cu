@@ -5,6 +5,9 @@
 // so a warp reads 256 contiguous bytes of one limb and the limb's modulus
 // constants are uniform across the CTA.
 
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 
@@ -426,6 +429,18 @@ __global__ void k_fp_table(DevRing R, const u64* __restrict__ in, double* __rest
     out[row * R.n + j] = static_cast<double>(in[row * R.n + j]);  // exact: residues < 2^53
 }
 }  // namespace
+
+void smem_opt_in(const void* kernel, int bytes) {
+    if (bytes <= 48 * 1024) return;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.emplace(kernel, dev, bytes).second)
+        cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                   "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+}
 
 void fp_table(const DevRing& R, const u64* in, double* out, int limbs, std::size_t count, const Launch& L) {
     const std::size_t rows = count * limbs;
