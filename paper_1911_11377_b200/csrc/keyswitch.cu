@@ -927,31 +927,56 @@ __global__ void k_limb0_combine(DevRing R, u64* __restrict__ acc01, const u64* _
 __global__ void k_limb0_crt_combine(DevRing R, u64* __restrict__ acc01, const u64* __restrict__ aux_out,
                                     u64* __restrict__ e0, const u64* __restrict__ fy, int limbs, int mode,
                                     long long count) {
+    // two consecutive coefficients per thread (16-byte accesses); the four CRT
+    // chains (2 coefficients x 2 components) are independent
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= count * R.n) return;
-    const long long ct = t / R.n, n = R.n;
-    const int j = static_cast<int>(t % R.n);
+    const long long n = R.n;
+    if (t >= count * (n >> 1)) return;
+    const long long ct = t / (n >> 1);
+    const int j = static_cast<int>(t % (n >> 1)) * 2;
+    u64 res[2][2][3];
 #pragma unroll
-    for (int comp = 0; comp < 2; ++comp) {
-        const u64* a1 = aux_out + ((ct * 2 + comp) * 4 + 1) * n + j;
-        const u64 res[3] = {a1[0], a1[n], a1[2 * n]};
-        e0[(ct * 2 + comp) * n + j] = aux_crt_value(R, res);
-    }
+    for (int comp = 0; comp < 2; ++comp)
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(aux_out + ((ct * 2 + comp) * 4 + 1 + s) * n + j));
+            res[comp][0][s] = v.x, res[comp][1][s] = v.y;
+        }
+    u64 e[2][2];
+#pragma unroll
+    for (int comp = 0; comp < 2; ++comp)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) e[comp][h] = aux_crt_value(R, res[comp][h]);
+#pragma unroll
+    for (int comp = 0; comp < 2; ++comp)
+        *reinterpret_cast<ulonglong2*>(e0 + (ct * 2 + comp) * n + j) = make_ulonglong2(e[comp][0], e[comp][1]);
     if (mode == 0) return;
     const ModConst m = R.mod[0];
     u64* o0 = acc01 + (ct * 2) * limbs * n + j;
     u64* o1 = o0 + static_cast<long long>(limbs) * n;
-    const u64 xa = *o0, xb = *o1;
+    const ulonglong2 xa = *reinterpret_cast<const ulonglong2*>(o0), xb = *reinterpret_cast<const ulonglong2*>(o1);
+    const u64 a[2] = {xa.x, xa.y}, bb[2] = {xb.x, xb.y};
+    u64 r0[2], r1[2];
     if (mode == 1) {
-        *o0 = mul_mod(xa, xa, m);
-        const u64 c = mul_mod(xa, xb, m);
-        *o1 = add_mod(c, c, m.q);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            r0[h] = mul_mod(a[h], a[h], m);
+            const u64 c = mul_mod(a[h], bb[h], m);
+            r1[h] = add_mod(c, c, m.q);
+        }
     } else {
         const u64* y0 = fy + (ct * 2) * limbs * n + j;
-        const u64 va = y0[0], vb = y0[static_cast<long long>(limbs) * n];
-        *o0 = mul_mod(xa, va, m);
-        *o1 = add_mod(mul_mod(xa, vb, m), mul_mod(xb, va, m), m.q);
+        const ulonglong2 va2 = *reinterpret_cast<const ulonglong2*>(y0);
+        const ulonglong2 vb2 = *reinterpret_cast<const ulonglong2*>(y0 + static_cast<long long>(limbs) * n);
+        const u64 va[2] = {va2.x, va2.y}, vb[2] = {vb2.x, vb2.y};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            r0[h] = mul_mod(a[h], va[h], m);
+            r1[h] = add_mod(mul_mod(a[h], vb[h], m), mul_mod(bb[h], va[h], m), m.q);
+        }
     }
+    *reinterpret_cast<ulonglong2*>(o0) = make_ulonglong2(r0[0], r0[1]);
+    *reinterpret_cast<ulonglong2*>(o1) = make_ulonglong2(r1[0], r1[1]);
 }
 
 // aux_tab build: rows of B (coefficients mod q0) -> slot s of [rows][4][n] = B mod q_s
@@ -1050,7 +1075,7 @@ const u64* run_keyswitch(const DevRing& R, const u32* digits, const u64* evk, co
         const long long pos = static_cast<long long>(count) << LOGN;
         if (defer) {
             L.begin("k_ks_aux_crt", double(pos) * 2 * 12, 8.0 * pos * (6 + 2 + (mode ? 4 : 0) + (mode == 2 ? 2 : 0)));
-            k_limb0_crt_combine<<<static_cast<unsigned>((pos + 255) / 256), 256, 0, L.stream>>>(
+            k_limb0_crt_combine<<<static_cast<unsigned>((pos / 2 + 255) / 256), 256, 0, L.stream>>>(
                 R, acc01, aux_scratch, e0, fy, limbs, mode, static_cast<long long>(count));
             L.count();
             return e0;
