@@ -62,6 +62,10 @@ __global__ void k_elementwise(DevRing R, int op, const u64* __restrict__ a, cons
 #ifndef HECNN_RESCALE_VEC
 #define HECNN_RESCALE_VEC 2  // coefficients per thread (16-byte loads / stores when 2)
 #endif
+#ifndef HECNN_RESCALE_UNROLL
+#define HECNN_RESCALE_UNROLL 1  // limbs per loop iteration
+#endif
+constexpr int kRescaleUnroll = HECNN_RESCALE_UNROLL;
 template <bool SCALED, bool ADD, bool RS = false>
 __global__ void __launch_bounds__(TPB, HECNN_RESCALE_MINB) k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level,
                           const ulonglong2* __restrict__ c, SumTerms t) {
@@ -113,6 +117,7 @@ __global__ void __launch_bounds__(TPB, HECNN_RESCALE_MINB) k_rescale(DevRing R, 
             wf[h] = ntt::to_fp(w[h] & ((1ull << 51) - 1));
         }
     }
+#pragma unroll kRescaleUnroll
     for (int i = 0; i < level; ++i) {
         const ModConst m = R.mod[i];
         const ulonglong2 inv = R.inv_dropped[level * R.limbs + i];

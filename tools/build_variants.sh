@@ -4,8 +4,10 @@ set -e
 cd "$(dirname "$0")/.."
 declare -A V
 V[na]=""
-V[col512]="-DHECNN_KS_MAXT_COL=512"
-V[col512m]="-DHECNN_KS_MAXT_COL=512 -DHECNN_KS_LOGE=3"
+V[u2]="-DHECNN_RESCALE_UNROLL=2"
+V[u2m4]="-DHECNN_RESCALE_UNROLL=2 -DHECNN_RESCALE_MINB=4"
+V[u4m4]="-DHECNN_RESCALE_UNROLL=4 -DHECNN_RESCALE_MINB=4"
+V[m4]="-DHECNN_RESCALE_MINB=4"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null

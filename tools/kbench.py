@@ -59,6 +59,12 @@ def main():
         g = lambda: hb._check(hb.lib().hecnn_ntt_inverse(eng.ctx, d, L, 1024))  # noqa: E731
         res["ntt_fwd_8192"] = timed(eng, f)[1]
         res["ntt_inv_8192"] = timed(eng, g)[1]
+    if "rescale" in which:
+        # C4 conv1's rescale shape: 16384 ciphertexts, level 8 -> 7 (one of the HBM-bound streams)
+        x = eng.tensor_from_words(uniform_words(p, 4096, L), L, p.scale)
+        res["rescale_l8_4096"] = timed(eng, lambda: eng.rescale(x))[1]
+        y = eng.tensor_from_words(uniform_words(p, 4096, L), L, p.scale)
+        res["add_l8_4096"] = timed(eng, lambda: eng.add(x, y))[1]
     if "ks" in which or "square" in which:
         lv = 7
         x = eng.tensor_from_words(uniform_words(p, 512, lv), lv, p.scale)
