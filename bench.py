@@ -634,6 +634,18 @@ def run_ours(args):
             "int_shoup_peak": int_only_peak / 1e9,
             "hbm_view": {"achieved_gbs": achieved_gbs, "peak_gbs": pk["hbm_gbs"], "frac": achieved_gbs / pk["hbm_gbs"]},
         }
+        # the standalone NTT kernels (north star: >= 50% of roofline on NTT and key
+        # switch); an N = 2^13 limb-NTT is balanced between the FP64 pipe and HBM,
+        # so its roofline time is the larger of the two
+        ntt_roof = {}
+        for kname in ("k_ntt_fwd_block", "k_ntt_inv_block", "k_ntt_inv_rescale"):
+            v = prof.get(kname)
+            if v and v["ms"] > 0:
+                ops_s, gbs = v["ops"] / (v["ms"] / 1e3), v["bytes"] / (v["ms"] / 1e3) / 1e9
+                ntt_roof[kname] = {"achieved_gmodmul_s": ops_s / 1e9, "achieved_gbs": gbs,
+                                   "frac": max(ops_s / int_peak, gbs / pk["hbm_gbs"]),
+                                   "ms_per_step": v["ms"] / args.steps}
+        roofline["ntt_kernels"] = ntt_roof
         kernels = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
                        "gmodmul_s": (v["ops"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0,
                        "gb_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0}
