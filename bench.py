@@ -252,6 +252,25 @@ def c5_measured(hb, device, stream=None, image=32, check=8, with_reference=True)
     res["64x64_extrapolated"] = {"seconds_per_set": t64, "images_per_s": (p.n // 2) / t64,
                                  "method": "measured 32x32 per-layer times x exact per-layer work ratios"}
     del y, x, model
+    if image == 32:
+        # the same method one size down, on the same stack: a measured 16x16 set
+        # extrapolated to 32x32 against the measured 32x32 set above (warm weight
+        # caches excluded: the 16x16 pass builds its own)
+        spec16 = hb.glorot_weights(hb.alexnet32_preset(image=16), 1)
+        d16 = np.random.default_rng(3).uniform(0, 1, size=(p.n // 2, spec16.input.positions()))
+        x16 = eng.encrypt_tensor(d16, seed=11, shape=spec16.input)
+        m16 = eng.model(spec16)
+        s16 = []
+        hb.forward_encrypted(m16, x16, eng, seed=13)  # caches and plans
+        s.record()
+        hb.forward_encrypted(m16, x16, eng, seed=13, layer_seconds=s16)
+        e.record()
+        torch.cuda.synchronize()
+        w16 = layer_work(hb, spec16)
+        t32 = sum(v * (b / a if a else 1.0) for v, a, b in zip(s16, w16, w32))
+        res["method_check_on_c5"] = {"from": "16x16 (measured, warm)", "to": "32x32", "extrapolated_s": t32,
+                                     "measured_s": sec, "ratio": t32 / sec, "measured_16x16_s": s.elapsed_time(e) / 1e3}
+        del x16, m16
     eng.close()
     if with_reference:
         from oracle import ref
