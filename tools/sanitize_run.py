@@ -1,7 +1,8 @@
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
 synccheck, one tool per run): the smoke C1 forward + HE square, the N = 2^13
-and N = 2^14 key switch (both CTA groups, column stage), an 11x11 tcgen05
-conv, and a row-streamed forward whose rings wrap. Exits 0 when every
+and N = 2^14 key switch (limb 0 through limbs 1..3, column stage), the raw key
+switch, a fused degree-2 activation, the scalar / plaintext ops, an 11x11
+tcgen05 conv, and a row-streamed forward whose rings wrap. Exits 0 when every
 result still matches (sanitizer output is checked by the caller)."""
 import os
 import sys
@@ -22,6 +23,21 @@ for preset, lv, cells in (("net-n8192-d8", 7, 3), ("large-n16384-d24", 4, 2)):
     b = e.mul(x, x).words()
     assert np.array_equal(a, b), "square != mul(x, x)"
     print(preset, "square == mul(x, x)", flush=True)
+
+# raw key switch (NTT-domain output: the aux route's CRT + forward NTT mod q0 and combine),
+# a degree-2 activation (its linear term fused into the last rescale), the scalar fast path
+p = hb.preset_params("net-n8192-d8")
+e = hb.CkksEngine(p).keygen(1)
+d2 = uniform_words(p, 2, 5)[:, 0]
+ks = e.key_switch(d2, 5)
+act = e.eval_activation(hb.relu_default_surrogate(), e.tensor_from_words(uniform_words(p, 3, 6), 6, p.scale))
+x = e.tensor_from_words(uniform_words(p, 3, 6), 6, p.scale)
+acc = e.make_zero_ciphertext(6, p.scale * p.scale, 3)
+e.mul_scalar_mac(acc, x, [e.make_scalar_plain(w, p.scale, 6) for w in (0.5, -0.25, 1.0)])
+e.add_scalar_inplace(acc, 0.125)
+m = e.mul_plain(x, e.encode_real(np.linspace(-1, 1, 16), 2.0 ** 30, 6))
+a2 = e.add_plain(x, e.encode_const(0.5, p.scale, 6))
+print("key switch / activation / scalar ops ok", ks.shape, act.level, m.level, flush=True)
 
 p = hb.preset_params("net-n8192-d8")
 e = hb.CkksEngine(p).keygen(2)
