@@ -910,7 +910,11 @@ static TensorPtr eval_activation_cells(Context& C, const Activation& act, const 
         const std::uint32_t lvl = p.level - (p.level ? 1 : 0);
         bool fuse = p.level > 0 && terms.size() + 1 <= static_cast<std::size_t>(kMaxTerms);
         for (auto& t : terms) fuse = fuse && t->level >= lvl;
-        if (lazy && !(fuse && x.level - 1 >= lvl)) materialize_lazy();
+        // the fused kernel reads x for the lazy term: not when its output would overwrite x
+        const auto xb = reinterpret_cast<std::uintptr_t>(x.data()), db = reinterpret_cast<std::uintptr_t>(dst);
+        const bool dst_overlaps_x = dst && db < xb + x.cells * x.cell_words() * 8 &&
+                                    xb < db + x.cells * 2 * (lvl + 1) * C.n() * 8;
+        if (lazy && !(fuse && x.level - 1 >= lvl && !dst_overlaps_x)) materialize_lazy();
         if (fuse) {
             DevBuf dc = mul_const_table(C, p, act.coefficients[d], u);
             const double sc = p.scale * u / static_cast<double>(C.ring.primes[p.level]);
