@@ -131,9 +131,26 @@ __global__ void __launch_bounds__(THREADS, MINB) k_ntt_inv_sel(DevRing R, u64* _
     if (ntt::fp_limb(q)) {
         const ntt::FpArith ar{static_cast<double>(q), R.inv_q[limb]};
         const double ni = R.n_inv_f[limb];
-        ntt::inv_block<LOGN, LOGE, THREADS>(
-            reinterpret_cast<double*>(smem), ar, R.inv_f + toff, 0, 0, [=](int i) { return ntt::to_fp(g[i]); },
-            [=](int i, double v, int, int) { store(i, ntt::fcanon(ntt::fmodmul(v, ni, ar.q, ar.qinv), ar.q, ar.qinv)); });
+        if constexpr (RESCALE) {
+            // the rescale on the FP64 pipe too: (c - centre(top)) p_L^-1 with exact
+            // FP64 modmuls (|x - cen| < 3q); the canonical result is the integer path's
+            const u64 qtop_half = R.mod[L].q >> 1;
+            const double pm = ntt::to_fp(R.p_mod[L * R.limbs + limb]);
+            const double invf = ntt::to_fp(R.inv_dropped[L * R.limbs + limb].x);
+            ntt::inv_block<LOGN, LOGE, THREADS>(
+                reinterpret_cast<double*>(smem), ar, R.inv_f + toff, 0, 0, [=](int i) { return ntt::to_fp(g[i]); },
+                [=](int i, double v, int, int) {
+                    const double x = ntt::fmodmul(v, ni, ar.q, ar.qinv);
+                    const u64 vt = top[i];
+                    double cen = ntt::fcentre(ntt::to_fp(vt), ar.q, ar.qinv);
+                    if (vt > qtop_half) cen -= pm;
+                    o[i] = ntt::fcanon(ntt::fmodmul(x - cen, invf, ar.q, ar.qinv), ar.q, ar.qinv);
+                });
+        } else {
+            ntt::inv_block<LOGN, LOGE, THREADS>(
+                reinterpret_cast<double*>(smem), ar, R.inv_f + toff, 0, 0, [=](int i) { return ntt::to_fp(g[i]); },
+                [=](int i, double v, int, int) { store(i, ntt::fcanon(ntt::fmodmul(v, ni, ar.q, ar.qinv), ar.q, ar.qinv)); });
+        }
     } else {
         const ntt::IntArith ar{q, q << 1};
         const ulonglong2 ni = R.n_inv[limb];
