@@ -66,8 +66,11 @@ __global__ void k_elementwise(DevRing R, int op, const u64* __restrict__ a, cons
 #define HECNN_RESCALE_UNROLL 1  // limbs per loop iteration
 #endif
 constexpr int kRescaleUnroll = HECNN_RESCALE_UNROLL;
+#ifndef HECNN_RESCALE_MINB_ADD
+#define HECNN_RESCALE_MINB_ADD 4  // the fused term sums need more than 32 registers (they spilled 132-288 B)
+#endif
 template <bool SCALED, bool ADD, bool RS = false>
-__global__ void __launch_bounds__(TPB, HECNN_RESCALE_MINB) k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level,
+__global__ void __launch_bounds__(TPB, ADD ? HECNN_RESCALE_MINB_ADD : HECNN_RESCALE_MINB) k_rescale(DevRing R, const u64* __restrict__ in, u64* __restrict__ out, int level,
                           const ulonglong2* __restrict__ c, SumTerms t) {
     constexpr int VW = HECNN_RESCALE_VEC;
     const int j = (blockIdx.y * TPB + threadIdx.x) * VW;

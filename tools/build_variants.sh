@@ -4,10 +4,10 @@ set -e
 cd "$(dirname "$0")/.."
 declare -A V
 V[na]=""
-V[u2]="-DHECNN_RESCALE_UNROLL=2"
-V[u2m4]="-DHECNN_RESCALE_UNROLL=2 -DHECNN_RESCALE_MINB=4"
-V[u4m4]="-DHECNN_RESCALE_UNROLL=4 -DHECNN_RESCALE_MINB=4"
-V[m4]="-DHECNN_RESCALE_MINB=4"
+V[a3]="-DHECNN_RESCALE_MINB_ADD=3"
+V[a2]="-DHECNN_RESCALE_MINB_ADD=2"
+V[p6]="-DHECNN_RESCALE_MINB=6"
+V[a5]="-DHECNN_RESCALE_MINB_ADD=5"
 for name in "${!V[@]}"; do
   [ -n "$1" ] && [[ ! " $* " =~ " $name " ]] && continue
   make -s -C paper_1911_11377_b200/csrc -j8 OUT=$PWD/build_variants/$name OBJ=$PWD/build_variants/$name/obj EXTRA_NVFLAGS="${V[$name]}" >/dev/null
