@@ -377,13 +377,12 @@ Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, doubl
         for (int a = 0; a < 3; ++a) {
             const u64 qa = ring.primes[1 + a];
             const u128 Ma = Pq / qa;
-            dev.aux_M[a][0] = static_cast<u64>(Ma), dev.aux_M[a][1] = static_cast<u64>(Ma >> 64);
             const u64 inv = ring.mods[1 + a].inv(static_cast<u64>(Ma % qa));
             dev.aux_inv[a] = make_ulonglong2(inv, shoup_of(inv, qa));
+            const u64 mq0 = static_cast<u64>(Ma % ring.primes[0]);
+            dev.aux_Mq0[a] = make_ulonglong2(mq0, shoup_of(mq0, ring.primes[0]));
         }
-        dev.aux_P[0] = static_cast<u64>(Pq), dev.aux_P[1] = static_cast<u64>(Pq >> 64);
-        const u128 Ph = Pq >> 1;
-        dev.aux_Ph[0] = static_cast<u64>(Ph), dev.aux_Ph[1] = static_cast<u64>(Ph >> 64);
+        for (int k = 0; k < 4; ++k) dev.aux_kPq0[k] = static_cast<u64>((Pq % ring.primes[0]) * k % ring.primes[0]);
         dev.aux_log2P = std::log2(static_cast<double>(ring.primes[1])) + std::log2(static_cast<double>(ring.primes[2])) +
                         std::log2(static_cast<double>(ring.primes[3]));
     }

@@ -41,9 +41,9 @@ struct DevRing {
     // aux_tab [Dtop][2][4][n] = NTT_{q_s}(INTT_{q0}(evk[t][c][0]) mod q_s) as
     // doubles in slots s = 1..3; CRT constants of P = q1 q2 q3.
     const double* aux_tab = nullptr;
-    u64 aux_M[3][2] = {};                    // P / q_s, 128-bit (lo, hi)
     ulonglong2 aux_inv[3] = {};              // ((P / q_s) mod q_s)^-1 mod q_s, Shoup
-    u64 aux_P[2] = {}, aux_Ph[2] = {};       // P and floor(P / 2)
+    ulonglong2 aux_Mq0[3] = {};              // (P / q_s) mod q0, Shoup
+    u64 aux_kPq0[4] = {};                    // k P mod q0, k = 0..3
     double aux_log2P = 0.0;
     bool small_primes = false;               // some q_i <= 2^20: key-switch digits need v mod q_i
 };

@@ -839,36 +839,25 @@ struct KsPlan {
 // each limb, a 3-prime CRT and a forward NTT mod q0. The 60-bit limb's D
 // integer-pipe digit NTTs disappear; every word stays the reference's.
 
-// E mod q_s (s = 1..3, canonical) -> centred E mod q0
+// E mod q_s (s = 1..3, canonical) -> centred E mod q0. X = sum_s y_s (P / q_s)
+// with y_s = r_s (P / q_s)^-1 mod q_s is E + k P, k = rint(sum_s y_s / q_s)
+// (= X / P, whose distance to k is |E| / P < 1/4: keyswitch_aux_ok keeps that
+// margin, far above the double sum's 2^-50 error), so
+// E mod q0 = sum_s y_s ((P / q_s) mod q0) - k (P mod q0): three Shoup
+// products mod q0, no 128-bit arithmetic
 __device__ __forceinline__ u64 aux_crt_value(const DevRing& R, const u64 (&res)[3]) {
-    u64 lo = 0, hi = 0;
+    const u64 q0 = R.mod[0].q;
+    double f = 0.0;
+    u64 acc = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const ModConst m = R.mod[1 + a];
-        const u64 r = res[a];
-        const u64 y = mul_shoup(r, R.aux_inv[a].x, R.aux_inv[a].y, m.q);  // < q_s < 2^42
-        // += y * M_a (M_a < 2^84): 128-bit multiply-add
-        const u64 p_lo = y * R.aux_M[a][0], p_hi = mulhi(y, R.aux_M[a][0]) + y * R.aux_M[a][1];
-        const u64 s = lo + p_lo;
-        hi += p_hi + (s < lo ? 1 : 0);
-        lo = s;
+        const u64 qa = R.mod[1 + a].q;
+        const u64 y = mul_shoup(res[a], R.aux_inv[a].x, R.aux_inv[a].y, qa);  // < q_s < 2^42
+        f += static_cast<double>(y) * R.inv_q[1 + a];
+        acc = add_mod(acc, mul_shoup(y, R.aux_Mq0[a].x, R.aux_Mq0[a].y, q0), q0);
     }
-    // X < 3P: reduce to [0, P)
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const bool ge = hi > R.aux_P[1] || (hi == R.aux_P[1] && lo >= R.aux_P[0]);
-        if (ge) {
-            const u64 nlo = lo - R.aux_P[0];
-            hi = hi - R.aux_P[1] - (lo < R.aux_P[0] ? 1 : 0);
-            lo = nlo;
-        }
-    }
-    const ModConst m0 = R.mod[0];
-    if (hi < R.aux_Ph[1] || (hi == R.aux_Ph[1] && lo <= R.aux_Ph[0])) return reduce128(lo, hi, m0);  // E = X >= 0
-    // E = X - P < 0: -(P - X) mod q0
-    const u64 dlo = R.aux_P[0] - lo, dhi = R.aux_P[1] - hi - (R.aux_P[0] < lo ? 1 : 0);
-    const u64 v = reduce128(dlo, dhi, m0);
-    return v ? m0.q - v : 0;
+    const int k = static_cast<int>(rint(f));
+    return sub_mod(acc, R.aux_kPq0[k], q0);
 }
 
 // CRT of each coefficient fused into the first round of the forward NTT mod
