@@ -66,3 +66,37 @@ def test_raw_key_switch_with_imported_keys(ref):
         orc.or_key_switch(ctypes.c_size_t(n), _p(primes), ctypes.c_size_t(top), _p(roots), ctypes.c_size_t(level),
                           _p(np.ascontiguousarray(d2)), _p(evk_c), _p(want))
         assert np.array_equal(got, want), f"key switch at level {level}"
+
+
+@pytest.mark.parametrize("preset,level", [("net-n8192-d8", 7), ("large-n16384-d24", 23), ("large-n16384-d24", 2)])
+def test_key_switch_crt_extremes(ref, preset, level):
+    """The CRT digits (k_crt_digits) at the edges of [0, Q): coefficients
+    with x = Q - 1 (residues q_i - 1: the quotient estimate sum_i w_i/q_i sits
+    just below an integer and the exact fix-up decides), x = 0, x = 1 and a
+    single-limb residue, the rest uniform -- the key switch against the C
+    restatement with the reference's keys."""
+    p = hb.preset_params(preset)
+    r = ref.RefEngine.from_params(p).keygen(5)
+    s, b, a, evk = r.export_keys()
+    eng = hb.CkksEngine(p)
+    eng.import_keys(secret=s, pk_b=b, pk_a=a, evk=evk)
+    orc = _orc()
+    n, top = p.n, p.top_level
+    primes = np.array(p.primes, dtype=np.uint64)
+    roots = np.zeros((top + 1, n), np.uint64)
+    iroots = np.zeros(n, np.uint64)
+    ninv = ctypes.c_uint64()
+    for i, q in enumerate(p.primes):
+        assert orc.or_ntt_tables(ctypes.c_size_t(n), ctypes.c_uint64(q), _p(roots[i]), _p(iroots), ctypes.byref(ninv)) == 0
+    d2 = r.sample_uniform(level, 91 + level)
+    q = primes[: level + 1, None]
+    d2[:, 0:64] = q - 1                      # x = Q - 1
+    d2[:, 64:128] = 0                        # x = 0
+    d2[:, 128:192] = 1                       # x = 1
+    d2[:, 192:256] = 0
+    d2[0, 192:256] = 1                       # x = Q/q_0 * [(Q/q_0)^-1 mod q_0]
+    got = eng.key_switch(d2[None], level)[0]
+    want = np.zeros((2, level + 1, n), np.uint64)
+    orc.or_key_switch(ctypes.c_size_t(n), _p(primes), ctypes.c_size_t(top), _p(roots), ctypes.c_size_t(level),
+                      _p(np.ascontiguousarray(d2)), _p(np.ascontiguousarray(evk)), _p(want))
+    assert np.array_equal(got, want)
