@@ -332,6 +332,20 @@ Context::Context(std::size_t n, const std::vector<u64>& primes, double sc, doubl
     dev.punct = tables.back().as<u64>();
     tables.push_back(upload_vec(ring.modulus));
     dev.modulus = tables.back().as<u64>();
+    {
+        // Garner's mixed-radix constants for k_crt_digits_garner (FP64 limbs only)
+        std::vector<double> gi(ring.limbs * ring.limbs, 0.0), c30(ring.limbs, 0.0);
+        for (std::size_t i = 1; i < ring.limbs; ++i) {
+            if (ring.primes[i] >= (1ull << 42)) continue;
+            c30[i] = static_cast<double>((1ull << 30) % ring.primes[i]);
+            for (std::size_t j = 0; j < i; ++j)
+                gi[i * ring.limbs + j] = static_cast<double>(ring.mods[i].inv(ring.primes[j] % ring.primes[i]));
+        }
+        tables.push_back(upload_vec(gi));
+        dev.garner_inv = tables.back().as<double>();
+        tables.push_back(upload_vec(c30));
+        dev.garner_c30 = tables.back().as<double>();
+    }
     tables.push_back(upload_vec(inv_q));
     dev.inv_q = tables.back().as<double>();
     tables.push_back(upload_vec(ring.fwd_f));

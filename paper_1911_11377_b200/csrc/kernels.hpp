@@ -26,6 +26,8 @@ struct DevRing {
     const ulonglong2* punct_inv = nullptr;   // [limbs][limbs] ((Q_l/q_i)^-1 mod q_i, shoup)
     const u64* punct = nullptr;              // [limbs][limbs][crt_words] Q_l/q_i
     const u64* modulus = nullptr;            // [limbs][crt_words] Q_l
+    const double* garner_inv = nullptr;      // [i][j] q_j^-1 mod q_i (j < i, FP64 limbs i), exact doubles
+    const double* garner_c30 = nullptr;      // [i] 2^30 mod q_i
     const double* inv_q = nullptr;           // [limbs] 1/q_i
     // FP64-path tables (limbs with q < 2^42): residues as exact doubles
     const double* fwd_f = nullptr;           // [limbs][n]

@@ -131,6 +131,73 @@ __global__ void __launch_bounds__(128) k_crt_digits(DevRing R, const u64* __rest
     }
 }
 
+// The same digits through Garner's mixed radix: x = v_0 + q_0 (v_1 + q_1 (v_2 + ...))
+// with v_i = ((a_i - v_0) q_0^-1 - v_1) q_1^-1 - ... mod q_i in [0, q_i): the
+// O(l^2 / 2) mixed-radix digits run as exact FP64 modmuls (limbs 1..l, q_i < 2^42;
+// the 60-bit v_0 enters as two 30-bit halves), then a Horner pass of l
+// multiword-by-prime products on the integer pipes, whose length grows with
+// the partial product -- half the 64-bit multiply-adds of the sum of
+// Q/q_i multiples above, and no quotient estimate: x lands in [0, Q) exactly.
+// Only chains whose 60-bit limb is limb 0 alone (the presets).
+template <int W>
+__global__ void __launch_bounds__(128) k_crt_digits_garner(DevRing R, const u64* __restrict__ d2,
+                                                           u32* __restrict__ digits, int level, int D, long long count) {
+    extern __shared__ u64 sv[];  // mixed-radix digits [limb][thread]
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= count * R.n) return;
+    const long long ct = t / R.n;
+    const int j = static_cast<int>(t % R.n);
+    const int limbs = level + 1, T = blockDim.x, tid = threadIdx.x;
+    const u64* a = d2 + ct * limbs * R.n + j;
+    const u64 v0 = a[0];
+    const double v0h = ntt::to_fp(v0 >> 30), v0l = ntt::to_fp(v0 & ((1ull << 30) - 1));
+    // (a column order -- every t_i stepped once v_k is known, the t_i in shared
+    // memory -- was measured slower: the extra shared-memory traffic outweighs the ILP)
+    for (int i = 1; i < limbs; ++i) {
+        const double q = static_cast<double>(R.mod[i].q), qinv = R.inv_q[i];
+        const double* gi = R.garner_inv + i * R.limbs;
+        double v = ntt::to_fp(a[static_cast<long long>(i) * R.n]) - (ntt::fmodmul(v0h, R.garner_c30[i], q, qinv) + v0l);
+        v = ntt::fmodmul(v, gi[0], q, qinv);
+        for (int k = 1; k < i; ++k) v = ntt::fmodmul(v - ntt::to_fp(sv[k * T + tid]), gi[k], q, qinv);
+        sv[i * T + tid] = ntt::fcanon(v, q, qinv);
+    }
+    u64 acc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) acc[w] = 0;
+    acc[0] = level ? sv[level * T + tid] : v0;
+    int nw = 1;
+    for (int i = level - 1; i >= 0; --i) {
+        const u64 qi = R.mod[i].q;
+        u64 carry = i ? sv[i * T + tid] : v0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            if (w < nw) {
+                u64 lo = acc[w] * qi, hi = mulhi(acc[w], qi);
+                lo += carry;
+                hi += lo < carry;
+                acc[w] = lo;
+                carry = hi;
+            } else if (w == nw) {
+                acc[w] = carry;
+            }
+        }
+        if (nw < W && acc[nw] != 0) ++nw;
+    }
+    const int lb = R.logn < 13 ? R.logn : 13, le = R.logn - lb;
+    const int jj = ((j & ((1 << lb) - 1)) << le) | (j >> lb);
+    u32* out = digits + ct * D * R.n + jj;
+    constexpr int DMAX = (64 * W + 19) / 20;
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) {
+        if (d >= D) break;
+        const int off = 20 * d;
+        const int wi = off >> 6, sh = off & 63;
+        u64 v = acc[wi] >> sh;
+        if (sh > 44 && wi + 1 < W) v |= acc[wi + 1] << (64 - sh);
+        out[static_cast<long long>(d) * R.n] = static_cast<u32>(v & 0xFFFFFu);
+    }
+}
+
 __device__ __forceinline__ u64 lift_digit(u32 v, u64 q) { return v < q ? v : v % q; }
 
 // ---- tensor memory / bulk-copy helpers: ks_saddr / ks_mbar_wait / ks_bulk_load (ntt_core.cuh)
@@ -1093,6 +1160,26 @@ void crt_digits(const DevRing& R, const u64* d2, u32* digits, int level, int D, 
     const long long total = static_cast<long long>(count) * R.n;
     const unsigned grid = static_cast<unsigned>((total + 127) / 128);
     const int W = R.crt_words;
+#ifndef HECNN_CRT_GARNER
+#define HECNN_CRT_GARNER 1
+#endif
+    const unsigned long long lmask = level + 1 >= 64 ? ~0ull : (1ull << (level + 1)) - 1;
+    if (HECNN_CRT_GARNER && R.garner_inv && (R.int_limbs & lmask) == 1) {
+        const int smem = 128 * (level + 1) * 8;
+#define HECNN_CRT_CASE(WW) \
+    case WW: smem_opt_in(k_crt_digits_garner<WW>, smem); L.begin("k_crt_digits", double(count) * R.n * (level + 1) * (WW + 1), double(count) * R.n * ((level + 1) * 8 + D * 4)); k_crt_digits_garner<WW><<<grid, 128, smem, L.stream>>>(R, d2, digits, level, D, static_cast<long long>(count)); break;
+        switch (W) {
+            HECNN_CRT_CASE(2) HECNN_CRT_CASE(3) HECNN_CRT_CASE(4) HECNN_CRT_CASE(5) HECNN_CRT_CASE(6) HECNN_CRT_CASE(7)
+            HECNN_CRT_CASE(8) HECNN_CRT_CASE(9) HECNN_CRT_CASE(10) HECNN_CRT_CASE(11) HECNN_CRT_CASE(12)
+            HECNN_CRT_CASE(13) HECNN_CRT_CASE(14) HECNN_CRT_CASE(15) HECNN_CRT_CASE(16) HECNN_CRT_CASE(17)
+            HECNN_CRT_CASE(18) HECNN_CRT_CASE(19) HECNN_CRT_CASE(20)
+            default: throw std::invalid_argument("key_switch: modulus chain too long for the device CRT kernel");
+        }
+#undef HECNN_CRT_CASE
+        L.count();
+        check_launch("crt_digits");
+        return;
+    }
 #define HECNN_CRT_CASE(WW) \
     case WW: L.begin("k_crt_digits", double(count) * R.n * (level + 1) * (WW + 1), double(count) * R.n * ((level + 1) * 8 + D * 4)); k_crt_digits<WW><<<grid, 128, 0, L.stream>>>(R, d2, digits, level, D, static_cast<long long>(count)); break;
     switch (W) {
