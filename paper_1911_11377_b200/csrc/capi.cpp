@@ -61,8 +61,10 @@ const Tensor& T(const hecnn_tensor* t) {
     if (!t || !t->t) throw std::invalid_argument("null tensor");
     return *t->t;
 }
-Tensor& TM(hecnn_tensor* t) {
+// a tensor modified in place must live in the context the call names
+Tensor& TM(hecnn_context* c, hecnn_tensor* t) {
     if (!t || !t->t) throw std::invalid_argument("null tensor");
+    if (!c || t->t->ctx != c->ctx.get()) throw std::invalid_argument("tensor belongs to another context");
     return *t->t;
 }
 std::shared_ptr<Context> owner(hecnn_context* c) { return c->ctx; }
@@ -500,17 +502,17 @@ int hecnn_ct_zero(hecnn_context* ctx, size_t cells, uint32_t level, double scale
     return guard([&] { *out = wrap(ctx, ct_zero(C(ctx), cells, level, scale)); });
 }
 int hecnn_ct_add_inplace(hecnn_context* ctx, hecnn_tensor* acc, const hecnn_tensor* x) {
-    return guard([&] { ct_add_inplace(C(ctx), TM(acc), T(x)); });
+    return guard([&] { ct_add_inplace(C(ctx), TM(ctx, acc), T(x)); });
 }
 int hecnn_ct_scalar_mac(hecnn_context* ctx, hecnn_tensor* acc, const hecnn_tensor* x, const uint64_t* residues,
                         size_t ncs, double sp_scale, uint32_t sp_level) {
     return guard([&] {
         if (!residues) throw std::invalid_argument("mul_scalar_mac: null residues");
-        ct_scalar_mac(C(ctx), TM(acc), T(x), residues, ncs, sp_scale, sp_level);
+        ct_scalar_mac(C(ctx), TM(ctx, acc), T(x), residues, ncs, sp_scale, sp_level);
     });
 }
 int hecnn_ct_add_scalar(hecnn_context* ctx, hecnn_tensor* ct, double c) {
-    return guard([&] { ct_add_scalar(C(ctx), TM(ct), c); });
+    return guard([&] { ct_add_scalar(C(ctx), TM(ctx, ct), c); });
 }
 int hecnn_ct_add_plain(hecnn_context* ctx, const hecnn_tensor* x, const uint64_t* pt, uint32_t pt_level,
                        double pt_scale, hecnn_tensor** out) {
