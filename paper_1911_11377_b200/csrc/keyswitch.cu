@@ -169,6 +169,8 @@ __global__ void __launch_bounds__(128) k_crt_digits_garner(DevRing R, const u64*
     for (int i = level - 1; i >= 0; --i) {
         const u64 qi = R.mod[i].q;
         u64 carry = i ? sv[i * T + tid] : v0;
+        bool grow = false;
+        // compile-time word indices only (a runtime acc[nw] would put acc[] in local memory)
 #pragma unroll
         for (int w = 0; w < W; ++w) {
             if (w < nw) {
@@ -179,9 +181,10 @@ __global__ void __launch_bounds__(128) k_crt_digits_garner(DevRing R, const u64*
                 carry = hi;
             } else if (w == nw) {
                 acc[w] = carry;
+                grow = carry != 0;
             }
         }
-        if (nw < W && acc[nw] != 0) ++nw;
+        nw += grow;
     }
     const int lb = R.logn < 13 ? R.logn : 13, le = R.logn - lb;
     const int jj = ((j & ((1 << lb) - 1)) << le) | (j >> lb);
@@ -923,8 +926,11 @@ __device__ __forceinline__ u64 aux_crt_value(const DevRing& R, const u64 (&res)[
         f += static_cast<double>(y) * R.inv_q[1 + a];
         acc = add_mod(acc, mul_shoup(y, R.aux_Mq0[a].x, R.aux_Mq0[a].y, q0), q0);
     }
-    const int k = static_cast<int>(rint(f));
-    return sub_mod(acc, R.aux_kPq0[k], q0);
+    const int k = static_cast<int>(rint(f));  // 0..3
+    // (selects, not a runtime index into the kernel-parameter array, which would
+    // copy DevRing to the stack)
+    const u64 kp = k == 0 ? 0 : (k == 1 ? R.aux_kPq0[1] : (k == 2 ? R.aux_kPq0[2] : R.aux_kPq0[3]));
+    return sub_mod(acc, kp, q0);
 }
 
 // CRT of each coefficient fused into the first round of the forward NTT mod
@@ -980,7 +986,7 @@ __global__ void k_limb0_combine(DevRing R, u64* __restrict__ acc01, const u64* _
 // acc01 gets the tensor product's (d0, d1) only, and e0 [ct * 2 + comp][n]
 // receives E mod q0 as coefficients, to be added after the caller's INTT --
 // NTT_q0 followed by INTT_q0 of E cancels, so neither runs
-__global__ void k_limb0_crt_combine(DevRing R, u64* __restrict__ acc01, const u64* __restrict__ aux_out,
+__global__ void __launch_bounds__(256, 4) k_limb0_crt_combine(DevRing R, u64* __restrict__ acc01, const u64* __restrict__ aux_out,
                                     u64* __restrict__ e0, const u64* __restrict__ fy, int limbs, int mode,
                                     long long count) {
     // two consecutive coefficients per thread (16-byte accesses); the four CRT
