@@ -983,6 +983,8 @@ class CkksEngine:
         sps = [sp] if isinstance(sp, ScalarPlain) else list(sp)
         if not sps:
             raise ValueError("mul_scalar_mac: no scalar")
+        if any(q.scale != sps[0].scale or q.level != sps[0].level for q in sps):
+            raise ValueError("mul_scalar_mac: per-cell scalars must share one scale and level")
         r = np.ascontiguousarray(np.stack([q.residues for q in sps]), dtype=np.uint64)
         _check(lib().hecnn_ct_scalar_mac(self.ctx, acc.handle, x.handle, _ptr(r), ctypes.c_size_t(len(sps)),
                                          ctypes.c_double(sps[0].scale), ctypes.c_uint32(sps[0].level)))
